@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py -- field multiply-adds per second of the B200 bitsliced M4RM product.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on
+rank 0.  N > 1 runs under torch.distributed.run (one rank per GPU, NCCL).
+
+Metric (BASELINE.json): field mul-adds/s = m*l*n / t for C = A B, with the fraction of the
+binding roofline (LOP3 integer-logic issue or shared-memory bandwidth).
+Workload (N=1): BASELINE.json configs[1], F5 4096x4096x4096, k=8; the other configs are
+reported under "per_config".  A step is one C = A B of the workload on inputs resident in
+HBM; with N GPUs every rank multiplies its own 4096-row (configs' m-row) slab of A by B,
+which rank 0 broadcasts over NCCL inside the step (weak scaling: per-GPU work fixed).
+L2 is flushed (256 MiB write) before every timed step; device time with CUDA events, summed
+over K steps, max over ranks.
+
+`--impl reference` times the reference's CPU path -- the oracle port of it (oracle/, C with
+pthreads on all host cores; the reference itself is Python and does not travel to the box)
+-- on a bounded row sample of the same workload, extrapolated to the full product.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# (name, field, m, l, n): BASELINE.json configs 0..4
+CONFIGS = [
+    ("F3 1024x1024x1024 k=8", "f3", 1024, 1024, 1024),
+    ("F5 4096x4096x4096 k=8", "f5", 4096, 4096, 4096),
+    ("GF(4) 8192x8192x8192 k=8", "gf4", 8192, 8192, 8192),
+    ("F7 16384x8192x16384 k=8", "f7", 16384, 8192, 16384),
+    ("F3 32768x32768x32768 k=8", "f3", 32768, 32768, 32768),
+]
+HEADLINE = 1
+METRIC = "field mul-adds/sec (m*l*n/t) for C=A*B over F3/F5/F7/GF(4), % of roofline"
+UNIT = "mul-adds/s"
+
+# Algorithmic work per field mul-add for the accumulate phase: LOP3 count of
+# the reference formulas and shared-memory table bytes; plus the table build once per GPU.
+LOP3_PER_MULADD = {"f2": 1 / 256, "f3": 9 / 256, "f5": 42 / 256, "f7": 32 / 256, "gf4": 3 / 256}
+SMEM_PER_MULADD = {"f2": 4 / 256, "f3": 16 / 256, "f5": 36 / 256, "f7": 36 / 256, "gf4": 16 / 256}
+TABLE_LOP3_PER_WORD = {"f2": 1, "f3": 5, "f5": 12, "f7": 10, "gf4": 2}  # one field add, 32-bit word
+PLANES = {"f2": 1, "f3": 2, "f5": 3, "f7": 3, "gf4": 2}
+ORDER = {"f2": 2, "f3": 3, "f5": 5, "f7": 7, "gf4": 4}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- our arm
+def make_inputs(field, m, l, n, rank, device, with_b):
+    import torch
+    import paper_0901_1413_b200 as sg
+    f = sg.by_name(field)
+    g = torch.Generator(device=device)
+    g.manual_seed(1000 + rank)
+    A = torch.randint(0, ORDER[field], (m, l), dtype=torch.uint8, device=device, generator=g)
+    Am = sg.BitslicedMatrix.from_dense(f, A, device=device)
+    del A
+    if with_b:
+        g.manual_seed(1)
+        B = torch.randint(0, ORDER[field], (l, n), dtype=torch.uint8, device=device, generator=g)
+        Bm = sg.BitslicedMatrix.from_dense(f, B, device=device)
+        del B
+    else:
+        Bm = sg.BitslicedMatrix.zero(f, l, n, device=device)
+    return f, Am, Bm
+
+
+def run_config(cfg, args, world, rank, device, peaks, e2e=False):
+    import torch
+    import torch.distributed as dist
+    import paper_0901_1413_b200 as sg
+    from paper_0901_1413_b200 import m4rm as M
+
+    name, field, m, l, n = cfg
+    f, A, B = make_inputs(field, m, l, n, rank, device, with_b=(rank == 0))
+    C = sg.BitslicedMatrix.zero(f, m, n, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    params = sg.M4rmParams(8)
+
+    def step():
+        if world > 1:
+            dist.broadcast(B.planes, src=0)
+        sg.m4rm_multiply(A, B, params, out=C)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = M.launch_count()
+    with ClockSampler(device.index or 0) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # evict L2 (126 MB) between timed steps; untimed
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    launches = M.launch_count() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    work = float(m) * l * n
+    value = world * work / (ms_per_step * 1e-3)
+
+    # dominant-kernel duration (events around each internal launch, on the launching stream)
+    M.set_timing(True)
+    kern, tr, red = [], [], []
+    for i in range(max(3, min(args.steps, 10))):
+        flush.fill_(i & 0xFF)
+        sg.m4rm_multiply(A, B, params, out=C)
+        lt = M.last_timing()
+        kern.append(lt["m4rm_ms"]); tr.append(lt["transpose_ms"]); red.append(lt["reduce_ms"])
+    M.set_timing(False)
+    k_ms = statistics.median(kern)
+    plan = sg.plan(f, m, l, n, 8)
+
+    # roofline of the M4RM kernel: min over the LOP3 and LDS rooflines
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    clk_hz = peaks["clock_mhz_for_peak"] * 1e6
+    p_lop3 = peaks["lop3_per_clk_per_sm"] * sms * clk_hz
+    p_smem = peaks["lds_bytes_per_clk_per_sm"] * sms * clk_hz
+    words32 = 2 * ((n + 63) // 64)
+    table_lop3 = (l / 8.0) * 255 * words32 * TABLE_LOP3_PER_WORD[field]
+    lop3 = work * LOP3_PER_MULADD[field] + table_lop3
+    smem = work * SMEM_PER_MULADD[field]
+    lop3_bound, smem_bound = lop3 / p_lop3, smem / p_smem
+    bound = "lop3" if lop3_bound >= smem_bound else "smem"
+    if bound == "lop3":
+        roof = {"bound": "lop3 (integer-logic pipe)", "achieved": lop3 / (k_ms * 1e-3) / 1e12, "peak": p_lop3 / 1e12,
+                "unit": "TLOP3/s"}
+    else:
+        roof = {"bound": "smem (LDS bandwidth)", "achieved": smem / (k_ms * 1e-3) / 1e12, "peak": p_smem / 1e12,
+                "unit": "TB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel_ms"] = k_ms
+    roof["kernel_share_of_step"] = k_ms / ms_per_step if world == 1 else None
+    roof["achieved_muladds_per_s"] = work / (k_ms * 1e-3)
+    roof["roofline_muladds_per_s"] = work / max(lop3_bound, smem_bound)
+    roof["peak_source"] = ("sg_probe_peaks on this GPU: %.1f LOP3/clk/SM, %.1f LDS B/clk/SM, x %d SMs x %.0f MHz (%s)"
+                           % (peaks["lop3_per_clk_per_sm"], peaks["lds_bytes_per_clk_per_sm"], sms,
+                              peaks["clock_mhz_for_peak"], peaks["clock_note"]))
+    out = {"value": value, "ms_per_step": ms_per_step, "gpu_launches": launches, "clocks": clk.summary(),
+           "roofline": roof, "plan": plan, "transpose_ms": statistics.median(tr), "reduce_ms": statistics.median(red)}
+
+    if e2e:
+        out["e2e"] = run_e2e(f, A, B, m, l, n, args, world, device)
+    del A, B, C, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_e2e(f, A, B, m, l, n, args, world, device):
+    """Same metric through the reference-facing host-buffer call sg_m4rm_host (pinned memory)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+    from paper_0901_1413_b200 import _lib
+
+    L = _lib.load()
+    Ah = A.planes.cpu().pin_memory()
+    Bh = B.planes.cpu().pin_memory()
+    Ch = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64).pin_memory()
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    dev = device.index or 0
+    for _ in range(max(1, args.warmup)):
+        _lib.check(L.sg_m4rm_host(f.code, vp(Ah), vp(Bh), vp(Ch), m, l, n, 8, dev))
+    if world > 1:
+        dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _lib.check(L.sg_m4rm_host(f.code, vp(Ah), vp(Bh), vp(Ch), m, l, n, 8, dev))
+        times.append(time.perf_counter() - t0)
+    total = torch.tensor([sum(times)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    per = float(total.item()) / args.steps
+    return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
+            "h2d_bytes_per_step": int(Ah.numel() * 8 + Bh.numel() * 8), "d2h_bytes_per_step": int(Ch.numel() * 8),
+            "path": "sg_m4rm_host (C ABI, pinned host planes, H2D + multiply + D2H, synchronous)"}
+
+
+# ----------------------------------------------------------------------------- CPU (oracle port)
+def cpu_estimate(field, m, l, n, sample_rows, threads):
+    """Time the restated reference path (oracle/, C + pthreads) on a row sample and extrapolate.
+
+    Each of `threads` workers builds every k-block table (as the reference's row-partition
+    contract does) and processes rows_per_thread rows.  Two sample sizes give the
+    table-build time a and the per-row time b; the full product costs a + b * ceil(m / threads).
+    """
+    import numpy as np
+
+    import oracle
+    rng = np.random.default_rng(0)
+    rows = max(threads * sample_rows, threads)
+    A = rng.integers(0, ORDER[field], size=(rows, l), dtype=np.uint8)
+    B = rng.integers(0, ORDER[field], size=(l, n), dtype=np.uint8)
+    Ap, Bp = oracle.pack(field, A), oracle.pack(field, B)
+
+    def run(r_per_thread):
+        rr = r_per_thread * threads
+        t0 = time.perf_counter()
+        oracle.m4rm(field, Ap[:, :rr], Bp, l, n, 8, threads=threads, canonical=False)
+        return time.perf_counter() - t0
+
+    t1 = min(run(1) for _ in range(2))
+    ts = min(run(sample_rows) for _ in range(2)) if sample_rows > 1 else t1
+    b = max((ts - t1) / max(sample_rows - 1, 1), 1e-9)
+    a = max(t1 - b, 0.0)
+    full = a + b * -(-m // threads)
+    return {"value": float(m) * l * n / full, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"oracle/sg_oracle.c M4RM (restated reference path, k=8) on {threads} threads: full table "
+                       f"builds for all {-(-l // 8)} k-blocks of a {l}x{n} B, with 1 and {sample_rows} A rows per thread "
+                       f"(best of 2 each: {t1:.3f} s, {ts:.3f} s); extrapolated linearly to {m} rows"),
+            "est_seconds_full": full}
+
+
+def cpu_sample_rows(field, l, n, threads, budget_s=8.0):
+    """Pick rows per thread so one sample run takes roughly budget_s (per-row cost model)."""
+    ops_per_row = (l / 8.0) * (n / 64.0) * {"f2": 2, "f3": 14, "f5": 80, "f7": 60, "gf4": 8}[field]
+    rate = 1.5e9  # 64-bit word-ops per second per core, rough
+    table_s = (l / 8.0) * 255 * (n / 64.0) * {"f2": 2, "f3": 8, "f5": 24, "f7": 20, "gf4": 3}[field] / rate
+    r = int(max(2, (budget_s - table_s) / max(ops_per_row / rate, 1e-9)))
+    return min(r, 512)
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    name, field, m, l, n = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    sample = cpu_sample_rows(field, l, n, threads, budget_s=max(2.0, 60.0 / max(args.steps + args.warmup, 1)))
+    for _ in range(args.warmup):
+        cpu_estimate(field, m, l, n, 1, threads)
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_estimate(field, m, l, n, sample, threads)
+        vals.append(last["value"])
+    value = statistics.median(vals)
+    ms = float(m) * l * n / value * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (bitsliced boolean words)", "data": "synthetic",
+            "config": {"workload": name, "field": field, "m": m, "l": l, "n": n, "k": 8,
+                       "parallelism": f"{threads} host threads, rows sharded"},
+            "cpu_baseline": {**last, "value": value},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=HEADLINE, help="index into BASELINE.json configs")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        sys.exit(run_reference(args, world, rank))
+
+    import torch
+    import torch.distributed as dist
+    from paper_0901_1413_b200 import m4rm as M
+
+    if args.warmup < 3:
+        log("warning: the contract needs >= 3 warm-up steps; using 3")
+        args.warmup = 3
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+
+    pk = M.probe_peaks(local)
+    peaks = {"lop3_per_clk_per_sm": pk["lop3_per_clk_per_sm"], "lds_bytes_per_clk_per_sm": pk["lds_bytes_per_clk_per_sm"],
+             "probe_sm_mhz": pk["sm_mhz"], "clock_mhz_for_peak": 1965.0,
+             "clock_note": "max SM clock, conservative; probe ran at %.0f MHz" % pk["sm_mhz"]}
+
+    head = CONFIGS[args.config]
+    res = run_config(head, args, world, rank, device, peaks, e2e=True)
+    per_config = {}
+    if not args.no_per_config:
+        for i, cfg in enumerate(CONFIGS):
+            if i == args.config:
+                continue
+            r = run_config(cfg, args, world, rank, device, peaks, e2e=False)
+            per_config[cfg[0]] = {"value": r["value"], "ms_per_step": r["ms_per_step"],
+                                  "roofline_frac": r["roofline"]["frac"], "bound": r["roofline"]["bound"],
+                                  "kernel_ms": r["roofline"]["kernel_ms"],
+                                  "achieved_muladds_per_s": r["roofline"]["achieved_muladds_per_s"],
+                                  "plan": r["plan"], "clocks": r["clocks"]}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        name, field, m, l, n = head
+        threads = os.cpu_count() or 1
+        cpu = cpu_estimate(field, m, l, n, cpu_sample_rows(field, l, n, threads, budget_s=10.0), threads)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        name, field, m, l, n = head
+        line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bitsliced boolean words)",
+                "data": "synthetic (seeded uniform residues, torch.randint on device)",
+                "config": {"workload": name, "field": field, "m_per_gpu": m, "l": l, "n": n, "k": 8,
+                           "parallelism": (f"rows of A/C sharded over {world} GPUs, B broadcast from rank 0 by NCCL "
+                                           "inside every step" if world > 1 else "1 GPU"),
+                           "l2": "flushed (256 MiB write) before every timed step"},
+                "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+                "roofline": res["roofline"], "plan": res["plan"], "cpu_baseline": cpu,
+                "peaks_probe": peaks, "per_config": per_config}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

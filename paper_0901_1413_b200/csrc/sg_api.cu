@@ -1,0 +1,499 @@
+// sg_api.cu -- the C ABI (include/slicegemm_b200.h): argument checks, the launch planner,
+// workspace management, the host-buffer entry point, timing and launch accounting.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+
+#include "../../include/slicegemm_b200.h"
+#include "sg_field.cuh"
+#include "sg_internal.h"
+
+using namespace sg;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+int g_override_rt = 0, g_override_splits = 0;
+bool g_timing = false;
+double g_last_ms[3] = {0, 0, 0};
+std::mutex g_mu;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define SG_CUDA(call, where)                        \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+bool valid_field(int f) { return f >= SG_F2 && f <= SG_GF4; }
+int planes(int f) { return f == SG_F2 ? 1 : (f == SG_F5 || f == SG_F7) ? 3 : 2; }
+int64_t w64_of(int64_t n) { return (n + 63) / 64; }
+
+// ---------------------------------------------------------------- per-device state
+struct DevState {
+  bool attrs_set = false;
+  int sms = 148;
+};
+std::map<int, DevState> g_dev;
+
+DevState& dev_state(int device) {
+  DevState& d = g_dev[device];
+  if (!d.attrs_set) {
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device);
+    for (int i = 0; i < m4rm_kernel_count(); ++i) {
+      KernelInfo* k = m4rm_kernel_at(i);
+      cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, k->fn) == cudaSuccess) k->regs = fa.numRegs;
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->threads, k->smem_bytes);
+      k->occupancy = occ;
+    }
+    cudaGetLastError();
+    d.attrs_set = true;
+  }
+  return d;
+}
+
+// Workspace cache keyed by (device, stream): stream-ordered reuse is safe, cross-stream is not.
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+std::map<std::pair<int, cudaStream_t>, Buf> g_ws;
+std::map<int, int*> g_flags;  // per-device error flag for pack / unpack
+
+int* flag_for(int device, cudaError_t* err) {
+  int*& f = g_flags[device];
+  *err = cudaSuccess;
+  if (!f) *err = cudaMalloc(&f, 16);
+  return *err == cudaSuccess ? f : nullptr;
+}
+
+void* workspace_for(int device, cudaStream_t st, size_t bytes, cudaError_t* err) {
+  Buf& b = g_ws[{device, st}];
+  *err = cudaSuccess;
+  if (b.bytes < bytes) {
+    if (b.p) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.p);
+    }
+    b.p = nullptr;
+    b.bytes = 0;
+    *err = cudaMalloc(&b.p, bytes);
+    if (*err != cudaSuccess) return nullptr;
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+// ---------------------------------------------------------------- planner
+struct Plan {
+  KernelInfo* ki = nullptr;
+  int kernel_index = -1;
+  int K = 8, splits = 1, bps = 0, nblocks = 0;
+  int64_t mpad = 0;
+  int wa32 = 0, wc32 = 0;
+  dim3 grid;
+  double est_clk = 0;
+};
+
+// Per-lane (4 words) ALU instructions and shared-memory bytes per (row, k-block), and the
+// table-build ALU work per entry; see DESIGN.md "Planner".
+void field_costs(int f, double* lane_alu, double* lane_smem, double* entry_alu) {
+  switch (f) {
+    case SG_F2: *lane_alu = 4 + 3; *lane_smem = 16 + 4; *entry_alu = 4 + 8; break;
+    case SG_F3: *lane_alu = 36 + 6; *lane_smem = 64 + 8; *entry_alu = 20 + 16; break;
+    case SG_GF4: *lane_alu = 12 + 6; *lane_smem = 64 + 8; *entry_alu = 8 + 16; break;
+    case SG_F5: *lane_alu = 168 + 9; *lane_smem = 144 + 12; *entry_alu = 48 + 24; break;
+    default: *lane_alu = 128 + 9; *lane_smem = 144 + 12; *entry_alu = 40 + 24; break;
+  }
+}
+
+int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Plan* out) {
+  DevState& ds = dev_state(device);
+  const int K = std::min(k, 8);
+  const int64_t wc32 = 2 * w64_of(n), wa32 = 2 * w64_of(l);
+  const int nblocks = (int)((l + K - 1) / K);
+  const int64_t slabs = (wc32 + SLAB_WORDS - 1) / SLAB_WORDS;
+  double lane_alu, lane_smem, entry_alu;
+  field_costs(field, &lane_alu, &lane_smem, &entry_alu);
+  const int R = planes(field);
+  Plan best;
+  best.est_clk = 1e300;
+  for (int i = 0; i < m4rm_kernel_count(); ++i) {
+    KernelInfo* ki = m4rm_kernel_at(i);
+    if (ki->field != field || ki->k != K) continue;
+    if (g_override_rt && ki->rt != g_override_rt) continue;
+    const int rows = ki->rt * ki->threads;
+    const int64_t rgroups = (m + rows - 1) / rows;
+    const double E = (double)(1 << K);
+    const double alu = (rows * lane_alu + E * entry_alu) / 64.0;
+    const double smem = (rows * lane_smem + E * R * ENTRY_BYTES + rows * R * 4.0) / 128.0;
+    const double t_block = std::max(alu, smem) + 350.0;
+    const int occ = std::max(1, ki->occupancy);
+    const int max_splits = std::max(1, std::min(nblocks, 64));
+    for (int sp = 1; sp <= max_splits; ++sp) {
+      if (g_override_splits && sp != g_override_splits) continue;
+      const int bps = (nblocks + sp - 1) / sp;
+      const int splits = (nblocks + bps - 1) / bps;
+      if (splits != sp) continue;
+      const double ctas = (double)slabs * rgroups * splits;
+      const double t_cta = bps * t_block + 3000.0;
+      const double waves = std::ceil(ctas / (ds.sms * occ));
+      double est = waves * t_cta * std::min<double>(occ, ctas / ds.sms > 1 ? occ : 1);
+      if (splits > 1) {
+        const double bytes = (splits + 1.0) * R * (double)m * wc32 * 4.0;
+        est += bytes / 3000.0 + 8000.0;  // ~3 KB/clk HBM + one extra launch
+      }
+      if (est < best.est_clk) {
+        best.est_clk = est;
+        best.ki = ki;
+        best.kernel_index = i;
+        best.splits = splits;
+        best.bps = bps;
+        best.mpad = rgroups * rows;
+        best.grid = dim3((unsigned)slabs, (unsigned)rgroups, (unsigned)splits);
+      }
+    }
+  }
+  if (!best.ki) return fail(SG_EUNSUPPORTED, "no compiled M4RM kernel matches the request (check sg_set_plan_override)");
+  best.K = K;
+  best.nblocks = nblocks;
+  best.wa32 = (int)wa32;
+  best.wc32 = (int)wc32;
+  if (best.grid.y > 65535) return fail(SG_EUNSUPPORTED, "too many row groups for one launch");
+  *out = best;
+  return SG_OK;
+}
+
+int64_t workspace_bytes_for(const Plan& p, int field) {
+  const int R = planes(field);
+  int64_t b = (int64_t)R * p.wa32 * p.mpad * 4;
+  b = (b + 255) / 256 * 256;
+  if (p.splits > 1) b += (int64_t)p.splits * R * p.mpad * p.wc32 * 4;
+  return std::max<int64_t>(b, 256);
+}
+
+int check_mul_args(int field, const void* A, const void* B, const void* C, int64_t m, int64_t l,
+                   int64_t n, int k) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (m < 0 || l < 0 || n < 0) return fail(SG_EINVAL, "negative dimension");
+  if (k < 1 || k > 16) return fail(SG_EINVAL, "k must be in 1..16 (SPEC.md:306-311)");
+  if (2 * w64_of(l) > 0x7fffffffLL || 2 * w64_of(n) > 0x7fffffffLL) return fail(SG_EINVAL, "dimension too large");
+  if (m && n && (!C || (l && (!A || !B)))) return fail(SG_EINVAL, "null matrix pointer");
+  return SG_OK;
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+int sg_abi_version(void) { return SG_ABI_VERSION; }
+const char* sg_last_error(void) { return g_err.c_str(); }
+int sg_field_planes(int field) { return valid_field(field) ? planes(field) : -1; }
+int64_t sg_launch_count(void) { return g_launches.load(); }
+
+int sg_set_plan_override(int rows_per_thread, int splits) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_override_rt = rows_per_thread;
+  g_override_splits = splits;
+  return SG_OK;
+}
+
+int sg_set_timing(int enable) {
+  g_timing = enable != 0;
+  return SG_OK;
+}
+
+int sg_last_timing(double* t, double* mm, double* r) {
+  if (t) *t = g_last_ms[0];
+  if (mm) *mm = g_last_ms[1];
+  if (r) *r = g_last_ms[2];
+  return SG_OK;
+}
+
+int sg_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld, uint64_t* planes_out,
+            void* stream) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (m < 0 || n < 0 || ld < n) return fail(SG_EINVAL, "bad shape or leading dimension");
+  if (m == 0 || n == 0) return SG_OK;
+  if (!dense || !planes_out) return fail(SG_EINVAL, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e;
+  int* flag = flag_for(dev, &e);
+  if (!flag) return cuda_fail(e, "sg_pack flag");
+  SG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st), "sg_pack");
+  SG_CUDA(launch_pack(field, dense, m, n, ld, planes_out, flag, st), "sg_pack launch");
+  g_launches++;
+  int h = 0;
+  SG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "sg_pack");
+  SG_CUDA(cudaStreamSynchronize(st), "sg_pack");
+  if (h) return fail(SG_ERANGE, "entries out of range for the field");
+  return SG_OK;
+}
+
+int sg_unpack(int field, const uint64_t* planes_in, int64_t m, int64_t n, uint8_t* dense, int64_t ld,
+              void* stream) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (m < 0 || n < 0 || ld < n) return fail(SG_EINVAL, "bad shape or leading dimension");
+  if (m == 0 || n == 0) return SG_OK;
+  if (!dense || !planes_in) return fail(SG_EINVAL, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e;
+  int* flag = flag_for(dev, &e);
+  if (!flag) return cuda_fail(e, "sg_unpack flag");
+  SG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st), "sg_unpack");
+  SG_CUDA(launch_unpack(field, planes_in, m, n, dense, ld, flag, st), "sg_unpack launch");
+  g_launches++;
+  int h = 0;
+  SG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "sg_unpack");
+  SG_CUDA(cudaStreamSynchronize(st), "sg_unpack");
+  if (h) return fail(SG_EPATTERN, "illegal F3 pattern (sign without unit) in planes");
+  return SG_OK;
+}
+
+int sg_reduce_canonical(int field, uint64_t* p, int64_t rows, int64_t n, void* stream) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (rows < 0 || n < 0) return fail(SG_EINVAL, "negative dimension");
+  if (rows == 0 || n == 0 || (field != SG_F5 && field != SG_F7)) return SG_OK;
+  if (!p) return fail(SG_EINVAL, "null pointer");
+  SG_CUDA(launch_canonicalize(field, p, rows, w64_of(n), (cudaStream_t)stream), "sg_reduce_canonical");
+  g_launches++;
+  return SG_OK;
+}
+
+static int op_plane_count(int op) {
+  switch (op) {
+    case SG_OP_F2_ADD: return 1;
+    case SG_OP_F3_ADD: case SG_OP_F3_SUB: case SG_OP_F3_NEG: case SG_OP_GF4_ADD: case SG_OP_GF4_MULX:
+    case SG_OP_SCALAR_MUL_F3: case SG_OP_SCALAR_MUL_GF4: return 2;
+    default: return 3;
+  }
+}
+
+static bool fill_planes(Planes* out, const uint64_t* const* arr, int R) {
+  out->p[0] = out->p[1] = out->p[2] = nullptr;
+  if (!arr) return false;
+  for (int d = 0; d < R; ++d) {
+    if (!arr[d]) return false;
+    out->p[d] = const_cast<uint64_t*>(arr[d]);
+  }
+  return true;
+}
+
+int sg_plane_op(int op, uint64_t* const* dst, const uint64_t* const* src, int64_t rows, int64_t words,
+                uint64_t tail, int scalar, void* stream) {
+  if (op < SG_OP_F2_ADD || op > SG_OP_SCALAR_MUL_GF4) return fail(SG_EINVAL, "unknown plane op");
+  if (rows < 0 || words < 0) return fail(SG_EINVAL, "negative dimension");
+  if (rows == 0 || words == 0) return SG_OK;
+  const bool unary = op == SG_OP_F3_NEG || op == SG_OP_F5_NEG || op == SG_OP_F5_DOUBLE ||
+                     op == SG_OP_F5_REDUCE || op == SG_OP_F7_NEG || op == SG_OP_F7_DOUBLE ||
+                     op == SG_OP_F7_REDUCE || op == SG_OP_GF4_MULX || op >= SG_OP_SCALAR_MUL_F3;
+  const int R = op_plane_count(op);
+  Planes d, s;
+  if (!fill_planes(&d, (const uint64_t* const*)dst, R)) return fail(SG_EINVAL, "null dst plane");
+  if (!unary && !fill_planes(&s, src, op == SG_OP_F5_FOLD5 ? 1 : R)) return fail(SG_EINVAL, "null src plane");
+  if (unary) s.p[0] = s.p[1] = s.p[2] = nullptr;
+  SG_CUDA(launch_plane_op(op, d, s, rows, words, tail, scalar, (cudaStream_t)stream), "sg_plane_op");
+  g_launches++;
+  return SG_OK;
+}
+
+int64_t sg_m4rm_workspace_bytes(int field, int64_t m, int64_t l, int64_t n, int k) {
+  if (check_mul_args(field, (void*)1, (void*)1, (void*)1, m, l, n, k) != SG_OK) return -1;
+  if (m == 0 || n == 0 || l == 0) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  Plan p;
+  if (make_plan(field, m, l, n, k, dev, &p) != SG_OK) return -1;
+  return workspace_bytes_for(p, field);
+}
+
+int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta, int* splits, int* ctas,
+            int* kernel_index) {
+  int rc = check_mul_args(field, (void*)1, (void*)1, (void*)1, m, l, n, k);
+  if (rc != SG_OK) return rc;
+  if (m == 0 || n == 0 || l == 0) return fail(SG_EINVAL, "empty product has no plan");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  Plan p;
+  rc = make_plan(field, m, l, n, k, dev, &p);
+  if (rc != SG_OK) return rc;
+  if (rows_per_cta) *rows_per_cta = p.ki->rt * p.ki->threads;
+  if (splits) *splits = p.splits;
+  if (ctas) *ctas = (int)(p.grid.x * p.grid.y * p.grid.z);
+  if (kernel_index) *kernel_index = p.kernel_index;
+  return SG_OK;
+}
+
+int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
+            int k, void* workspace, int64_t workspace_bytes, void* stream) {
+  int rc = check_mul_args(field, A, B, C, m, l, n, k);
+  if (rc != SG_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int R = planes(field);
+  if (m == 0 || n == 0) return SG_OK;
+  if (l == 0) {  // empty inner dimension: C = 0
+    SG_CUDA(cudaMemsetAsync(C, 0, (size_t)R * m * w64_of(n) * 8, st), "sg_m4rm zero");
+    return SG_OK;
+  }
+  int dev = 0;
+  SG_CUDA(cudaGetDevice(&dev), "sg_m4rm");
+  std::lock_guard<std::mutex> lk(g_mu);
+  Plan p;
+  rc = make_plan(field, m, l, n, k, dev, &p);
+  if (rc != SG_OK) return rc;
+  const int64_t need = workspace_bytes_for(p, field);
+  char* ws = (char*)workspace;
+  if (ws) {
+    if (workspace_bytes < need) return fail(SG_EINVAL, "workspace too small (see sg_m4rm_workspace_bytes)");
+  } else {
+    cudaError_t e;
+    ws = (char*)workspace_for(dev, st, (size_t)need, &e);
+    if (!ws) return cuda_fail(e, "sg_m4rm workspace");
+  }
+  uint32_t* AT = (uint32_t*)ws;
+  int64_t at_bytes = ((int64_t)R * p.wa32 * p.mpad * 4 + 255) / 256 * 256;
+  uint32_t* partial = p.splits > 1 ? (uint32_t*)(ws + at_bytes) : nullptr;
+
+  cudaEvent_t ev[4];
+  if (g_timing)
+    for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
+  if (g_timing) cudaEventRecord(ev[0], st);
+  SG_CUDA(launch_transpose_a(field, (const uint32_t*)A, AT, m, p.mpad, p.wa32, st), "sg_m4rm transpose");
+  g_launches++;
+  if (g_timing) cudaEventRecord(ev[1], st);
+  M4rmArgs a;
+  a.B = (const uint32_t*)B;
+  a.AT = AT;
+  a.C = p.splits > 1 ? partial : (uint32_t*)C;
+  a.m = m;
+  a.l = l;
+  a.mpad = p.mpad;
+  a.wa32 = p.wa32;
+  a.wc32 = p.wc32;
+  a.nblocks = p.nblocks;
+  a.bps = p.bps;
+  a.partial = p.splits > 1;
+  SG_CUDA(launch_m4rm(*p.ki, a, p.grid, st), "sg_m4rm kernel");
+  g_launches++;
+  if (g_timing) cudaEventRecord(ev[2], st);
+  if (p.splits > 1) {
+    SG_CUDA(launch_reduce_splits(field, partial, (uint32_t*)C, m, p.mpad, p.wc32, p.splits, st),
+            "sg_m4rm reduce");
+    g_launches++;
+  }
+  if (g_timing) {
+    cudaEventRecord(ev[3], st);
+    cudaEventSynchronize(ev[3]);
+    float t0 = 0, t1 = 0, t2 = 0;
+    cudaEventElapsedTime(&t0, ev[0], ev[1]);
+    cudaEventElapsedTime(&t1, ev[1], ev[2]);
+    cudaEventElapsedTime(&t2, ev[2], ev[3]);
+    g_last_ms[0] = t0;
+    g_last_ms[1] = t1;
+    g_last_ms[2] = t2;
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+  }
+  return SG_OK;
+}
+
+int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
+                 int k, int device) {
+  int rc = check_mul_args(field, A, B, C, m, l, n, k);
+  if (rc != SG_OK) return rc;
+  if (m == 0 || n == 0) return SG_OK;
+  SG_CUDA(cudaSetDevice(device), "sg_m4rm_host set device");
+  const int R = planes(field);
+  const size_t a_bytes = (size_t)R * m * w64_of(l) * 8, b_bytes = (size_t)R * l * w64_of(n) * 8,
+               c_bytes = (size_t)R * m * w64_of(n) * 8;
+  static std::map<int, std::pair<cudaStream_t, Buf>> io;  // per device: stream + staging buffer
+  char* dbuf = nullptr;
+  cudaStream_t st;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& slot = io[device];
+    if (!slot.first) SG_CUDA(cudaStreamCreateWithFlags(&slot.first, cudaStreamNonBlocking), "sg_m4rm_host stream");
+    st = slot.first;
+    const size_t need = a_bytes + b_bytes + c_bytes + 3 * 256;
+    if (slot.second.bytes < need) {
+      if (slot.second.p) cudaFree(slot.second.p);
+      slot.second.p = nullptr;
+      slot.second.bytes = 0;
+      SG_CUDA(cudaMalloc(&slot.second.p, need), "sg_m4rm_host alloc");
+      slot.second.bytes = need;
+    }
+    dbuf = (char*)slot.second.p;
+  }
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  uint64_t* dA = (uint64_t*)dbuf;
+  uint64_t* dB = (uint64_t*)(dbuf + up(a_bytes));
+  uint64_t* dC = (uint64_t*)(dbuf + up(a_bytes) + up(b_bytes));
+  if (a_bytes) SG_CUDA(cudaMemcpyAsync(dA, A, a_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D A");
+  if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D B");
+  rc = sg_m4rm(field, dA, dB, dC, m, l, n, k, nullptr, 0, st);
+  if (rc != SG_OK) return rc;
+  SG_CUDA(cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st), "sg_m4rm_host D2H C");
+  SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
+  return SG_OK;
+}
+
+int sg_build_table(int field, const uint64_t* const* B, int64_t b_rows, int64_t row_base, int kp, int64_t words,
+                   uint64_t* const* T, void* stream) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (kp < 0 || kp > 16 || row_base < 0 || words < 0 || b_rows < 0) return fail(SG_EINVAL, "bad table shape");
+  Planes b, t;
+  if (!fill_planes(&b, B, planes(field)) || !fill_planes(&t, (const uint64_t* const*)T, planes(field)))
+    return fail(SG_EINVAL, "null plane pointer");
+  SG_CUDA(launch_build_table(field, b, b_rows, row_base, kp, words, t, (cudaStream_t)stream), "sg_build_table");
+  g_launches++;
+  return SG_OK;
+}
+
+int sg_m4rm_block(int field, uint64_t* const* C, int64_t c_words, const uint64_t* const* A, int64_t a_words,
+                  int64_t col0, int kp, const uint64_t* const* T, int64_t row0, int64_t row1, void* stream) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (kp < 0 || kp > 16 || col0 < 0 || row0 < 0 || row1 < row0) return fail(SG_EINVAL, "bad block arguments");
+  if (col0 + kp > a_words * 64) return fail(SG_EINVAL, "block exceeds A's columns");
+  if (row1 == row0 || c_words == 0 || kp == 0) return SG_OK;
+  Planes c, a, t;
+  const int R = planes(field);
+  if (!fill_planes(&c, (const uint64_t* const*)C, R) || !fill_planes(&a, A, R) || !fill_planes(&t, T, R))
+    return fail(SG_EINVAL, "null plane pointer");
+  SG_CUDA(launch_block_driver(field, c, c_words, a, a_words, col0, kp, t, row0, row1, (cudaStream_t)stream),
+          "sg_m4rm_block");
+  g_launches++;
+  return SG_OK;
+}
+
+int sg_probe_peaks(int device, double* lop3, double* lds, double* mhz) {
+  if (!lop3 || !lds || !mhz) return fail(SG_EINVAL, "null pointer");
+  if (probe_peaks(device, lop3, lds, mhz) != 0) return fail(SG_ECUDA, "peak probe failed");
+  g_launches += 6;
+  return SG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// sg_internal.h -- launch-level interfaces shared by the .cu translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sg {
+
+// Column slab per CTA (32-bit words); each lane owns one uint4 (4 words = 128 lanes) of a row.
+constexpr int SLAB_WORDS = 4;
+// Table replicas: the 8 lanes of one LDS.128 phase read 8 different C rows, so entry g is
+// stored 8 times, replica j at bank offset 4j; lane (tid & 7) always reads replica (tid & 7).
+constexpr int COPIES = 8;
+constexpr int ENTRY_BYTES = COPIES * 16;
+constexpr int THREADS = 256;
+
+struct M4rmArgs {
+  const uint32_t* B;   // [R][l][wc32]   32-bit view of B's planes (row = 2*W64 words)
+  const uint32_t* AT;  // [R][wa32][mpad] index planes of A, transposed (F3: A0^A1, A1)
+  uint32_t* C;         // final [R][m][wc32] or partial [splits][R][mpad][wc32]
+  int64_t m, l, mpad;
+  int wa32, wc32;      // 32-bit words per row of A and of B/C
+  int nblocks, bps;    // k-blocks in total, k-blocks per split
+  int partial;         // 1: write raw partial sums (split-K), 0: canonical C
+};
+
+struct KernelInfo {
+  void (*fn)(M4rmArgs);
+  int field, k, rt, threads;
+  int smem_bytes;
+  int regs;            // filled in lazily from cudaFuncGetAttributes
+  int occupancy;       // CTAs per SM, filled lazily
+};
+
+// Registry of compiled M4RM instantiations (sg_m4rm.cu).
+int m4rm_kernel_count();
+KernelInfo* m4rm_kernel_at(int i);
+
+cudaError_t launch_transpose_a(int field, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
+                               int wa32, cudaStream_t st);
+cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st);
+cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int64_t m, int64_t mpad,
+                                 int wc32, int splits, cudaStream_t st);
+
+// sg_pack.cu
+cudaError_t launch_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld,
+                        uint64_t* planes, int* err_flag, cudaStream_t st);
+cudaError_t launch_unpack(int field, const uint64_t* planes, int64_t m, int64_t n, uint8_t* dense,
+                          int64_t ld, int* err_flag, cudaStream_t st);
+cudaError_t launch_canonicalize(int field, uint64_t* planes, int64_t rows, int64_t w64,
+                                cudaStream_t st);
+struct Planes {
+  uint64_t* p[3];
+};
+cudaError_t launch_plane_op(int op, Planes dst, Planes src, int64_t rows, int64_t w64, uint64_t tail,
+                            int scalar, cudaStream_t st);
+cudaError_t launch_block_driver(int field, Planes C, int64_t wc64, Planes A, int64_t wa64, int64_t col0,
+                                int kp, Planes T, int64_t row0, int64_t row1, cudaStream_t st);
+cudaError_t launch_build_table(int field, Planes B, int64_t b_rows, int64_t row_base, int kp, int64_t wc64,
+                               Planes T, cudaStream_t st);
+
+// sg_peaks.cu
+int probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_sm, double* sm_mhz);
+
+}  // namespace sg

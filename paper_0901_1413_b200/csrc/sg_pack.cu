@@ -1,0 +1,366 @@
+// sg_pack.cu -- HBM-bound kernels around the M4RM product:
+//   pack / unpack        dense uint8 residues <-> bit planes   (BitslicedMatrix.from_dense /
+//                        to_dense; layout implied by _core_py.py:186-192)
+//   canonicalize         f5_reduce / f7_reduce over whole planes (_core_py.py:143-148, 171-175)
+//   plane ops            the reference backend's in-place plane kernels on device arrays
+//                        (_core_py.py:24-175; argument order dst planes then src planes)
+//   block driver / table the plugin-granularity mirror of m4rm_block_<f> (_core_py.py:205-281)
+//                        and build_table for callers of the _core API.
+// Layout everywhere: planes [R][rows][W64] uint64, column c -> word c>>6, bit c&63;
+// viewed as 32-bit words, column c -> word c>>5, bit c&31 (little endian).
+#include "sg_field.cuh"
+#include "sg_internal.h"
+
+namespace sg {
+
+__host__ __device__ inline int planes_of(int field) {
+  return field == F2 ? 1 : (field == F5 || field == F7) ? 3 : 2;
+}
+
+// 4 bytes of a word -> bit d of each byte gathered into a nibble (byte i -> bit i)
+__device__ __forceinline__ u32 gather_bit(u32 x, int d) {
+  return ((((x >> d) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
+}
+// nibble -> one 0/1 byte per bit (bit i -> byte i)
+__device__ __forceinline__ u32 spread_nibble(u32 nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+// One thread per (row, 32-bit plane word): 32 consecutive dense bytes -> R plane words.
+__global__ void pack_kernel(int field, const uint8_t* __restrict__ dense, int64_t m, int64_t n,
+                            int64_t ld, u32* __restrict__ planes, int wc32, int* err) {
+  const int R = planes_of(field);
+  const int order = field == F2 ? 2 : field == F3 ? 3 : field == F5 ? 5 : field == F7 ? 7 : 4;
+  const int64_t total = m * wc32;
+  const u32 lim = 0x01010101u * (u32)order;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / wc32;
+    const int w = (int)(i % wc32);
+    const int64_t c0 = (int64_t)w * 32;
+    const uint8_t* src = dense + row * ld + c0;
+    u32 x[8];
+    const bool full = c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    if (full) {
+      const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        u32 v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int64_t c = c0 + 4 * q + b;
+          if (c < n) v |= (u32)src[4 * q + b] << (8 * b);
+        }
+        x[q] = v;
+      }
+    }
+    bool bad = false;
+    u32 p0 = 0, p1 = 0, p2 = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      u32 v = x[q];
+      bad |= __vcmpgeu4(v, lim) != 0u;
+      if (field == F3) v = ((v | (v >> 1)) & 0x01010101u) | (v & 0x02020202u);  // 1->01, 2->11
+      p0 |= gather_bit(v, 0) << (4 * q);
+      if (R > 1) p1 |= gather_bit(v, 1) << (4 * q);
+      if (R > 2) p2 |= gather_bit(v, 2) << (4 * q);
+    }
+    if (bad) atomicOr(err, 1);
+    planes[row * wc32 + w] = p0;
+    if (R > 1) planes[(m + row) * wc32 + w] = p1;
+    if (R > 2) planes[(2 * m + row) * wc32 + w] = p2;
+  }
+}
+
+// One thread per (row, 32-bit plane word): R plane words -> 32 dense residues.
+__global__ void unpack_kernel(int field, const u32* __restrict__ planes, int64_t m, int64_t n,
+                              uint8_t* __restrict__ dense, int64_t ld, int wc32, int* err) {
+  const int R = planes_of(field);
+  const int64_t total = m * wc32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / wc32;
+    const int w = (int)(i % wc32);
+    const int64_t c0 = (int64_t)w * 32;
+    if (c0 >= n) continue;
+    const u32 p0 = planes[row * wc32 + w];
+    const u32 p1 = R > 1 ? planes[(m + row) * wc32 + w] : 0u;
+    const u32 p2 = R > 2 ? planes[(2 * m + row) * wc32 + w] : 0u;
+    u32 x[8];
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const u32 b0 = spread_nibble((p0 >> (4 * q)) & 0xFu);
+      const u32 b1 = spread_nibble((p1 >> (4 * q)) & 0xFu);
+      const u32 b2 = spread_nibble((p2 >> (4 * q)) & 0xFu);
+      u32 v;
+      if (field == F3) {
+        bad |= (b1 & ~b0) != 0u;  // sign without unit: illegal (fields.py:88-101)
+        v = b0 + b1;
+      } else {
+        v = b0 | (b1 << 1) | (b2 << 2);
+        if (field == F5) v = __vsub4(v, __vcmpgeu4(v, 0x05050505u) & 0x05050505u);
+        if (field == F7) v = __vsub4(v, __vcmpeq4(v, 0x07070707u) & 0x07070707u);
+      }
+      x[q] = v;
+    }
+    if (bad) atomicOr(err, 2);
+    uint8_t* dst = dense + row * ld + c0;
+    if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      reinterpret_cast<uint4*>(dst)[0] = make_uint4(x[0], x[1], x[2], x[3]);
+      reinterpret_cast<uint4*>(dst)[1] = make_uint4(x[4], x[5], x[6], x[7]);
+    } else {
+      for (int c = 0; c < 32 && c0 + c < n; ++c) dst[c] = (uint8_t)(x[c >> 2] >> (8 * (c & 3)));
+    }
+  }
+}
+
+__global__ void canonicalize_kernel(int field, uint64_t* __restrict__ p, int64_t n_words) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_words;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t a = p[i], b = p[n_words + i], c = p[2 * n_words + i];
+    u32 lo[3] = {(u32)a, (u32)b, (u32)c}, hi[3] = {(u32)(a >> 32), (u32)(b >> 32), (u32)(c >> 32)};
+    if (field == F5) { f5_reduce(lo[0], lo[1], lo[2]); f5_reduce(hi[0], hi[1], hi[2]); }
+    else { f7_reduce(lo[0], lo[1], lo[2]); f7_reduce(hi[0], hi[1], hi[2]); }
+    p[i] = lo[0] | ((uint64_t)hi[0] << 32);
+    p[n_words + i] = lo[1] | ((uint64_t)hi[1] << 32);
+    p[2 * n_words + i] = lo[2] | ((uint64_t)hi[2] << 32);
+  }
+}
+
+// ------------------------------------------------------------------ plane ops (plugin kernels)
+// op codes mirror include/slicegemm_b200.h SG_OP_*
+enum {
+  OP_F2_ADD = 0, OP_F3_ADD, OP_F3_SUB, OP_F3_NEG, OP_F5_ADD, OP_F5_SUB, OP_F5_NEG, OP_F5_DOUBLE,
+  OP_F5_REDUCE, OP_F7_ADD, OP_F7_SUB, OP_F7_NEG, OP_F7_DOUBLE, OP_F7_REDUCE, OP_GF4_ADD,
+  OP_GF4_MULX, OP_F5_FOLD5, OP_SCALAR_MUL_F3, OP_SCALAR_MUL_F5, OP_SCALAR_MUL_F7,
+  OP_SCALAR_MUL_GF4, OP_COUNT
+};
+
+__device__ __forceinline__ void apply_op(int op, u32* d, const u32* s, u32 tail, int scalar) {
+  switch (op) {
+    case OP_F2_ADD: d[0] ^= s[0]; break;
+    case OP_GF4_ADD: d[0] ^= s[0]; d[1] ^= s[1]; break;
+    case OP_GF4_MULX: { u32 t = d[1]; d[1] ^= d[0]; d[0] = t; } break;
+    case OP_F3_ADD: f3_add(d[0], d[1], s[0], s[1]); break;
+    case OP_F3_SUB: f3_sub(d[0], d[1], s[0], s[1]); break;
+    case OP_F3_NEG: d[1] ^= d[0]; break;
+    case OP_F5_ADD: f5_add(d[0], d[1], d[2], s[0], s[1], s[2]); break;
+    case OP_F5_SUB: { u32 a = s[0], b = s[1], c = s[2]; f5_neg(a, b, c); f5_add(d[0], d[1], d[2], a, b, c); } break;
+    case OP_F5_NEG: f5_neg(d[0], d[1], d[2]); break;
+    case OP_F5_DOUBLE: f5_double(d[0], d[1], d[2]); break;
+    case OP_F5_REDUCE: f5_reduce(d[0], d[1], d[2]); break;
+    case OP_F5_FOLD5: { u32 r0, r1, r2; fold5(d[0], d[1], d[2], s[0], r0, r1, r2); d[0] = r0; d[1] = r1; d[2] = r2; } break;
+    case OP_F7_ADD: f7_add(d[0], d[1], d[2], s[0], s[1], s[2]); break;
+    case OP_F7_SUB: { u32 a = s[0], b = s[1], c = s[2]; f7_neg(a, b, c, tail); f7_add(d[0], d[1], d[2], a, b, c); } break;
+    case OP_F7_NEG: f7_neg(d[0], d[1], d[2], tail); break;
+    case OP_F7_DOUBLE: f7_double(d[0], d[1], d[2]); break;
+    case OP_F7_REDUCE: f7_reduce(d[0], d[1], d[2]); break;
+    case OP_SCALAR_MUL_F3: {  // c in {0, 1, 2}: 0 clears, 2 = -1 negates
+      if (scalar == 0) { d[0] = 0; d[1] = 0; } else if (scalar == 2) d[1] ^= d[0];
+    } break;
+    case OP_SCALAR_MUL_F5:
+    case OP_SCALAR_MUL_F7: {  // Horner over the bits of c with double and add
+      const bool five = op == OP_SCALAR_MUL_F5;
+      u32 x0 = d[0], x1 = d[1], x2 = d[2], a0 = 0, a1 = 0, a2 = 0;
+      for (int b = 2; b >= 0; --b) {
+        if (five) f5_double(a0, a1, a2); else f7_double(a0, a1, a2);
+        if ((scalar >> b) & 1) { if (five) f5_add(a0, a1, a2, x0, x1, x2); else f7_add(a0, a1, a2, x0, x1, x2); }
+      }
+      d[0] = a0; d[1] = a1; d[2] = a2;
+    } break;
+    case OP_SCALAR_MUL_GF4: {  // c = c0 + c1 x
+      const u32 x0 = d[0], x1 = d[1];
+      u32 r0 = 0, r1 = 0;
+      if (scalar & 1) { r0 ^= x0; r1 ^= x1; }
+      if (scalar & 2) { r0 ^= x1; r1 ^= x0 ^ x1; }
+      d[0] = r0; d[1] = r1;
+    } break;
+  }
+}
+
+__device__ __forceinline__ int op_planes(int op) {
+  switch (op) {
+    case OP_F2_ADD: return 1;
+    case OP_F3_ADD: case OP_F3_SUB: case OP_F3_NEG: case OP_GF4_ADD: case OP_GF4_MULX:
+    case OP_SCALAR_MUL_F3: case OP_SCALAR_MUL_GF4: return 2;
+    default: return 3;
+  }
+}
+
+// dst/src: R planes (one device pointer each) of rows * w64 words; the tail mask applies to
+// the last word of every row (padding lanes, _core_py.py:155-168).
+__global__ void plane_op_kernel(int op, Planes dst, Planes src, int64_t rows, int64_t w64, uint64_t tail,
+                                int scalar, int has_src) {
+  const int R = op_planes(op);
+  const int RS = has_src ? (op == OP_F5_FOLD5 ? 1 : R) : 0;  // fold5's 4th input bit is src plane 0
+  const int64_t total = rows * w64;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t tm = (i % w64 == w64 - 1) ? tail : ~0ull;
+    u32 dl[3] = {0, 0, 0}, dh[3] = {0, 0, 0}, sl[3] = {0, 0, 0}, shh[3] = {0, 0, 0};
+    for (int d = 0; d < R; ++d) {
+      const uint64_t x = dst.p[d][i];
+      dl[d] = (u32)x; dh[d] = (u32)(x >> 32);
+    }
+    for (int d = 0; d < RS; ++d) {
+      const uint64_t y = src.p[d][i];
+      sl[d] = (u32)y; shh[d] = (u32)(y >> 32);
+    }
+    apply_op(op, dl, sl, (u32)tm, scalar);
+    apply_op(op, dh, shh, (u32)(tm >> 32), scalar);
+    for (int d = 0; d < R; ++d) dst.p[d][i] = dl[d] | ((uint64_t)dh[d] << 32);
+  }
+}
+
+// ------------------------------------------------------------------ block-level plugin mirror
+// C_i += sum_d alpha_d T[phi_d(A_i, col0..col0+kp)] for rows row0..row1 (_core_py.py:205-281).
+// One thread per (row, 64-bit word of C); the table uses the reference layout, one plane array
+// of 2^kp rows x wc64 words each.
+template <int F>
+__global__ void block_driver_kernel(Planes C, int64_t wc64, Planes A, int64_t wa64, int64_t col0, int kp,
+                                    Planes T, int64_t row0, int64_t row1) {
+  constexpr int R = Traits<F>::R;
+  const int64_t total = (row1 - row0) * wc64;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = row0 + i / wc64, w = i % wc64;
+    u32 g[3] = {0, 0, 0};
+    for (int d = 0; d < R; ++d) {
+      u32 x = 0;
+      for (int t = 0; t < kp; ++t) {
+        const int64_t c = col0 + t;
+        x |= (u32)((A.p[d][row * wa64 + (c >> 6)] >> (c & 63)) & 1ull) << t;
+      }
+      g[d] = x;
+    }
+    if (F == F3) g[0] ^= g[1];  // pos = A0 ^ A1, neg = A1
+    uint64_t out[3] = {0, 0, 0};
+    for (int half = 0; half < 2; ++half) {
+      const int sh = 32 * half;
+      V<F> c;
+      for (int d = 0; d < R; ++d) c.p[d] = (u32)(C.p[d][row * wc64 + w] >> sh);
+      auto T_ = [&](int d, u32 gg) { return (u32)(T.p[d][(int64_t)gg * wc64 + w] >> sh); };
+      if constexpr (F == F2) {
+        c.p[0] ^= T_(0, g[0]);
+      } else if constexpr (F == F3) {
+        f3_add(c.p[0], c.p[1], T_(0, g[0]), T_(1, g[0]));
+        f3_sub(c.p[0], c.p[1], T_(0, g[1]), T_(1, g[1]));
+      } else if constexpr (F == GF4) {
+        const u32 q1 = T_(1, g[1]);
+        c.p[0] ^= T_(0, g[0]) ^ q1;
+        c.p[1] ^= T_(1, g[0]) ^ T_(0, g[1]) ^ q1;
+      } else {
+        u32 x0 = T_(0, g[2]), x1 = T_(1, g[2]), x2 = T_(2, g[2]);
+        if constexpr (F == F5) {
+          f5_double(x0, x1, x2); f5_add(x0, x1, x2, T_(0, g[1]), T_(1, g[1]), T_(2, g[1]));
+          f5_double(x0, x1, x2); f5_add(x0, x1, x2, T_(0, g[0]), T_(1, g[0]), T_(2, g[0]));
+          f5_add(c.p[0], c.p[1], c.p[2], x0, x1, x2);
+        } else {
+          f7_double(x0, x1, x2); f7_add(x0, x1, x2, T_(0, g[1]), T_(1, g[1]), T_(2, g[1]));
+          f7_double(x0, x1, x2); f7_add(x0, x1, x2, T_(0, g[0]), T_(1, g[0]), T_(2, g[0]));
+          f7_add(c.p[0], c.p[1], c.p[2], x0, x1, x2);
+        }
+      }
+      for (int d = 0; d < R; ++d) out[d] |= (uint64_t)c.p[d] << sh;
+    }
+    for (int d = 0; d < R; ++d) C.p[d][row * wc64 + w] = out[d];
+  }
+}
+
+// T[g] = sum over set bits t of g of B[row_base + t]  (mask-indexed); rows past
+// b_rows are zero.  One thread per (entry, 64-bit word).
+template <int F>
+__global__ void build_table_kernel(Planes B, int64_t b_rows, int64_t row_base, int kp, int64_t wc64, Planes T) {
+  constexpr int R = Traits<F>::R;
+  const int64_t total = ((int64_t)1 << kp) * wc64;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = i / wc64, w = i % wc64;
+    uint64_t out[3] = {0, 0, 0};
+    for (int half = 0; half < 2; ++half) {
+      const int sh = 32 * half;
+      V<F> acc;
+      for (int d = 0; d < R; ++d) acc.p[d] = 0;
+      for (int t = 0; t < kp; ++t) {
+        if (((g >> t) & 1) && row_base + t < b_rows) {
+          V<F> b;
+          for (int d = 0; d < R; ++d) b.p[d] = (u32)(B.p[d][(row_base + t) * wc64 + w] >> sh);
+          vadd<F>(acc, b);
+        }
+      }
+      for (int d = 0; d < R; ++d) out[d] |= (uint64_t)acc.p[d] << sh;
+    }
+    for (int d = 0; d < R; ++d) T.p[d][g * wc64 + w] = out[d];
+  }
+}
+
+static unsigned grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld,
+                        uint64_t* planes, int* err, cudaStream_t st) {
+  const int wc32 = (int)(2 * ((n + 63) / 64));
+  if (m == 0 || wc32 == 0) return cudaSuccess;
+  pack_kernel<<<grid_for(m * wc32, 256), 256, 0, st>>>(field, dense, m, n, ld,
+                                                        reinterpret_cast<u32*>(planes), wc32, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(int field, const uint64_t* planes, int64_t m, int64_t n, uint8_t* dense,
+                          int64_t ld, int* err, cudaStream_t st) {
+  const int wc32 = (int)(2 * ((n + 63) / 64));
+  if (m == 0 || wc32 == 0) return cudaSuccess;
+  unpack_kernel<<<grid_for(m * wc32, 256), 256, 0, st>>>(field, reinterpret_cast<const u32*>(planes), m, n,
+                                                          dense, ld, wc32, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_canonicalize(int field, uint64_t* planes, int64_t rows, int64_t w64, cudaStream_t st) {
+  if (field != F5 && field != F7) return cudaSuccess;
+  const int64_t nw = rows * w64;
+  if (nw == 0) return cudaSuccess;
+  canonicalize_kernel<<<grid_for(nw, 256), 256, 0, st>>>(field, planes, nw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plane_op(int op, Planes dst, Planes src, int64_t rows, int64_t w64, uint64_t tail,
+                            int scalar, cudaStream_t st) {
+  if (op < 0 || op >= OP_COUNT) return cudaErrorInvalidValue;
+  const int64_t nw = rows * w64;
+  if (nw == 0) return cudaSuccess;
+  plane_op_kernel<<<grid_for(nw, 256), 256, 0, st>>>(op, dst, src, rows, w64, tail, scalar, src.p[0] != nullptr);
+  return cudaGetLastError();
+}
+
+#define SG_FIELD_SWITCH(field, KERNEL, ...)                                              \
+  switch (field) {                                                                      \
+    case F2: KERNEL<F2><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
+    case F3: KERNEL<F3><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
+    case F5: KERNEL<F5><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
+    case F7: KERNEL<F7><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
+    default: KERNEL<GF4><<<g, 256, 0, st>>>(__VA_ARGS__); break;                        \
+  }
+
+cudaError_t launch_block_driver(int field, Planes C, int64_t wc64, Planes A, int64_t wa64, int64_t col0, int kp,
+                                Planes T, int64_t row0, int64_t row1, cudaStream_t st) {
+  const int64_t work = (row1 - row0) * wc64;
+  if (work <= 0) return cudaSuccess;
+  const unsigned g = grid_for(work, 256);
+  SG_FIELD_SWITCH(field, block_driver_kernel, C, wc64, A, wa64, col0, kp, T, row0, row1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_table(int field, Planes B, int64_t b_rows, int64_t row_base, int kp, int64_t wc64,
+                               Planes T, cudaStream_t st) {
+  const int64_t work = ((int64_t)1 << kp) * wc64;
+  if (work <= 0) return cudaSuccess;
+  const unsigned g = grid_for(work, 256);
+  SG_FIELD_SWITCH(field, build_table_kernel, B, b_rows, row_base, kp, wc64, T);
+  return cudaGetLastError();
+}
+
+}  // namespace sg

@@ -1,0 +1,59 @@
+"""Field descriptors for the B200 path (a restatement of the reference's FieldSpec data).
+
+Names, orders and encodings follow slicegemm/fields.py: F2 (:78-86), F3 unit/sign planes
+(:88-101), F5 and F7 plain 3-bit redundant patterns (:103-129), and F4 = GF(4) as
+F2[x]/(x^2+x+1) (:215), which this path stores directly as a 2-plane matrix (plane 0 =
+coefficient of 1, plane 1 = coefficient of x).  Z4/Z8 and F8/F9/F25/F27 are not on this
+path (SURVEY.md 8f lists them as next).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class FieldSpec:
+    name: str
+    order: int
+    char: int
+    bits: int               # bit planes per element
+    code: int               # SG_* field code of the C ABI
+    decode_table: tuple     # pattern -> residue (None = illegal)
+    canonical_table: tuple  # residue -> pattern
+
+    def decode(self, pattern: int) -> int:
+        e = self.decode_table[pattern]
+        if e is None:
+            raise ValueError(f"invalid {self.name} pattern {pattern:#b}")
+        return e
+
+    def canonical(self, residue: int) -> int:
+        if not 0 <= residue < self.order:
+            raise ValueError(f"{residue} is not a residue of {self.name}")
+        return self.canonical_table[residue]
+
+    def __repr__(self):
+        return f"FieldSpec({self.name})"
+
+
+F2 = FieldSpec("f2", 2, 2, 1, _lib.SG_F2, (0, 1), (0, 1))
+F3 = FieldSpec("f3", 3, 3, 2, _lib.SG_F3, (0, 1, None, 2), (0, 1, 3))
+F5 = FieldSpec("f5", 5, 5, 3, _lib.SG_F5, (0, 1, 2, 3, 4, 0, 1, 2), (0, 1, 2, 3, 4))
+F7 = FieldSpec("f7", 7, 7, 3, _lib.SG_F7, (0, 1, 2, 3, 4, 5, 6, 0), (0, 1, 2, 3, 4, 5, 6))
+# GF(4) = F2[x]/(x^2 + x + 1): the residue r in [0, 4) is the polynomial (r & 1) + (r >> 1) x.
+F4 = FieldSpec("f4", 4, 2, 2, _lib.SG_GF4, (0, 1, 2, 3), (0, 1, 2, 3))
+GF4 = F4
+
+FIELDS = {f.name: f for f in (F2, F3, F5, F7)}
+EXT_FIELDS = {"f4": F4}
+ALL_FIELDS = {**FIELDS, **EXT_FIELDS, "gf4": F4}
+
+
+def by_name(name: str) -> FieldSpec:
+    try:
+        return ALL_FIELDS[name.lower()]
+    except KeyError:
+        raise ValueError(f"unknown field {name!r}") from None

@@ -1,0 +1,140 @@
+"""m4rm_multiply and friends: the reference multiply API over the B200 kernels.
+
+Contract: SPEC.md:301-367 (the reference's m4rm.py is missing; names from __init__.py:16).
+  M4rmParams(k)        SPEC.md:306-311   (1 <= k <= 16)
+  choose_k(l)          SPEC.md:340-346   clamp(floor(log2 l) - 2, 1, 10)
+  build_table(B, s, k) SPEC.md:313-325   mask-indexed table of one k-row block of B
+  m4rm_multiply(A, B)  SPEC.md:326-332   C = A B, equal to the oracle after canonicalization;
+                                          this implementation returns C canonical and
+                                          bit-identical for every k (k > 8 uses 8-row blocks).
+Device matrices run sg_m4rm on the current CUDA stream; two host matrices run the
+host-buffer entry point sg_m4rm_host (H2D, multiply, D2H).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .matrix import BitslicedMatrix, _require_cuda, _vp
+
+
+@dataclass(frozen=True)
+class M4rmParams:
+    k: int = None
+
+    def __post_init__(self):
+        if self.k is not None and not 1 <= self.k <= 16:
+            raise ValueError("k must be in 1..16")
+
+
+def choose_k(l: int) -> int:
+    if l < 1:
+        return 1
+    return max(1, min(10, l.bit_length() - 1 - 2))
+
+
+def _check(A: BitslicedMatrix, B: BitslicedMatrix):
+    if not isinstance(A, BitslicedMatrix) or not isinstance(B, BitslicedMatrix):
+        raise TypeError("m4rm_multiply takes two BitslicedMatrix operands")
+    if A.field is not B.field:
+        raise ValueError(f"field mismatch: {A.field.name} vs {B.field.name}")
+    if A.ncols != B.nrows:
+        raise ValueError(f"inner dimensions {A.ncols} != {B.nrows}")
+
+
+def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = None,
+                  out: BitslicedMatrix = None) -> BitslicedMatrix:
+    _check(A, B)
+    k = (params.k if params is not None and params.k is not None else None) or choose_k(A.ncols)
+    m, l, n = A.nrows, A.ncols, B.ncols
+    field = A.field
+    L = _lib.load()
+    if A.device.type == "cpu" and B.device.type == "cpu":
+        # host buffers in, host buffers out: the reference-facing call with copies included
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device is available: the B200 path has no CPU fallback")
+        a = A.planes.contiguous()
+        b = B.planes.contiguous()
+        C = BitslicedMatrix.zero(field, m, n, device="cpu") if out is None else out
+        if m and n:
+            _lib.check(L.sg_m4rm_host(field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k,
+                                      torch.cuda.current_device()))
+        return C
+    dev = A.device if A.device.type == "cuda" else B.device
+    _require_cuda(dev)
+    a = A.planes.to(dev).contiguous()
+    b = B.planes.to(dev).contiguous()
+    if out is None:
+        C = BitslicedMatrix(field, m, n, torch.empty((field.bits, m, (n + 63) // 64), dtype=torch.int64, device=dev))
+    else:
+        if out.field is not field or (out.nrows, out.ncols) != (m, n) or out.device != dev:
+            raise ValueError("out has the wrong field, shape or device")
+        C = out
+    if m and n:
+        with torch.cuda.device(dev):
+            _lib.check(L.sg_m4rm(field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k, None, 0,
+                                 _lib.current_stream_handle(dev)))
+    return C
+
+
+def build_table(B: BitslicedMatrix, s: int, k: int) -> torch.Tensor:
+    """Table of block s (rows s*k .. s*k+kp-1 of B): int64 tensor (R, 2^kp, words).
+
+    Entry g is the field sum of the rows whose bit is set in g (so T[0] = 0); the final block
+    may be narrower (kp = l - s*k).
+    """
+    if not 1 <= k <= 16:
+        raise ValueError("k must be in 1..16")
+    l = B.nrows
+    if not 0 <= s * k < max(l, 1):
+        raise ValueError("block index out of range")
+    kp = min(k, l - s * k)
+    Bg = B._on_gpu()
+    R, W = B.field.bits, B.words_per_row
+    T = torch.zeros((R, 1 << kp, W), dtype=torch.int64, device=Bg.device)
+    bp, _k1 = _lib.ptr_array([Bg.planes[d].data_ptr() for d in range(R)])
+    tp, _k2 = _lib.ptr_array([T[d].data_ptr() for d in range(R)])
+    with torch.cuda.device(Bg.device):
+        _lib.check(_lib.load().sg_build_table(B.field.code, bp, l, s * k, kp, W, tp,
+                                              _lib.current_stream_handle(Bg.device)))
+    return T
+
+
+def plan(field, m: int, l: int, n: int, k: int = 8) -> dict:
+    """The launch the planner picks for this product (rows per CTA, k-splits, CTAs)."""
+    from .fields import by_name
+    if isinstance(field, str):
+        field = by_name(field)
+    rows, splits, ctas, idx = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.check(_lib.load().sg_plan(field.code, m, l, n, k, ctypes.byref(rows), ctypes.byref(splits),
+                                   ctypes.byref(ctas), ctypes.byref(idx)))
+    return {"rows_per_cta": rows.value, "splits": splits.value, "ctas": ctas.value, "kernel": idx.value}
+
+
+def set_plan_override(rows_per_thread: int = 0, splits: int = 0):
+    _lib.check(_lib.load().sg_set_plan_override(rows_per_thread, splits))
+
+
+def last_timing() -> dict:
+    t, mm, r = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.load().sg_last_timing(ctypes.byref(t), ctypes.byref(mm), ctypes.byref(r)))
+    return {"transpose_ms": t.value, "m4rm_ms": mm.value, "reduce_ms": r.value}
+
+
+def set_timing(enable: bool):
+    _lib.check(_lib.load().sg_set_timing(1 if enable else 0))
+
+
+def launch_count() -> int:
+    return int(_lib.load().sg_launch_count())
+
+
+def probe_peaks(device: int = 0) -> dict:
+    a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.load().sg_probe_peaks(device, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return {"lop3_per_clk_per_sm": a.value, "lds_bytes_per_clk_per_sm": b.value, "sm_mhz": c.value}

@@ -1,0 +1,261 @@
+"""BitslicedMatrix: the reference's matrix type, stored plane-major in B200 HBM.
+
+Contract: SPEC.md:198-299 (the reference's matrix.py is missing, __init__.py:15).  Storage is
+one int64 tensor of shape (R, nrows, words_per_row) holding the exact uint64 bit patterns of
+the reference layout: plane d holds bit d of every entry, column c -> word c >> 6, bit c & 63,
+padding lanes zero.  A matrix may live on a CUDA device (where
+every operation runs, through libslicegemm_b200.so) or on the host as a plain container; a
+host matrix is moved to the GPU by any operation that computes, and m4rm_multiply on two host
+matrices runs the host-buffer entry point sg_m4rm_host (copies included).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .fields import FieldSpec, by_name
+
+
+def _words(n: int) -> int:
+    return (n + 63) // 64
+
+
+def _dev(device):
+    d = torch.device(device)
+    if d.type == "cuda" and d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
+def _require_cuda(device):
+    if device.type != "cuda":
+        raise ValueError("this operation runs on a CUDA device (no CPU fallback)")
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device is available: the B200 path has no CPU fallback")
+
+
+def _vp(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class BitslicedMatrix:
+    __slots__ = ("field", "nrows", "ncols", "planes")
+
+    def __init__(self, field: FieldSpec, nrows: int, ncols: int, planes: torch.Tensor):
+        if isinstance(field, str):
+            field = by_name(field)
+        if nrows < 0 or ncols < 0:
+            raise ValueError("dimensions must be non-negative")
+        shape = (field.bits, nrows, _words(ncols))
+        if tuple(planes.shape) != shape or planes.dtype != torch.int64:
+            raise ValueError(f"planes must be int64 of shape {shape}, got {tuple(planes.shape)} {planes.dtype}")
+        self.field = field
+        self.nrows = nrows
+        self.ncols = ncols
+        self.planes = planes.contiguous()
+
+    # ------------------------------------------------------------------ construction
+    @property
+    def words_per_row(self) -> int:
+        return _words(self.ncols)
+
+    @property
+    def device(self) -> torch.device:
+        return self.planes.device
+
+    @classmethod
+    def zero(cls, field, m: int, n: int, device="cuda") -> "BitslicedMatrix":
+        if isinstance(field, str):
+            field = by_name(field)
+        if m < 0 or n < 0:
+            raise ValueError("dimensions must be non-negative")
+        return cls(field, m, n, torch.zeros((field.bits, m, _words(n)), dtype=torch.int64, device=device))
+
+    @classmethod
+    def from_planes(cls, field, planes, n: int, device=None) -> "BitslicedMatrix":
+        """Wrap reference-layout planes (numpy uint64 (R, m, W) or a torch int64 tensor)."""
+        if isinstance(field, str):
+            field = by_name(field)
+        if isinstance(planes, np.ndarray):
+            t = torch.from_numpy(np.ascontiguousarray(planes, dtype=np.uint64).view(np.int64))
+        else:
+            t = planes
+        if device is not None:
+            t = t.to(device)
+        return cls(field, t.shape[1], n, t)
+
+    @classmethod
+    def from_dense(cls, field, D, device="cuda") -> "BitslicedMatrix":
+        """Pack dense residues (numpy / torch / an object with .entries) on the GPU."""
+        if isinstance(field, str):
+            field = by_name(field)
+        entries = getattr(D, "entries", D)
+        if isinstance(entries, torch.Tensor):
+            if entries.dtype.is_floating_point:
+                raise ValueError("entries must be integers")
+            if entries.numel() and (int(entries.min()) < 0 or int(entries.max()) >= field.order):
+                raise ValueError(f"entries out of range for {field.name}")
+            dense = entries.to(torch.uint8)
+        else:
+            arr = np.asarray(entries)
+            if arr.ndim != 2:
+                raise ValueError("entries must be two-dimensional")
+            if arr.size and (arr.min() < 0 or arr.max() >= field.order):
+                raise ValueError(f"entries out of range for {field.name}")
+            dense = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint8))
+        if dense.dim() != 2:
+            raise ValueError("entries must be two-dimensional")
+        m, n = dense.shape
+        target = _dev(device)
+        gpu = target if target.type == "cuda" else _dev("cuda")
+        _require_cuda(gpu)
+        out = cls.zero(field, m, n, device=gpu)
+        if m and n:
+            dd = dense.to(gpu, non_blocking=False).contiguous()
+            with torch.cuda.device(gpu):
+                _lib.check(_lib.load().sg_pack(field.code, _vp(dd), m, n, n, _vp(out.planes),
+                                               _lib.current_stream_handle(gpu)))
+        return out if target.type == "cuda" else out.to(target)
+
+    @classmethod
+    def random(cls, field, m: int, n: int, seed: int, device="cuda") -> "BitslicedMatrix":
+        """Deterministic uniform residues: the DenseMatrix.random stream (oracle.py:47-50)."""
+        if isinstance(field, str):
+            field = by_name(field)
+        g = np.random.Generator(np.random.PCG64(seed))
+        dense = np.empty((m, n), dtype=np.uint8)
+        step = max(1, (1 << 24) // max(n, 1))
+        for r0 in range(0, m, step):
+            r1 = min(m, r0 + step)
+            dense[r0:r1] = g.integers(0, field.order, size=(r1 - r0, n), dtype=np.int64)
+        return cls.from_dense(field, dense, device=device)
+
+    # ------------------------------------------------------------------ movement
+    def to(self, device) -> "BitslicedMatrix":
+        return BitslicedMatrix(self.field, self.nrows, self.ncols, self.planes.to(device))
+
+    def cpu(self) -> "BitslicedMatrix":
+        return self.to("cpu")
+
+    def cuda(self, device=None) -> "BitslicedMatrix":
+        return self.to(_dev("cuda" if device is None else device))
+
+    def copy(self) -> "BitslicedMatrix":
+        return BitslicedMatrix(self.field, self.nrows, self.ncols, self.planes.clone())
+
+    def planes_numpy(self) -> np.ndarray:
+        """The reference-layout planes as a host uint64 array of shape (R, m, W)."""
+        return self.planes.cpu().numpy().view(np.uint64)
+
+    def _on_gpu(self) -> "BitslicedMatrix":
+        return self if self.device.type == "cuda" else self.cuda()
+
+    # ------------------------------------------------------------------ dense views
+    def to_dense(self) -> np.ndarray:
+        """Unpack to dense residues (uint8, shape (m, n)) on the GPU, returned on the host."""
+        g = self._on_gpu()
+        _require_cuda(g.device)
+        out = torch.empty((self.nrows, self.ncols), dtype=torch.uint8, device=g.device)
+        if self.nrows and self.ncols:
+            with torch.cuda.device(g.device):
+                _lib.check(_lib.load().sg_unpack(self.field.code, _vp(g.planes), self.nrows, self.ncols,
+                                                 _vp(out), self.ncols, _lib.current_stream_handle(g.device)))
+        return out.cpu().numpy()
+
+    def get(self, i: int, j: int) -> int:
+        if not (0 <= i < self.nrows and 0 <= j < self.ncols):
+            raise IndexError("index out of range")
+        words = self.planes[:, i, j >> 6].cpu().numpy().view(np.uint64)
+        pat = sum(int((int(words[d]) >> (j & 63)) & 1) << d for d in range(self.field.bits))
+        return self.field.decode(pat)
+
+    def set(self, i: int, j: int, e: int) -> None:
+        if not (0 <= i < self.nrows and 0 <= j < self.ncols):
+            raise IndexError("index out of range")
+        pat = self.field.canonical(e)
+        words = self.planes[:, i, j >> 6].cpu().numpy().view(np.uint64).copy()
+        bit = np.uint64(1 << (j & 63))
+        for d in range(self.field.bits):
+            if (pat >> d) & 1:
+                words[d] |= bit
+            else:
+                words[d] &= ~bit
+        self.planes[:, i, j >> 6] = torch.from_numpy(words.view(np.int64)).to(self.device)
+
+    # ------------------------------------------------------------------ elementwise (GPU)
+    def _check_same(self, other: "BitslicedMatrix"):
+        if not isinstance(other, BitslicedMatrix) or other.field is not self.field:
+            raise ValueError("field mismatch")
+        if (other.nrows, other.ncols) != (self.nrows, self.ncols):
+            raise ValueError("shape mismatch")
+
+    def _plane_op(self, op: str, src: "BitslicedMatrix" = None, scalar: int = 0, tail=True):
+        dst = self._on_gpu().copy()
+        R = self.field.bits
+        dptr, _k1 = _lib.ptr_array([dst.planes[d].data_ptr() for d in range(R)])
+        if src is not None:
+            s = src.planes.to(dst.device).contiguous()
+            sptr, _k2 = _lib.ptr_array([s[d].data_ptr() for d in range(R)])
+        else:
+            sptr = None
+        rem = self.ncols % 64
+        tmask = ((1 << rem) - 1) if (rem and tail) else (1 << 64) - 1
+        if self.nrows and self.words_per_row:
+            with torch.cuda.device(dst.device):
+                _lib.check(_lib.load().sg_plane_op(_lib.OPS[op], dptr, sptr, self.nrows, self.words_per_row,
+                                                   tmask, scalar, _lib.current_stream_handle(dst.device)))
+        return dst
+
+    def add(self, other: "BitslicedMatrix") -> "BitslicedMatrix":
+        self._check_same(other)
+        name = {"f2": "f2_add", "f3": "f3_add", "f5": "f5_add", "f7": "f7_add", "f4": "gf4_add"}[self.field.name]
+        return self._plane_op(name, other)
+
+    def sub(self, other: "BitslicedMatrix") -> "BitslicedMatrix":
+        self._check_same(other)
+        name = {"f2": "f2_add", "f3": "f3_sub", "f5": "f5_sub", "f7": "f7_sub", "f4": "gf4_add"}[self.field.name]
+        return self._plane_op(name, other)
+
+    def neg(self) -> "BitslicedMatrix":
+        name = self.field.name
+        if name in ("f2", "f4"):
+            return self._on_gpu().copy()
+        return self._plane_op({"f3": "f3_neg", "f5": "f5_neg", "f7": "f7_neg"}[name])
+
+    def scalar_mul(self, c: int) -> "BitslicedMatrix":
+        if not 0 <= c < self.field.order:
+            raise ValueError(f"{c} is not a residue of {self.field.name}")
+        name = self.field.name
+        if name == "f2":
+            return self._on_gpu().copy() if c else BitslicedMatrix.zero(self.field, self.nrows, self.ncols,
+                                                                       self._on_gpu().device)
+        op = {"f3": "scalar_mul_f3", "f5": "scalar_mul_f5", "f7": "scalar_mul_f7", "f4": "scalar_mul_gf4"}[name]
+        return self._plane_op(op, scalar=c)
+
+    def reduce_canonical(self) -> "BitslicedMatrix":
+        out = self._on_gpu().copy()
+        if self.nrows and self.ncols:
+            with torch.cuda.device(out.device):
+                _lib.check(_lib.load().sg_reduce_canonical(self.field.code, _vp(out.planes), self.nrows,
+                                                           self.ncols, _lib.current_stream_handle(out.device)))
+        return out
+
+    def equals(self, other) -> bool:
+        """True iff the decoded entries agree (canonicalizes internally)."""
+        if not isinstance(other, BitslicedMatrix) or other.field is not self.field:
+            return False
+        if (other.nrows, other.ncols) != (self.nrows, self.ncols):
+            return False
+        a = self.reduce_canonical().planes
+        b = other.reduce_canonical().planes.to(a.device)
+        return bool(torch.equal(a, b))
+
+    __eq__ = equals
+    __hash__ = None
+
+    def __repr__(self):
+        return f"BitslicedMatrix({self.field.name}, {self.nrows}x{self.ncols}, {self.device})"

@@ -1,0 +1,79 @@
+"""Full BASELINE-size checks (BASELINE.json configs 0-4, one GPU).
+
+At these sizes the bitsliced oracle is too slow, so the checks are:
+  * exact: C equals (A_f32 @ B_f32) mod p computed by cuBLAS fp32 with TF32 disabled -- exact,
+    since every partial sum is an integer below l*(p-1)^2 <= 294,912 < 2^24;
+  * size-independent: Freivalds' identity C x = A (B x) mod p for random x, computed on the host
+    in int64 from the unpacked matrices.
+Inputs are the DenseMatrix.random streams: A = seed 0, B = seed 1."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_0901_1413_b200 as sg
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+CONFIGS = [("f3", 1024, 1024, 1024), ("f5", 4096, 4096, 4096), ("gf4", 8192, 8192, 8192),
+           ("f7", 16384, 8192, 16384), ("f3", 32768, 32768, 32768)]
+FIELDS = {"f3": sg.F3, "f5": sg.F5, "f7": sg.F7, "gf4": sg.F4}
+
+
+def exact_gpu_product(fname, A, B):
+    """(A @ B) over the field with an exact fp32 GEMM, returned as dense uint8 (host)."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    m, n = A.shape[0], B.shape[1]
+    out = np.empty((m, n), dtype=np.uint8)
+    Bt = torch.from_numpy(B).cuda()
+    if fname == "gf4":
+        b0, b1 = (Bt & 1).float(), (Bt >> 1).float()
+    else:
+        bf = Bt.float()
+    step = 4096
+    for r0 in range(0, m, step):
+        a = torch.from_numpy(A[r0:r0 + step]).cuda()
+        if fname == "gf4":
+            a0, a1 = (a & 1).float(), (a >> 1).float()
+            p11 = a1 @ b1
+            c0 = torch.remainder(a0 @ b0 + p11, 2)
+            c1 = torch.remainder(a0 @ b1 + a1 @ b0 + p11, 2)
+            c = c0.to(torch.uint8) | (c1.to(torch.uint8) << 1)
+        else:
+            c = torch.remainder(a.float() @ bf, oracle.ORDER[fname]).to(torch.uint8)
+        out[r0:r0 + step] = c.cpu().numpy()
+    return out
+
+
+def freivalds(fname, A, B, C, trials=2):
+    rng = np.random.default_rng(0)
+    p = 2 if fname == "gf4" else oracle.ORDER[fname]
+    if fname == "gf4":  # check both coefficient planes as F2 products of the closed form
+        a0, a1 = (A & 1).astype(np.int64), (A >> 1).astype(np.int64)
+        b0, b1 = (B & 1).astype(np.int64), (B >> 1).astype(np.int64)
+        c0, c1 = (C & 1).astype(np.int64), (C >> 1).astype(np.int64)
+        for _ in range(trials):
+            x = rng.integers(0, 2, size=B.shape[1], dtype=np.int64)
+            bx0, bx1 = b0 @ x, b1 @ x
+            assert np.array_equal((c0 @ x) % 2, (a0 @ bx0 + a1 @ bx1) % 2)
+            assert np.array_equal((c1 @ x) % 2, (a0 @ bx1 + a1 @ bx0 + a1 @ bx1) % 2)
+        return
+    for _ in range(trials):
+        x = rng.integers(0, p, size=B.shape[1], dtype=np.int64)
+        bx = (B.astype(np.int64) @ x) % p
+        assert np.array_equal((C.astype(np.int64) @ x) % p, (A.astype(np.int64) @ bx) % p)
+
+
+@pytest.mark.parametrize("fname,m,l,n", CONFIGS)
+def test_baseline_config_exact(fname, m, l, n):
+    A = oracle.random_dense(fname, m, l, 0)
+    B = oracle.random_dense(fname, l, n, 1)
+    f = FIELDS[fname]
+    C = sg.m4rm_multiply(sg.BitslicedMatrix.from_dense(f, A), sg.BitslicedMatrix.from_dense(f, B), sg.M4rmParams(8))
+    Cd = C.to_dense()
+    freivalds(fname, A, B, Cd)
+    assert np.array_equal(Cd, exact_gpu_product(fname, A, B))
+    # the planes are canonical (pack of the dense result is the unique canonical packing)
+    if m * n <= 8192 * 8192:
+        assert np.array_equal(C.planes_numpy(), oracle.pack(fname, Cd))

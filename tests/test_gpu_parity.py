@@ -1,0 +1,279 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle and the reference's
+golden outputs.  Bar: bit-exact planes (F5/F7 outputs are canonical, compared against the
+canonicalized reference)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_0901_1413_b200 as sg
+from paper_0901_1413_b200 import _core_cuda, m4rm as m4rm_mod
+from tests import _golden
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = {"f2": sg.F2, "f3": sg.F3, "f5": sg.F5, "f7": sg.F7, "gf4": sg.F4}
+
+
+def gpu_multiply(fname, A, B, k=8):
+    f = FIELDS[fname]
+    Ag = sg.BitslicedMatrix.from_dense(f, A)
+    Bg = sg.BitslicedMatrix.from_dense(f, B)
+    return sg.m4rm_multiply(Ag, Bg, sg.M4rmParams(k))
+
+
+def expect(fname, A, B):
+    return oracle.pack(fname, oracle.dense_multiply(fname, A, B))
+
+
+@pytest.fixture(autouse=True)
+def _reset_override():
+    m4rm_mod.set_plan_override(0, 0)
+    yield
+    m4rm_mod.set_plan_override(0, 0)
+
+
+# ---------------------------------------------------------------- formulas, lane by lane
+def test_plane_kernels_exhaustive_on_device():
+    """Each device formula against kernels.KERNELS' exhaustive lane tables (kernels.py:466-509)."""
+    table = _golden.kernel_cases()
+    n_in = {"f3_add": (2, 2), "f3_sub": (2, 2), "f3_neg": (2, 0), "f5_add": (3, 3), "f5_double": (3, 0),
+            "f5_neg": (3, 0), "f5_reduce": (3, 0), "f7_add": (3, 3), "f7_double": (3, 0), "f7_neg": (3, 0),
+            "f7_reduce": (3, 0), "f5_fold5": (3, 1)}
+    for name, (nd, ns) in n_in.items():
+        info = table[name]
+        cases = info["cases"]
+        words = np.zeros(nd + ns, dtype=np.uint64)
+        for lane, (inp, _) in enumerate(cases):
+            for j, b in enumerate(inp):
+                if b:
+                    words[j] |= np.uint64(1 << lane)
+        dst = [torch.from_numpy(words[j:j + 1].view(np.int64).copy()).cuda() for j in range(nd)]
+        src = [torch.from_numpy(words[j:j + 1].view(np.int64).copy()).cuda() for j in range(nd, nd + ns)]
+        tail = (1 << len(cases)) - 1 if name in ("f7_neg",) else (1 << 64) - 1
+        _core_cuda._op(name, dst, src, tail=tail)
+        out = [int(t.cpu().numpy().view(np.uint64)[0]) for t in dst]
+        for lane, (inp, acceptable) in enumerate(cases):
+            bits = [(out[d] >> lane) & 1 for d in range(info["n_out"])]
+            assert bits in acceptable, (name, inp, bits)
+
+
+# ---------------------------------------------------------------- pack / unpack
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_pack_unpack_roundtrip(fname):
+    for (m, n) in [(1, 1), (3, 31), (5, 32), (7, 33), (2, 64), (9, 65), (4, 130), (33, 1000), (0, 5), (5, 0)]:
+        d = oracle.random_dense(fname, m, n, m * 131 + n)
+        M = sg.BitslicedMatrix.from_dense(FIELDS[fname], d)
+        assert np.array_equal(M.planes_numpy(), oracle.pack(fname, d)), (fname, m, n)
+        assert np.array_equal(M.to_dense(), d)
+
+
+def test_pack_rejects_out_of_range_on_device():
+    d = torch.tensor([[0, 1, 2, 3]], dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        sg.BitslicedMatrix.from_dense(sg.F3, d)
+
+
+def test_unpack_rejects_illegal_f3_pattern():
+    M = sg.BitslicedMatrix.zero(sg.F3, 1, 5)
+    M.planes[1, 0, 0] = 1  # sign without unit
+    with pytest.raises(ValueError):
+        M.to_dense()
+
+
+# ---------------------------------------------------------------- golden fixtures
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_m4rm_matches_reference_golden(fname):
+    for c in _golden.cases(fname):
+        C = gpu_multiply(fname, c["A"], c["B"], c["k"])
+        got = C.planes_numpy()
+        assert np.array_equal(got, oracle.canonicalize(fname, c["Craw"])), (fname, c["m"], c["l"], c["n"], c["k"])
+        if fname in ("f2", "f3", "gf4"):
+            assert np.array_equal(got, c["Craw"])
+        assert np.array_equal(C.to_dense(), c["C"])
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_spec3_random_grid(fname):
+    """200 random (m, l, n) <= 65 per field, exact."""
+    rng = np.random.default_rng(99)
+    for t in range(200):
+        m, l, n = (int(x) for x in rng.integers(1, 66, size=3))
+        A = oracle.random_dense(fname, m, l, 1000 + t)
+        B = oracle.random_dense(fname, l, n, 2000 + t)
+        C = gpu_multiply(fname, A, B)
+        assert np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, m, l, n)
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_k_invariance(fname):
+    A = oracle.random_dense(fname, 100, 257, 5)
+    B = oracle.random_dense(fname, 257, 300, 6)
+    want = expect(fname, A, B)
+    for k in range(1, 17):
+        assert np.array_equal(gpu_multiply(fname, A, B, k).planes_numpy(), want), (fname, k)
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_every_compiled_plan(fname):
+    """Force every rows-per-thread variant and several k-splits (split-K partial + reduce)."""
+    A = oracle.random_dense(fname, 700, 1000, 7)
+    B = oracle.random_dense(fname, 1000, 777, 8)
+    want = expect(fname, A, B)
+    for rt in (1, 2, 4, 8, 16):
+        for splits in (1, 2, 5, 16):
+            m4rm_mod.set_plan_override(rt, splits)
+            try:
+                C = gpu_multiply(fname, A, B)
+            except ValueError:
+                raise
+            except RuntimeError as e:
+                assert "no compiled" in str(e)
+                continue
+            assert np.array_equal(C.planes_numpy(), want), (fname, rt, splits)
+
+
+@pytest.mark.parametrize("fname,m,l,n", [("f3", 1024, 1024, 1024), ("f5", 1000, 3000, 700), ("f7", 513, 2049, 1500),
+                                         ("gf4", 1500, 1200, 1300), ("f2", 800, 4000, 900)])
+def test_medium_shapes_against_dense_oracle(fname, m, l, n):
+    A = oracle.random_dense(fname, m, l, 0)
+    B = oracle.random_dense(fname, l, n, 1)
+    C = gpu_multiply(fname, A, B)
+    assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
+
+
+def test_f3_1024_config0_against_bitsliced_oracle():
+    """BASELINE config 0: F3 1024^3, seeds 0/1, k=8, vs the restated reference path."""
+    A = oracle.random_dense("f3", 1024, 1024, 0)
+    B = oracle.random_dense("f3", 1024, 1024, 1)
+    ref = oracle.m4rm("f3", oracle.pack("f3", A), oracle.pack("f3", B), 1024, 1024, 8, threads=8)
+    assert np.array_equal(gpu_multiply("f3", A, B).planes_numpy(), ref)
+
+
+# ---------------------------------------------------------------- API semantics
+def test_spec_known_answers_on_gpu():
+    C = gpu_multiply("f3", np.array([[1, 2], [0, 1]]), np.array([[1, 1], [1, 0]]))
+    assert np.array_equal(C.to_dense(), [[0, 1], [1, 0]])
+    C = gpu_multiply("f7", np.array([[6]]), np.array([[6]]))
+    assert C.to_dense()[0, 0] == 1
+    C = gpu_multiply("gf4", np.array([[2]]), np.array([[2]]))
+    assert C.to_dense()[0, 0] == 3  # alpha * alpha = alpha + 1
+    B = oracle.random_dense("f5", 65, 65, 9)
+    C = gpu_multiply("f5", np.eye(65, dtype=np.uint8), B)
+    assert np.array_equal(C.to_dense(), B)
+
+
+def test_empty_and_degenerate_shapes():
+    for (m, l, n) in [(0, 5, 5), (5, 0, 5), (5, 5, 0), (1, 1, 1)]:
+        A = oracle.random_dense("f7", m, l, 1)
+        B = oracle.random_dense("f7", l, n, 2)
+        C = gpu_multiply("f7", A, B)
+        assert (C.nrows, C.ncols) == (m, n)
+        assert np.array_equal(C.planes_numpy(), expect("f7", A, B))
+
+
+def test_host_buffers_e2e_path():
+    for fname in FIELDS:
+        A = oracle.random_dense(fname, 300, 500, 3)
+        B = oracle.random_dense(fname, 500, 200, 4)
+        Ah = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, A), 500, device="cpu")
+        Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), 200, device="cpu")
+        C = sg.m4rm_multiply(Ah, Bh)
+        assert C.device.type == "cpu"
+        assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
+
+
+def test_elementwise_ops_match_dense():
+    for fname in ("f2", "f3", "f5", "f7", "gf4"):
+        f = FIELDS[fname]
+        p = oracle.CHAR[fname] if fname != "gf4" else 2
+        a = oracle.random_dense(fname, 13, 131, 1)
+        b = oracle.random_dense(fname, 13, 131, 2)
+        A, B = sg.BitslicedMatrix.from_dense(f, a), sg.BitslicedMatrix.from_dense(f, b)
+        if fname == "gf4":
+            assert np.array_equal(A.add(B).to_dense(), a ^ b)
+            for c in range(4):  # c * a over GF(4)
+                want = oracle.dense_multiply("gf4", a.reshape(-1, 1), np.array([[c]], np.uint8)).reshape(a.shape)
+                assert np.array_equal(A.scalar_mul(c).to_dense(), want)
+            continue
+        q = oracle.ORDER[fname]
+        assert np.array_equal(A.add(B).to_dense(), (a.astype(int) + b) % q)
+        assert np.array_equal(A.sub(B).to_dense(), (a.astype(int) - b) % q)
+        assert np.array_equal(A.neg().to_dense(), (-a.astype(int)) % q)
+        for c in range(q):
+            assert np.array_equal(A.scalar_mul(c).to_dense(), (a.astype(int) * c) % q)
+        # padding lanes stay zero
+        for M in (A.add(B), A.sub(B), A.neg()):
+            tailbits = M.planes_numpy()[:, :, -1] >> np.uint64(131 % 64)
+            assert not tailbits.any()
+
+
+def test_equals_canonicalizes():
+    M = sg.BitslicedMatrix.zero(sg.F5, 1, 3)
+    N = sg.BitslicedMatrix.zero(sg.F5, 1, 3)
+    M.set(0, 1, 1)
+    N.planes[1, 0, 0] = 2  # pattern 6 == 1 (mod 5) in column 1
+    N.planes[2, 0, 0] = 2
+    assert M.equals(N)
+    N.set(0, 2, 3)
+    assert not M.equals(N)
+
+
+def test_plugin_block_api_reproduces_product():
+    """The _core-style block API (build_table + m4rm_block_<f>) drives a whole product."""
+    for fname in ("f2", "f3", "f5", "f7"):
+        f = FIELDS[fname]
+        m, l, n, k = 70, 45, 130, 6
+        A = oracle.random_dense(fname, m, l, 11)
+        B = oracle.random_dense(fname, l, n, 12)
+        Ag, Bg = sg.BitslicedMatrix.from_dense(f, A), sg.BitslicedMatrix.from_dense(f, B)
+        C = torch.zeros_like(Ag.planes[:, :, :1].expand(-1, -1, (n + 63) // 64)).contiguous()
+        drv = getattr(_core_cuda, f"m4rm_block_{fname}")
+        for s in range((l + k - 1) // k):
+            T = sg.build_table(Bg, s, k)
+            kp = min(k, l - s * k)
+            drv(*[C[d] for d in range(f.bits)], *[Ag.planes[d] for d in range(f.bits)], s * k, kp,
+                *[T[d] for d in range(f.bits)], 0, m)
+        got = oracle.canonicalize(fname, C.cpu().numpy().view(np.uint64))
+        assert np.array_equal(got, expect(fname, A, B)), fname
+
+
+def test_plugin_accepts_numpy_planes():
+    a = oracle.pack("f3", oracle.random_dense("f3", 4, 100, 1))
+    b = oracle.pack("f3", oracle.random_dense("f3", 4, 100, 2))
+    want = oracle.pack("f3", (oracle.unpack("f3", a, 100).astype(int) + oracle.unpack("f3", b, 100)) % 3)
+    _core_cuda.f3_add(a[0], a[1], b[0], b[1])
+    assert np.array_equal(a, want)
+
+
+def test_ext_multiply_matches_karatsuba_golden():
+    for c in _golden.cases("gf4"):
+        f2 = [sg.BitslicedMatrix.from_dense(sg.F2, (c["A"] >> i) & 1) for i in range(2)]
+        g2 = [sg.BitslicedMatrix.from_dense(sg.F2, (c["B"] >> i) & 1) for i in range(2)]
+        C = sg.ext_multiply(sg.ExtMatrix(sg.F4, f2), sg.ExtMatrix(sg.F4, g2))
+        got = np.concatenate([C.coeffs[0].planes_numpy(), C.coeffs[1].planes_numpy()])
+        assert np.array_equal(got, c["Craw"])
+
+
+def test_checker_detects_a_corrupted_result():
+    """Fault injection: flip one table-sourced bit of a correct result; parity must fail."""
+    A = oracle.random_dense("f5", 64, 64, 1)
+    B = oracle.random_dense("f5", 64, 64, 2)
+    C = gpu_multiply("f5", A, B)
+    good = C.planes_numpy()
+    assert np.array_equal(good, expect("f5", A, B))
+    C.planes[0, 3, 0] ^= 1 << 5
+    assert not np.array_equal(C.planes_numpy(), expect("f5", A, B))
+
+
+def test_stream_ordering_on_side_stream():
+    A = oracle.random_dense("f7", 300, 900, 1)
+    B = oracle.random_dense("f7", 900, 300, 2)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        Ag = sg.BitslicedMatrix.from_dense(sg.F7, A)
+        Bg = sg.BitslicedMatrix.from_dense(sg.F7, B)
+        C = sg.m4rm_multiply(Ag, Bg)
+    s.synchronize()
+    assert np.array_equal(C.planes_numpy(), expect("f7", A, B))
