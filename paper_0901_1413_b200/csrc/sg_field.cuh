@@ -18,28 +18,40 @@ enum Field : int { F2 = 0, F3 = 1, F5 = 2, F7 = 3, GF4 = 4 };
 
 typedef uint32_t u32;
 
+// One LOP3 (any 3-input boolean function; IMM = F(0xF0, 0xCC, 0xAA)).  Not volatile: the
+// compiler schedules it freely.
+template <int IMM> __device__ __forceinline__ u32 lop3(u32 a, u32 b, u32 c) {
+  u32 d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(IMM));
+  return d;
+}
+constexpr int LOP_XOR3 = 0x96, LOP_MAJ = 0xE8, LOP_AND2 = 0xC0;
+
 template <int F> struct Traits;
 // R = bit planes per element; NI = table lookups per (row, k-block) = basis size;
-template <> struct Traits<F2>  { static constexpr int R = 1, NI = 1; };
-template <> struct Traits<F3>  { static constexpr int R = 2, NI = 2; };
-template <> struct Traits<F5>  { static constexpr int R = 3, NI = 3; };
-template <> struct Traits<F7>  { static constexpr int R = 3, NI = 3; };
-template <> struct Traits<GF4> { static constexpr int R = 2, NI = 2; };
+// RS = planes of the M4RM kernel's row accumulator (F5 accumulates mod 15 in 4 planes).
+template <> struct Traits<F2>  { static constexpr int R = 1, NI = 1, RS = 1; };
+template <> struct Traits<F3>  { static constexpr int R = 2, NI = 2, RS = 2; };
+template <> struct Traits<F5>  { static constexpr int R = 3, NI = 3, RS = 4; };
+template <> struct Traits<F7>  { static constexpr int R = 3, NI = 3, RS = 3; };
+template <> struct Traits<GF4> { static constexpr int R = 2, NI = 2, RS = 2; };
 
 // ---------------------------------------------------------------- F3
-// x += y : the two shared subexpressions u = xu^ys, v = xs^yu make this six 2-input ops.
+// x += y and x -= y in three LOP3 each (a minimum found by exhaustive search over LOP3
+// networks, tools/lop3/search.c; the reference spends six 2-input ops on each,
+// kernels.py:151-168).  Both share w = F(xu, xs, ys).  Valid on the three legal patterns;
+// the illegal pattern 10 is a don't-care (SPEC.md design decisions).
 __device__ __forceinline__ void f3_add(u32& xu, u32& xs, u32 yu, u32 ys) {
-  u32 u = xu ^ ys, v = xs ^ yu;
-  u32 ru = (u ^ xs) | (v ^ ys);
-  xs = u & v;
+  const u32 w = lop3<0x61>(xu, xs, ys);
+  const u32 ru = lop3<0x7c>(xu, yu, w);
+  xs = lop3<0x24>(xs, yu, w);
   xu = ru;
 }
-// x -= y : six 2-input ops (one fewer than neg-then-add).
 __device__ __forceinline__ void f3_sub(u32& xu, u32& xs, u32 yu, u32 ys) {
-  u32 t = xu ^ yu;
-  u32 rs = (t ^ ys) & (yu ^ xs);
-  xu = t | (xs ^ ys);
-  xs = rs;
+  const u32 w = lop3<0x61>(xu, xs, ys);
+  const u32 ru = lop3<0xbc>(xu, yu, w);
+  xs = lop3<0x28>(xs, yu, w);
+  xu = ru;
 }
 __device__ __forceinline__ void f3_neg(u32& /*xu*/, u32& xs, u32 xu_in) { xs ^= xu_in; }
 
@@ -63,23 +75,23 @@ __device__ __forceinline__ void fold5(u32 s0, u32 s1, u32 s2, u32 s3, u32& r0, u
   r1 = (r2 & s0) ^ (s3 ^ s1);
   r0 = (t ^ s2) | (r1 & s3);
 }
-// 8 == 1 (mod 7): end-around carry; the sum of two lanes <= 14 never carries out again
-__device__ __forceinline__ void fold7(u32 s0, u32 s1, u32 s2, u32 s3, u32& r0, u32& r1, u32& r2) {
-  u32 c0 = s0 & s3;
-  r0 = s0 ^ s3;
-  r1 = s1 ^ c0;
-  r2 = s2 ^ (s1 & c0);
-}
-
 __device__ __forceinline__ void f5_add(u32& x0, u32& x1, u32& x2, u32 y0, u32 y1, u32 y2) {
   u32 s0, s1, s2, s3;
   add3(x0, x1, x2, y0, y1, y2, s0, s1, s2, s3);
   fold5(s0, s1, s2, s3, x0, x1, x2);
 }
+// x += y mod 7 as a 3-bit one's-complement (end-around-carry) adder: 8 LOP3.  co = [x+y >= 8]
+// re-enters at bit 0 (8 == 1 mod 7); x + y + co never carries out again (<= 15 - 8).  Same
+// residues as the reference's 17-op adder chain + fold (_core_py.py:65-88), any of 0/7 for zero.
 __device__ __forceinline__ void f7_add(u32& x0, u32& x1, u32& x2, u32 y0, u32 y1, u32 y2) {
-  u32 s0, s1, s2, s3;
-  add3(x0, x1, x2, y0, y1, y2, s0, s1, s2, s3);
-  fold7(s0, s1, s2, s3, x0, x1, x2);
+  const u32 c0 = lop3<LOP_AND2>(x0, y0, 0u);
+  const u32 c1 = lop3<LOP_MAJ>(x1, y1, c0);
+  const u32 co = lop3<LOP_MAJ>(x2, y2, c1);
+  const u32 k1 = lop3<LOP_MAJ>(x0, y0, co);
+  const u32 k2 = lop3<LOP_MAJ>(x1, y1, k1);
+  x0 = lop3<LOP_XOR3>(x0, y0, co);
+  x2 = lop3<LOP_XOR3>(x2, y2, k2);
+  x1 = lop3<LOP_XOR3>(x1, y1, k1);
 }
 // -x mod 5 on 3-bit lanes (4 ops)
 __device__ __forceinline__ void f5_neg(u32& p0, u32& p1, u32& p2) {
@@ -117,6 +129,34 @@ __device__ __forceinline__ void f5_reduce(u32& p0, u32& p1, u32& p2) {
 __device__ __forceinline__ void f7_reduce(u32& p0, u32& p1, u32& p2) {
   u32 t = p0 & p1 & p2;
   p0 ^= t; p1 ^= t; p2 ^= t;
+}
+
+// ---------------------------------------------------------------- F5 accumulator (mod 15)
+// The M4RM kernel accumulates F5 rows as 4-bit lanes modulo 15 (a multiple of 5): doubling is
+// a free 4-bit rotation (16 == 1 mod 15) and the add is an 11-LOP3 one's-complement adder,
+// against the reference's 5-op double + 20-op add per Horner step (_core_py.py:116-140).
+// Table entries stay 3-bit F5 values (any representative mod 5 is a valid mod-15 input).
+__device__ __forceinline__ void add15(u32& a0, u32& a1, u32& a2, u32& a3, u32 b0, u32 b1, u32 b2, u32 b3) {
+  const u32 c0 = a0 & b0;
+  const u32 c1 = lop3<LOP_MAJ>(a1, b1, c0);
+  const u32 c2 = lop3<LOP_MAJ>(a2, b2, c1);
+  const u32 co = lop3<LOP_MAJ>(a3, b3, c2);
+  const u32 k1 = lop3<LOP_MAJ>(a0, b0, co);
+  const u32 k2 = lop3<LOP_MAJ>(a1, b1, k1);
+  const u32 k3 = lop3<LOP_MAJ>(a2, b2, k2);
+  a0 = a0 ^ b0 ^ co;
+  a1 = a1 ^ b1 ^ k1;
+  a2 = a2 ^ b2 ^ k2;
+  a3 = a3 ^ b3 ^ k3;
+}
+// 4-bit lane value 0..15 -> canonical F5 residue 0..4 in 3 planes (6 LOP3, searched)
+__device__ __forceinline__ void mod15_to_f5(u32 v0, u32 v1, u32 v2, u32 v3, u32& r0, u32& r1, u32& r2) {
+  const u32 w4 = lop3<0x07>(v0, v1, v2);
+  const u32 w5 = lop3<0x18>(v0, v1, v2);
+  const u32 w6 = lop3<0x2c>(v1, v3, w5);
+  r0 = lop3<0x29>(v2, w4, w6);
+  r1 = lop3<0x14>(v1, v3, w5);
+  r2 = lop3<0x24>(v0, v2, w6);
 }
 
 // ---------------------------------------------------------------- generic row helpers

@@ -46,59 +46,69 @@ template <int F> __device__ __forceinline__ V<F> vzero() {
   return v;
 }
 
+// Row accumulator of one lane: 4 words x RS planes.
+template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
+
 // One (row, k-block) update of the 4 C words a lane owns.  tl = this lane's replica base,
-// TPL = uint4 stride between table planes, g[] = the basis indices of the row.
+// TPL = uint4 stride between table planes, e = the byte offsets of the basis entries.
 template <int F, int TPL>
-__device__ __forceinline__ void accumulate(V<F> (&c)[4], const uint4* __restrict__ tl, const u32 (&g)[3]) {
-  constexpr int STRIDE = ENTRY_BYTES / 16;
+__device__ __forceinline__ void accumulate(Acc<F>& c, const unsigned char* __restrict__ tl, const u32 (&e)[3]) {
+  auto T = [&](int d, int i) { return *reinterpret_cast<const uint4*>(tl + e[i] + d * TPL * 16); };
   if constexpr (F == F2) {
-    const uint4 p = tl[g[0] * STRIDE];
-    c[0].p[0] ^= p.x; c[1].p[0] ^= p.y; c[2].p[0] ^= p.z; c[3].p[0] ^= p.w;
+    const uint4 p = T(0, 0);
+    c.w[0][0] ^= p.x; c.w[1][0] ^= p.y; c.w[2][0] ^= p.z; c.w[3][0] ^= p.w;
   } else if constexpr (F == F3) {
-    // basis {1, -1}: C += T[pos]; C -= T[neg]   (_core_py.py:213-222)
-    const uint4 pu = tl[g[0] * STRIDE], ps = tl[TPL + g[0] * STRIDE];
-    const uint4 nu = tl[g[1] * STRIDE], ns = tl[TPL + g[1] * STRIDE];
-    f3_add(c[0].p[0], c[0].p[1], pu.x, ps.x);
-    f3_add(c[1].p[0], c[1].p[1], pu.y, ps.y);
-    f3_add(c[2].p[0], c[2].p[1], pu.z, ps.z);
-    f3_add(c[3].p[0], c[3].p[1], pu.w, ps.w);
-    f3_sub(c[0].p[0], c[0].p[1], nu.x, ns.x);
-    f3_sub(c[1].p[0], c[1].p[1], nu.y, ns.y);
-    f3_sub(c[2].p[0], c[2].p[1], nu.z, ns.z);
-    f3_sub(c[3].p[0], c[3].p[1], nu.w, ns.w);
-  } else if constexpr (F == GF4) {
-    // power basis {1, x}: C += T[g0] + x*T[g1],  x*(t0, t1) = (t1, t0 ^ t1)
-    const uint4 p0 = tl[g[0] * STRIDE], p1 = tl[TPL + g[0] * STRIDE];
-    const uint4 q0 = tl[g[1] * STRIDE], q1 = tl[TPL + g[1] * STRIDE];
-    c[0].p[0] ^= p0.x ^ q1.x; c[0].p[1] ^= p1.x ^ q0.x ^ q1.x;
-    c[1].p[0] ^= p0.y ^ q1.y; c[1].p[1] ^= p1.y ^ q0.y ^ q1.y;
-    c[2].p[0] ^= p0.z ^ q1.z; c[2].p[1] ^= p1.z ^ q0.z ^ q1.z;
-    c[3].p[0] ^= p0.w ^ q1.w; c[3].p[1] ^= p1.w ^ q0.w ^ q1.w;
-  } else {
-    // F5 / F7, basis {1, 2, 4} with Horner: acc = T[g2]; acc = 2acc + T[g1]; acc = 2acc + T[g0]
-    // (_core_py.py:241-255); C += acc.
-    const uint4 a0 = tl[g[2] * STRIDE], a1 = tl[TPL + g[2] * STRIDE], a2 = tl[2 * TPL + g[2] * STRIDE];
-    const uint4 b0 = tl[g[1] * STRIDE], b1 = tl[TPL + g[1] * STRIDE], b2 = tl[2 * TPL + g[1] * STRIDE];
-    const uint4 e0 = tl[g[0] * STRIDE], e1 = tl[TPL + g[0] * STRIDE], e2 = tl[2 * TPL + g[0] * STRIDE];
-    const u32 A0[4] = {a0.x, a0.y, a0.z, a0.w}, A1[4] = {a1.x, a1.y, a1.z, a1.w}, A2[4] = {a2.x, a2.y, a2.z, a2.w};
-    const u32 B0[4] = {b0.x, b0.y, b0.z, b0.w}, B1[4] = {b1.x, b1.y, b1.z, b1.w}, B2[4] = {b2.x, b2.y, b2.z, b2.w};
-    const u32 E0[4] = {e0.x, e0.y, e0.z, e0.w}, E1[4] = {e1.x, e1.y, e1.z, e1.w}, E2[4] = {e2.x, e2.y, e2.z, e2.w};
+    // basis {1, -1}: C += T[pos]; C -= T[neg]   (_core_py.py:213-222), 6 LOP3 per word
+    const uint4 pu = T(0, 0), ps = T(1, 0), nu = T(0, 1), ns = T(1, 1);
+    const u32 PU[4] = {pu.x, pu.y, pu.z, pu.w}, PS[4] = {ps.x, ps.y, ps.z, ps.w};
+    const u32 NU[4] = {nu.x, nu.y, nu.z, nu.w}, NS[4] = {ns.x, ns.y, ns.z, ns.w};
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      u32 x0 = A0[w], x1 = A1[w], x2 = A2[w];
-      if constexpr (F == F5) {
-        f5_double(x0, x1, x2);
-        f5_add(x0, x1, x2, B0[w], B1[w], B2[w]);
-        f5_double(x0, x1, x2);
-        f5_add(x0, x1, x2, E0[w], E1[w], E2[w]);
-        f5_add(c[w].p[0], c[w].p[1], c[w].p[2], x0, x1, x2);
-      } else {
-        f7_double(x0, x1, x2);
-        f7_add(x0, x1, x2, B0[w], B1[w], B2[w]);
-        f7_double(x0, x1, x2);
-        f7_add(x0, x1, x2, E0[w], E1[w], E2[w]);
-        f7_add(c[w].p[0], c[w].p[1], c[w].p[2], x0, x1, x2);
+      f3_add(c.w[w][0], c.w[w][1], PU[w], PS[w]);
+      f3_sub(c.w[w][0], c.w[w][1], NU[w], NS[w]);
+    }
+  } else if constexpr (F == GF4) {
+    // power basis {1, x}: C += T[g0] + x*T[g1],  x*(t0, t1) = (t1, t0 ^ t1)
+    const uint4 p0 = T(0, 0), p1 = T(1, 0), q0 = T(0, 1), q1 = T(1, 1);
+    c.w[0][0] ^= p0.x ^ q1.x; c.w[0][1] ^= p1.x ^ q0.x ^ q1.x;
+    c.w[1][0] ^= p0.y ^ q1.y; c.w[1][1] ^= p1.y ^ q0.y ^ q1.y;
+    c.w[2][0] ^= p0.z ^ q1.z; c.w[2][1] ^= p1.z ^ q0.z ^ q1.z;
+    c.w[3][0] ^= p0.w ^ q1.w; c.w[3][1] ^= p1.w ^ q0.w ^ q1.w;
+  } else {
+    // F5 / F7, basis {1, 2, 4}: C += T[g0] + 2*T[g1] + 4*T[g2] (the reference's Horner form,
+    // _core_py.py:241-255, reassociated); doubling is a plane rotation in both accumulators.
+    const uint4 a0 = T(0, 0), a1 = T(1, 0), a2 = T(2, 0);
+    const uint4 b0 = T(0, 1), b1 = T(1, 1), b2 = T(2, 1);
+    const uint4 d0 = T(0, 2), d1 = T(1, 2), d2 = T(2, 2);
+    const u32 X0[4] = {a0.x, a0.y, a0.z, a0.w}, X1[4] = {a1.x, a1.y, a1.z, a1.w}, X2[4] = {a2.x, a2.y, a2.z, a2.w};
+    const u32 Y0[4] = {b0.x, b0.y, b0.z, b0.w}, Y1[4] = {b1.x, b1.y, b1.z, b1.w}, Y2[4] = {b2.x, b2.y, b2.z, b2.w};
+    const u32 Z0[4] = {d0.x, d0.y, d0.z, d0.w}, Z1[4] = {d1.x, d1.y, d1.z, d1.w}, Z2[4] = {d2.x, d2.y, d2.z, d2.w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      u32* q = c.w[w];
+      if constexpr (F == F7) {  // 2y = (y2, y0, y1), 4z = (z1, z2, z0) mod 7; 3 x 8 LOP3
+        f7_add(q[0], q[1], q[2], X0[w], X1[w], X2[w]);
+        f7_add(q[0], q[1], q[2], Y2[w], Y0[w], Y1[w]);
+        f7_add(q[0], q[1], q[2], Z1[w], Z2[w], Z0[w]);
+      } else {  // mod 15: x = (x0,x1,x2,0), 2y = (0,y0,y1,y2), 4z = (z2,0,z0,z1)
+        add15(q[0], q[1], q[2], q[3], X0[w], X1[w], X2[w], 0u);
+        add15(q[0], q[1], q[2], q[3], 0u, Y0[w], Y1[w], Y2[w]);
+        add15(q[0], q[1], q[2], q[3], Z2[w], 0u, Z0[w], Z1[w]);
       }
+    }
+  }
+}
+
+// Accumulator -> output planes (canonical for the final C; F5 always leaves mod 15 here).
+template <int F> __device__ __forceinline__ void finish(const u32 (&q)[Traits<F>::RS], u32 (&o)[Traits<F>::R],
+                                                        bool canonical) {
+  if constexpr (F == F5) {
+    mod15_to_f5(q[0], q[1], q[2], q[3], o[0], o[1], o[2]);
+  } else {
+#pragma unroll
+    for (int d = 0; d < Traits<F>::R; ++d) o[d] = q[d];
+    if constexpr (F == F7) {
+      if (canonical) f7_reduce(o[0], o[1], o[2]);
     }
   }
 }
@@ -160,13 +170,15 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
   cp_async_wait<1>();
   __syncthreads();
 
-  V<F> c[RT][4];
+  Acc<F> c[RT];
 #pragma unroll
   for (int t = 0; t < RT; ++t)
 #pragma unroll
-    for (int w = 0; w < 4; ++w) c[t][w] = vzero<F>();
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int d = 0; d < Traits<F>::RS; ++d) c[t].w[w][d] = 0u;
 
-  const uint4* tl = tab + (tid & (COPIES - 1));
+  const unsigned char* tl = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
 
   for (int s = s_begin; s < s_end; ++s) {
     // ---- phase 1: half tables from the staged B rows
@@ -233,21 +245,24 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
       const int w0 = col0 >> 5, sh = col0 & 31;
       const u32* aw0 = ast + (w0 & 1) * R * ROWS;
       const u32* aw1 = ast + ((w0 + 1) & 1) * R * ROWS;
+      const u32 sel = 0x4440u | (u32)(sh >> 3);  // PRMT: byte sh/8 of x, zero-extended
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int lr = t * NT + tid;
-        u32 g[3] = {0u, 0u, 0u};
+        u32 e[3] = {0u, 0u, 0u};
 #pragma unroll
         for (int d = 0; d < R; ++d) {
           u32 x = aw0[d * ROWS + lr];
-          if constexpr (32 % K == 0) {
-            x >>= sh;
+          if constexpr (K == 8) {
+            x = __byte_perm(x, 0u, sel);
+          } else if constexpr (32 % K == 0) {
+            x = (x >> sh) & (E - 1);
           } else {
-            x = (sh + K > 32) ? __funnelshift_r(x, aw1[d * ROWS + lr], sh) : (x >> sh);
+            x = ((sh + K > 32) ? __funnelshift_r(x, aw1[d * ROWS + lr], sh) : (x >> sh)) & (E - 1);
           }
-          g[d] = x & (E - 1);
+          e[d] = x * ENTRY_BYTES;
         }
-        accumulate<F, TPL>(c[t], tl, g);
+        accumulate<F, TPL>(c[t], tl, e);
       }
     }
   }
@@ -263,15 +278,14 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
   for (int t = 0; t < RT; ++t) {
     const int64_t row = row0 + t * NT + tid;
     if (row < a.m) {
-      if (!a.partial) {
+      u32 o[4][R];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) vcanon<F>(c[t][w]);
-      }
+      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], !a.partial);
 #pragma unroll
       for (int d = 0; d < R; ++d) {
         u32* dst = out + ((int64_t)d * rows_out + row) * a.wc32 + word0;
-        if (word0 < a.wc32) *reinterpret_cast<uint2*>(dst) = make_uint2(c[t][0].p[d], c[t][1].p[d]);
-        if (word0 + 2 < a.wc32) *reinterpret_cast<uint2*>(dst + 2) = make_uint2(c[t][2].p[d], c[t][3].p[d]);
+        if (word0 < a.wc32) *reinterpret_cast<uint2*>(dst) = make_uint2(o[0][d], o[1][d]);
+        if (word0 + 2 < a.wc32) *reinterpret_cast<uint2*>(dst + 2) = make_uint2(o[2][d], o[3][d]);
       }
     }
   }

@@ -15,6 +15,17 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+// Whole-launch span from %globaltimer (min start, max end over CTAs) and the SM clock from
+// CTA 0's clock64 / globaltimer ratio: rate = total work / (span x clock) / SMs.
+__device__ void record_span(unsigned long long* st, long long c0, long long c1, uint64_t t0, uint64_t t1) {
+  atomicMin(&st[0], (unsigned long long)t0);
+  atomicMax(&st[1], (unsigned long long)t1);
+  if (blockIdx.x == 0) {
+    st[2] = (unsigned long long)(c1 - c0);
+    st[3] = (unsigned long long)(t1 - t0);
+  }
+}
+
 __global__ void lop3_probe_kernel(uint32_t* out, unsigned long long* stats, int iters, uint32_t seed) {
   uint32_t v[8];
 #pragma unroll
@@ -36,10 +47,7 @@ __global__ void lop3_probe_kernel(uint32_t* out, unsigned long long* stats, int 
 #pragma unroll
   for (int c = 0; c < 8; ++c) acc ^= v[c];
   if (acc == 0x12345678u) out[threadIdx.x] = acc;
-  if (threadIdx.x == 0) {
-    atomicAdd(&stats[0], (unsigned long long)(c1 - c0));
-    atomicAdd(&stats[1], (unsigned long long)(t1 - t0));
-  }
+  if (threadIdx.x == 0) record_span(stats, c0, c1, t0, t1);
 }
 
 __global__ void lds_probe_kernel(uint32_t* out, unsigned long long* stats, int iters) {
@@ -64,10 +72,31 @@ __global__ void lds_probe_kernel(uint32_t* out, unsigned long long* stats, int i
   const long long c1 = clock64();
   const uint64_t t1 = gtimer();
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) out[threadIdx.x] = acc.x;
-  if (threadIdx.x == 0) {
-    atomicAdd(&stats[0], (unsigned long long)(c1 - c0));
-    atomicAdd(&stats[1], (unsigned long long)(t1 - t0));
+  if (threadIdx.x == 0) record_span(stats, c0, c1, t0, t1);
+}
+
+static int run_probe(bool lop3, int sms, uint32_t* out, unsigned long long* stats, int rep, double* rate,
+                     double* mhz) {
+  const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+  if (cudaMemcpy(stats, init, sizeof init, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+  double work = 0;
+  if (lop3) {
+    const int tpb = 256, per_sm = 8, iters = 2048;
+    lop3_probe_kernel<<<sms * per_sm, tpb>>>(out, stats, iters, rep + 1);
+    work = (double)sms * per_sm * tpb * iters * 16 * 8;
+  } else {
+    const int tpb = 512, per_sm = 3, iters = 2048;
+    lds_probe_kernel<<<sms * per_sm, tpb, 65536>>>(out, stats, iters);
+    work = (double)sms * per_sm * tpb * iters * 8 * 16;
   }
+  unsigned long long h[4];
+  if (cudaMemcpy(h, stats, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  const double span_ns = (double)(h[1] - h[0]);
+  const double f_ghz = h[3] ? (double)h[2] / (double)h[3] : 0.0;
+  if (span_ns <= 0 || f_ghz <= 0) return -1;
+  *rate = work / (span_ns * f_ghz) / sms;
+  *mhz = f_ghz * 1e3;
+  return 0;
 }
 
 int probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_sm, double* sm_mhz) {
@@ -77,35 +106,17 @@ int probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_s
   uint32_t* out = nullptr;
   unsigned long long* stats = nullptr;
   if (cudaMalloc(&out, 1 << 16) != cudaSuccess) return -1;
-  if (cudaMalloc(&stats, 16) != cudaSuccess) { cudaFree(out); return -1; }
-  double best_lop3 = 0, best_lds = 0, mhz = 0;
-  // LOP3: 8 warps x 4 CTAs per SM; per-SM rate = ops per CTA * CTAs per SM / cycles
-  for (int rep = 0; rep < 3; ++rep) {
-    const int tpb = 256, per_sm = 8, iters = 2048;
-    cudaMemset(stats, 0, 16);
-    lop3_probe_kernel<<<sms * per_sm, tpb>>>(out, stats, iters, rep + 1);
-    unsigned long long h[2];
-    if (cudaMemcpy(h, stats, 16, cudaMemcpyDeviceToHost) != cudaSuccess) break;
-    const double cyc = (double)h[0] / (sms * per_sm), ns = (double)h[1] / (sms * per_sm);
-    const double ops_per_cta = (double)tpb * iters * 16 * 8;
-    const double r = ops_per_cta * per_sm / cyc;
-    if (r > best_lop3) { best_lop3 = r; mhz = cyc / ns * 1e3; }
-  }
+  if (cudaMalloc(&stats, 32) != cudaSuccess) { cudaFree(out); return -1; }
   cudaFuncSetAttribute(lds_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  double best_lop3 = 0, best_lds = 0, mhz = 0;
   for (int rep = 0; rep < 3; ++rep) {
-    const int tpb = 512, per_sm = 3, iters = 2048;
-    cudaMemset(stats, 0, 16);
-    lds_probe_kernel<<<sms * per_sm, tpb, 65536>>>(out, stats, iters);
-    unsigned long long h[2];
-    if (cudaMemcpy(h, stats, 16, cudaMemcpyDeviceToHost) != cudaSuccess) break;
-    const double cyc = (double)h[0] / (sms * per_sm);
-    const double bytes_per_cta = (double)tpb * iters * 8 * 16;
-    const double r = bytes_per_cta * per_sm / cyc;
-    if (r > best_lds) best_lds = r;
+    double r, f;
+    if (run_probe(true, sms, out, stats, rep, &r, &f) == 0 && r > best_lop3) { best_lop3 = r; mhz = f; }
+    if (run_probe(false, sms, out, stats, rep, &r, &f) == 0 && r > best_lds) best_lds = r;
   }
   cudaFree(out);
   cudaFree(stats);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  if (cudaGetLastError() != cudaSuccess || best_lop3 <= 0 || best_lds <= 0) return -1;
   *lop3_per_clk_sm = best_lop3;
   *lds_bytes_per_clk_sm = best_lds;
   *sm_mhz = mhz;
