@@ -129,8 +129,10 @@ int sg_m4rm_block(int field, uint64_t* const* C, int64_t c_words, const uint64_t
 
 /* Introspection and measurement. */
 int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta, int* splits,
-            int* ctas, int* kernel_index);
-int sg_set_plan_override(int rows_per_thread, int splits); /* 0 = automatic */
+            int* ctas, int* kernel_index, int* pipelined, int* threads);
+/* force rows per thread / k-splits / threads per CTA (0 = automatic) and the pipelined
+ * schedule (-1 = automatic) */
+int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads);
 int sg_set_timing(int enable);                              /* event-time each internal launch */
 int sg_last_timing(double* transpose_ms, double* m4rm_ms, double* reduce_ms);
 int64_t sg_launch_count(void);                              /* kernels launched by this library */

@@ -68,8 +68,8 @@ def load():
         "sg_m4rm_host": ([i32, vp, vp, vp, i64, i64, i64, i32, i32], i32),
         "sg_build_table": ([i32, pp, i64, i64, i32, i64, pp, vp], i32),
         "sg_m4rm_block": ([i32, pp, i64, pp, i64, i64, i32, pp, i64, i64, vp], i32),
-        "sg_plan": ([i32, i64, i64, i64, i32, ip, ip, ip, ip], i32),
-        "sg_set_plan_override": ([i32, i32], i32),
+        "sg_plan": ([i32, i64, i64, i64, i32, ip, ip, ip, ip, ip, ip], i32),
+        "sg_set_plan_override": ([i32, i32, i32, i32], i32),
         "sg_set_timing": ([i32], i32),
         "sg_last_timing": ([dp, dp, dp], i32),
         "sg_launch_count": ([], i64),

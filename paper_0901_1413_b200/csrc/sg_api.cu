@@ -20,7 +20,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
-int g_override_rt = 0, g_override_splits = 0;
+int g_override_rt = 0, g_override_splits = 0, g_override_pipe = -1, g_override_threads = 0;
 bool g_timing = false;
 double g_last_ms[3] = {0, 0, 0};
 std::mutex g_mu;
@@ -107,6 +107,7 @@ struct Plan {
   int K = 8, splits = 1, bps = 0, nblocks = 0;
   int64_t mpad = 0;
   int wa32 = 0, wc32 = 0;
+  int at_words = 0, at_planes = 0;  // staged index array: k=8 packed words (1 plane), else A^T planes
   dim3 grid;
   double est_clk = 0;
 };
@@ -138,12 +139,17 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
     KernelInfo* ki = m4rm_kernel_at(i);
     if (ki->field != field || ki->k != K) continue;
     if (g_override_rt && ki->rt != g_override_rt) continue;
+    if (g_override_pipe >= 0 && (int)ki->pipe != g_override_pipe) continue;
+    if (g_override_threads && ki->threads != g_override_threads) continue;
+    if (ki->occupancy < 1) continue;  // does not fit this device
     const int rows = ki->rt * ki->threads;
     const int64_t rgroups = (m + rows - 1) / rows;
     const double E = (double)(1 << K);
-    const double alu = (rows * lane_alu + E * entry_alu) / 64.0;
-    const double smem = (rows * lane_smem + E * R * ENTRY_BYTES + rows * R * 4.0) / 128.0;
-    const double t_block = std::max(alu, smem) + 350.0;
+    const double alu_l = rows * lane_alu / 64.0, alu_t = E * entry_alu / 64.0;
+    const double smem_l = (rows * lane_smem + rows * R * 4.0) / 128.0, smem_t = E * R * ENTRY_BYTES / 128.0;
+    // serialized schedule: table build, then lookups; pipelined: both share the pipes
+    const double t_block = ki->pipe ? std::max(alu_l + alu_t, smem_l + smem_t) + 150.0
+                                    : std::max(alu_l, smem_l) + std::max(alu_t, smem_t) + 400.0;
     const int occ = std::max(1, ki->occupancy);
     const int max_splits = std::max(1, std::min(nblocks, 64));
     for (int sp = 1; sp <= max_splits; ++sp) {
@@ -175,6 +181,14 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
   best.nblocks = nblocks;
   best.wa32 = (int)wa32;
   best.wc32 = (int)wc32;
+  if (K == 8) {
+    const int rpw = field == SG_F2 ? 4 : (field == SG_F5 || field == SG_F7) ? 1 : 2;
+    best.at_words = (nblocks + rpw - 1) / rpw;
+    best.at_planes = 1;
+  } else {
+    best.at_words = (int)wa32;
+    best.at_planes = R;
+  }
   if (best.grid.y > 65535) return fail(SG_EUNSUPPORTED, "too many row groups for one launch");
   *out = best;
   return SG_OK;
@@ -182,7 +196,7 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
 
 int64_t workspace_bytes_for(const Plan& p, int field) {
   const int R = planes(field);
-  int64_t b = (int64_t)R * p.wa32 * p.mpad * 4;
+  int64_t b = (int64_t)p.at_planes * p.at_words * p.mpad * 4;
   b = (b + 255) / 256 * 256;
   if (p.splits > 1) b += (int64_t)p.splits * R * p.mpad * p.wc32 * 4;
   return std::max<int64_t>(b, 256);
@@ -208,10 +222,12 @@ const char* sg_last_error(void) { return g_err.c_str(); }
 int sg_field_planes(int field) { return valid_field(field) ? planes(field) : -1; }
 int64_t sg_launch_count(void) { return g_launches.load(); }
 
-int sg_set_plan_override(int rows_per_thread, int splits) {
+int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads) {
   std::lock_guard<std::mutex> lk(g_mu);
+  g_override_threads = threads;
   g_override_rt = rows_per_thread;
   g_override_splits = splits;
+  g_override_pipe = pipe < 0 ? -1 : (pipe ? 1 : 0);
   return SG_OK;
 }
 
@@ -332,7 +348,7 @@ int64_t sg_m4rm_workspace_bytes(int field, int64_t m, int64_t l, int64_t n, int 
 }
 
 int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta, int* splits, int* ctas,
-            int* kernel_index) {
+            int* kernel_index, int* pipelined, int* threads) {
   int rc = check_mul_args(field, (void*)1, (void*)1, (void*)1, m, l, n, k);
   if (rc != SG_OK) return rc;
   if (m == 0 || n == 0 || l == 0) return fail(SG_EINVAL, "empty product has no plan");
@@ -346,6 +362,8 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
   if (splits) *splits = p.splits;
   if (ctas) *ctas = (int)(p.grid.x * p.grid.y * p.grid.z);
   if (kernel_index) *kernel_index = p.kernel_index;
+  if (pipelined) *pipelined = p.ki->pipe ? 1 : 0;
+  if (threads) *threads = p.ki->threads;
   return SG_OK;
 }
 
@@ -376,14 +394,15 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
     if (!ws) return cuda_fail(e, "sg_m4rm workspace");
   }
   uint32_t* AT = (uint32_t*)ws;
-  int64_t at_bytes = ((int64_t)R * p.wa32 * p.mpad * 4 + 255) / 256 * 256;
+  int64_t at_bytes = ((int64_t)p.at_planes * p.at_words * p.mpad * 4 + 255) / 256 * 256;
   uint32_t* partial = p.splits > 1 ? (uint32_t*)(ws + at_bytes) : nullptr;
 
   cudaEvent_t ev[4];
   if (g_timing)
     for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
   if (g_timing) cudaEventRecord(ev[0], st);
-  SG_CUDA(launch_transpose_a(field, (const uint32_t*)A, AT, m, p.mpad, p.wa32, st), "sg_m4rm transpose");
+  SG_CUDA(launch_transpose_a(field, p.K, (const uint32_t*)A, AT, m, p.mpad, p.wa32, p.at_words, st),
+          "sg_m4rm index pre-pass");
   g_launches++;
   if (g_timing) cudaEventRecord(ev[1], st);
   M4rmArgs a;
@@ -393,7 +412,7 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   a.m = m;
   a.l = l;
   a.mpad = p.mpad;
-  a.wa32 = p.wa32;
+  a.wa32 = p.at_words;
   a.wc32 = p.wc32;
   a.nblocks = p.nblocks;
   a.bps = p.bps;

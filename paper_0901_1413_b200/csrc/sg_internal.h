@@ -15,7 +15,7 @@ constexpr int THREADS = 256;
 
 struct M4rmArgs {
   const uint32_t* B;   // [R][l][wc32]   32-bit view of B's planes (row = 2*W64 words)
-  const uint32_t* AT;  // [R][wa32][mpad] index planes of A, transposed (F3: A0^A1, A1)
+  const uint32_t* AT;  // k = 8: index words [wa32 := nwords][mpad]; else A^T planes [R][wa32][mpad]
   uint32_t* C;         // final [R][m][wc32] or partial [splits][R][mpad][wc32]
   int64_t m, l, mpad;
   int wa32, wc32;      // 32-bit words per row of A and of B/C
@@ -26,6 +26,7 @@ struct M4rmArgs {
 struct KernelInfo {
   void (*fn)(M4rmArgs);
   int field, k, rt, threads;
+  bool pipe;           // double-buffered table, one barrier per k-block
   int smem_bytes;
   int regs;            // filled in lazily from cudaFuncGetAttributes
   int occupancy;       // CTAs per SM, filled lazily
@@ -35,8 +36,9 @@ struct KernelInfo {
 int m4rm_kernel_count();
 KernelInfo* m4rm_kernel_at(int i);
 
-cudaError_t launch_transpose_a(int field, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
-                               int wa32, cudaStream_t st);
+// k = 8: packed index words [nwords][mpad]; k < 8: A^T bit planes [R][wa32][mpad]
+cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
+                               int wa32, int nwords, cudaStream_t st);
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st);
 cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int64_t m, int64_t mpad,
                                  int wc32, int splits, cudaStream_t st);

@@ -49,51 +49,52 @@ template <int F> __device__ __forceinline__ V<F> vzero() {
 // Row accumulator of one lane: 4 words x RS planes.
 template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
 
-// One (row, k-block) update of the 4 C words a lane owns.  tl = this lane's replica base,
-// TPL = uint4 stride between table planes, e = the byte offsets of the basis entries.
+// Table rows of one (row, k-block): NI lookups x R planes, one uint4 (4 words) each.
+template <int F> struct Rows { uint4 v[Traits<F>::NI][Traits<F>::R]; };
+
+// Load the table rows at byte offsets e[] (entry * ENTRY_BYTES) from this lane's replica base.
 template <int F, int TPL>
-__device__ __forceinline__ void accumulate(Acc<F>& c, const unsigned char* __restrict__ tl, const u32 (&e)[3]) {
-  auto T = [&](int d, int i) { return *reinterpret_cast<const uint4*>(tl + e[i] + d * TPL * 16); };
-  if constexpr (F == F2) {
-    const uint4 p = T(0, 0);
-    c.w[0][0] ^= p.x; c.w[1][0] ^= p.y; c.w[2][0] ^= p.z; c.w[3][0] ^= p.w;
-  } else if constexpr (F == F3) {
-    // basis {1, -1}: C += T[pos]; C -= T[neg]   (_core_py.py:213-222), 6 LOP3 per word
-    const uint4 pu = T(0, 0), ps = T(1, 0), nu = T(0, 1), ns = T(1, 1);
-    const u32 PU[4] = {pu.x, pu.y, pu.z, pu.w}, PS[4] = {ps.x, ps.y, ps.z, ps.w};
-    const u32 NU[4] = {nu.x, nu.y, nu.z, nu.w}, NS[4] = {ns.x, ns.y, ns.z, ns.w};
+__device__ __forceinline__ void load_rows(Rows<F>& r, const unsigned char* __restrict__ tl, const u32 (&e)[3]) {
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      f3_add(c.w[w][0], c.w[w][1], PU[w], PS[w]);
-      f3_sub(c.w[w][0], c.w[w][1], NU[w], NS[w]);
-    }
-  } else if constexpr (F == GF4) {
-    // power basis {1, x}: C += T[g0] + x*T[g1],  x*(t0, t1) = (t1, t0 ^ t1)
-    const uint4 p0 = T(0, 0), p1 = T(1, 0), q0 = T(0, 1), q1 = T(1, 1);
-    c.w[0][0] ^= p0.x ^ q1.x; c.w[0][1] ^= p1.x ^ q0.x ^ q1.x;
-    c.w[1][0] ^= p0.y ^ q1.y; c.w[1][1] ^= p1.y ^ q0.y ^ q1.y;
-    c.w[2][0] ^= p0.z ^ q1.z; c.w[2][1] ^= p1.z ^ q0.z ^ q1.z;
-    c.w[3][0] ^= p0.w ^ q1.w; c.w[3][1] ^= p1.w ^ q0.w ^ q1.w;
-  } else {
-    // F5 / F7, basis {1, 2, 4}: C += T[g0] + 2*T[g1] + 4*T[g2] (the reference's Horner form,
-    // _core_py.py:241-255, reassociated); doubling is a plane rotation in both accumulators.
-    const uint4 a0 = T(0, 0), a1 = T(1, 0), a2 = T(2, 0);
-    const uint4 b0 = T(0, 1), b1 = T(1, 1), b2 = T(2, 1);
-    const uint4 d0 = T(0, 2), d1 = T(1, 2), d2 = T(2, 2);
-    const u32 X0[4] = {a0.x, a0.y, a0.z, a0.w}, X1[4] = {a1.x, a1.y, a1.z, a1.w}, X2[4] = {a2.x, a2.y, a2.z, a2.w};
-    const u32 Y0[4] = {b0.x, b0.y, b0.z, b0.w}, Y1[4] = {b1.x, b1.y, b1.z, b1.w}, Y2[4] = {b2.x, b2.y, b2.z, b2.w};
-    const u32 Z0[4] = {d0.x, d0.y, d0.z, d0.w}, Z1[4] = {d1.x, d1.y, d1.z, d1.w}, Z2[4] = {d2.x, d2.y, d2.z, d2.w};
+  for (int i = 0; i < Traits<F>::NI; ++i)
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      u32* q = c.w[w];
+    for (int d = 0; d < Traits<F>::R; ++d)
+      r.v[i][d] = *reinterpret_cast<const uint4*>(tl + e[i] + d * TPL * 16);
+}
+
+__device__ __forceinline__ u32 comp(const uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
+
+// One (row, k-block) update of the 4 C words a lane owns from its loaded table rows.
+template <int F>
+__device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    u32* q = c.w[w];
+    if constexpr (F == F2) {
+      q[0] ^= comp(r.v[0][0], w);
+    } else if constexpr (F == F3) {
+      // basis {1, -1}: C += T[pos]; C -= T[neg]   (_core_py.py:213-222), 6 LOP3 per word
+      f3_add(q[0], q[1], comp(r.v[0][0], w), comp(r.v[0][1], w));
+      f3_sub(q[0], q[1], comp(r.v[1][0], w), comp(r.v[1][1], w));
+    } else if constexpr (F == GF4) {
+      // power basis {1, x}: C += T[g0] + x*T[g1],  x*(t0, t1) = (t1, t0 ^ t1)
+      const u32 q1 = comp(r.v[1][1], w);
+      q[0] ^= comp(r.v[0][0], w) ^ q1;
+      q[1] ^= comp(r.v[0][1], w) ^ comp(r.v[1][0], w) ^ q1;
+    } else {
+      // F5 / F7, basis {1, 2, 4}: C += T[g0] + 2*T[g1] + 4*T[g2] (the reference's Horner form,
+      // _core_py.py:241-255, reassociated); doubling is a plane rotation in both accumulators.
+      const u32 x0 = comp(r.v[0][0], w), x1 = comp(r.v[0][1], w), x2 = comp(r.v[0][2], w);
+      const u32 y0 = comp(r.v[1][0], w), y1 = comp(r.v[1][1], w), y2 = comp(r.v[1][2], w);
+      const u32 z0 = comp(r.v[2][0], w), z1 = comp(r.v[2][1], w), z2 = comp(r.v[2][2], w);
       if constexpr (F == F7) {  // 2y = (y2, y0, y1), 4z = (z1, z2, z0) mod 7; 3 x 8 LOP3
-        f7_add(q[0], q[1], q[2], X0[w], X1[w], X2[w]);
-        f7_add(q[0], q[1], q[2], Y2[w], Y0[w], Y1[w]);
-        f7_add(q[0], q[1], q[2], Z1[w], Z2[w], Z0[w]);
+        f7_add(q[0], q[1], q[2], x0, x1, x2);
+        f7_add(q[0], q[1], q[2], y2, y0, y1);
+        f7_add(q[0], q[1], q[2], z1, z2, z0);
       } else {  // mod 15: x = (x0,x1,x2,0), 2y = (0,y0,y1,y2), 4z = (z2,0,z0,z1)
-        add15(q[0], q[1], q[2], q[3], X0[w], X1[w], X2[w], 0u);
-        add15(q[0], q[1], q[2], q[3], 0u, Y0[w], Y1[w], Y2[w]);
-        add15(q[0], q[1], q[2], q[3], Z2[w], 0u, Z0[w], Z1[w]);
+        add15(q[0], q[1], q[2], q[3], x0, x1, x2, 0u);
+        add15(q[0], q[1], q[2], q[3], 0u, y0, y1, y2);
+        add15(q[0], q[1], q[2], q[3], z2, 0u, z0, z1);
       }
     }
   }
@@ -113,9 +114,11 @@ template <int F> __device__ __forceinline__ void finish(const u32 (&q)[Traits<F>
   }
 }
 
-template <int F, int K, int RT>
-__global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
-  constexpr int NT = THREADS;
+// PIPE = false: per k-block  phase1 | sync | phase2 | sync | lookups   (one table buffer)
+// PIPE = true : per k-block  lookups(s) + phase2(s+1) + phase1(s+2) | sync  (two table buffers):
+//               the next table is written while the current one is read, one barrier per block.
+template <int F, int K, int RT, bool PIPE, int NT>
+__global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
   constexpr int R = Traits<F>::R;
   constexpr int E = 1 << K;
   constexpr int KLO = K < 4 ? K : 4;
@@ -124,12 +127,26 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
   constexpr int TPLANE = E * ENTRY_BYTES;  // bytes per table plane
   constexpr int TPL = TPLANE / 16;         // uint4 per table plane
   constexpr int HALF = 16 * R * 4;         // u32 per half table
+  constexpr int NTAB = PIPE ? 2 : 1;
+  constexpr int PD = PIPE ? 3 : 2;         // cp.async prefetch distance in k-blocks
+  // k = 8: A's index bytes arrive pre-packed as one record of NIP bytes per k-block (the
+  // index_words pre-pass), RPW records per 32-bit word, NSLOT staging slots of ROWS words.
+  // k < 8: A^T bit planes, R planes x 2 slots.
+  constexpr bool IW = (K == 8);
+  constexpr int NI = Traits<F>::NI;
+  constexpr int NIP = NI == 3 ? 4 : NI;
+  constexpr int RPW = 4 / NIP;
+  constexpr int NSLOT = IW ? PD + 1 : 2;
+  constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
+  constexpr int TPE_RAW = NT / E;
+  constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
+  constexpr int CPT = COPIES / TPE;        // replicas written per thread
 
   extern __shared__ __align__(128) unsigned char smem[];
-  uint4* tab = reinterpret_cast<uint4*>(smem);
-  u32* thalf = reinterpret_cast<u32*>(smem + R * TPLANE);  // [2 buf][2 half][16][R][4]
-  u32* bst = thalf + 2 * 2 * HALF;                          // [2 buf][K][R][4]
-  u32* ast = bst + 2 * K * R * 4;                           // [2 slot][R][ROWS]
+  uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][R][E][COPIES] uint4
+  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][16][R][4]
+  u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
+  u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
 
   const int tid = threadIdx.x;
   const int word0 = blockIdx.x * SLAB_WORDS;
@@ -138,11 +155,11 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
   const int s_end = min(a.nblocks, s_begin + a.bps);
   if (s_begin >= s_end) return;
 
-  int next_word = (s_begin * K) >> 5;
+  int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
   // Stage block s's B rows (K x R x 16 B) and any A^T words it needs that are not yet staged.
   auto issue = [&](int s) {
     if (s < s_end) {
-      u32* bdst = bst + (s & 1) * K * R * 4;
+      u32* bdst = bst + (s % 3) * K * R * 4;
       for (int q = tid; q < K * R * 2; q += NT) {
         const int i = q / (R * 2), d = (q >> 1) % R, half = q & 1;
         const int64_t row = (int64_t)s * K + i;
@@ -151,11 +168,11 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
         const u32* src = ok ? a.B + ((int64_t)d * a.l + row) * a.wc32 + w : a.B;
         cp_async8(bdst + (i * R + d) * 4 + 2 * half, src, ok ? 8 : 0);
       }
-      const int whi = (s * K + K - 1) >> 5;
+      const int whi = IW ? s / RPW : (s * K + K - 1) >> 5;
       for (; next_word <= whi; ++next_word) {
-        u32* adst = ast + (next_word & 1) * R * ROWS;
+        u32* adst = ast + (next_word % NSLOT) * NAP * ROWS;
         const bool ok = next_word < a.wa32;
-        for (int q = tid; q < R * ROWS / 4; q += NT) {
+        for (int q = tid; q < NAP * ROWS / 4; q += NT) {
           const int d = q / (ROWS / 4), r4 = q % (ROWS / 4);
           const u32* src = ok ? a.AT + ((int64_t)d * a.wa32 + next_word) * a.mpad + row0 + 4 * r4 : a.AT;
           cp_async16(adst + d * ROWS + 4 * r4, src, ok ? 16 : 0);
@@ -165,10 +182,60 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
     cp_async_commit();
   };
 
-  issue(s_begin);
-  issue(s_begin + 1);
-  cp_async_wait<1>();
-  __syncthreads();
+  // phase 1: the two 16-entry half tables of block s (rows 0..KLO-1 and KLO..K-1)
+  auto phase1 = [&](int s) {
+    const u32* bs = bst + (s % 3) * K * R * 4;
+    u32* th = thalf + (s & 1) * 2 * HALF;
+    if (tid < 128) {
+      const int h = tid >> 6, e = (tid >> 2) & 15, w = tid & 3;
+      const int nrows = h ? KHI : KLO;
+      if (e < (1 << nrows)) {
+        V<F> acc = vzero<F>();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < nrows && ((e >> i) & 1)) {
+            V<F> b;
+#pragma unroll
+            for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
+            vadd<F>(acc, b);
+          }
+        }
+#pragma unroll
+        for (int d = 0; d < R; ++d) th[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
+      }
+    }
+  };
+
+  // phase 2a: this thread's table entry g = Thi[g >> KLO] + Tlo[g & (2^KLO - 1)] (4 words x R)
+  const int g_own = tid / TPE, part = tid % TPE;
+  auto phase2_compute = [&](int s, V<F> (&v)[4]) {
+    const u32* th = thalf + (s & 1) * 2 * HALF;
+    if (g_own < E) {
+      const uint4* lo = reinterpret_cast<const uint4*>(th + (g_own & ((1 << KLO) - 1)) * R * 4);
+      const uint4* hi = reinterpret_cast<const uint4*>(th + HALF + (g_own >> KLO) * R * 4);
+      V<F> hv[4];
+#pragma unroll
+      for (int d = 0; d < R; ++d) {
+        const uint4 L = lo[d], H = hi[d];
+        v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
+        hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
+      }
+      if constexpr (KHI > 0) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) vadd<F>(v[w], hv[w]);
+      }
+    }
+  };
+  // phase 2b: write replica number cc (of this thread's CPT) of entry g_own into table buffer tb.
+  // The replica order is rotated by g so the 8 lanes of a store phase hit 8 different banks.
+  auto phase2_store = [&](uint4* tb, const V<F> (&v)[4], int cc) {
+    if (g_own < E) {
+      const int copy = (part * CPT + cc + g_own) & (COPIES - 1);
+#pragma unroll
+      for (int d = 0; d < R; ++d)
+        tb[d * TPL + g_own * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
+    }
+  };
 
   Acc<F> c[RT];
 #pragma unroll
@@ -178,92 +245,109 @@ __global__ void __launch_bounds__(THREADS, 1) m4rm_kernel(const M4rmArgs a) {
 #pragma unroll
       for (int d = 0; d < Traits<F>::RS; ++d) c[t].w[w][d] = 0u;
 
-  const unsigned char* tl = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
+  const unsigned char* tl0 = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
 
-  for (int s = s_begin; s < s_end; ++s) {
-    // ---- phase 1: half tables from the staged B rows
-    {
-      const u32* bs = bst + (s & 1) * K * R * 4;
-      u32* th = thalf + (s & 1) * 2 * HALF;
-      if (tid < 128) {
-        const int h = tid >> 6, e = (tid >> 2) & 15, w = tid & 3;
-        const int nrows = h ? KHI : KLO;
-        if (e < (1 << nrows)) {
-          V<F> acc = vzero<F>();
+  // Byte offsets of row-slot t's table entries for block s.
+  auto entries = [&](int s, int t, u32 (&e)[3]) {
+    const int lr = t * NT + tid;
+    e[0] = e[1] = e[2] = 0u;
+    if constexpr (IW) {
+      const u32 x = ast[((s / RPW) % NSLOT) * ROWS + lr];
+      const int b0 = (s % RPW) * NIP;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (i < nrows && ((e >> i) & 1)) {
-              V<F> b;
-#pragma unroll
-              for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
-              vadd<F>(acc, b);
-            }
-          }
-#pragma unroll
-          for (int d = 0; d < R; ++d) th[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
-        }
-      }
-    }
-    __syncthreads();
-    issue(s + 2);
-    // ---- phase 2: full table, 8 replicas
-    {
-      constexpr int TPE_RAW = NT / E;
-      constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);
-      constexpr int CPT = COPIES / TPE;  // replicas written per thread
-      const u32* th = thalf + (s & 1) * 2 * HALF;
-      const int g = tid / TPE, part = tid % TPE;
-      if (g < E) {
-        const uint4* lo = reinterpret_cast<const uint4*>(th + (g & ((1 << KLO) - 1)) * R * 4);
-        const uint4* hi = reinterpret_cast<const uint4*>(th + HALF + (g >> KLO) * R * 4);
-        V<F> v[4], hv[4];
-#pragma unroll
-        for (int d = 0; d < R; ++d) {
-          const uint4 L = lo[d], H = hi[d];
-          v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
-          hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
-        }
-        if constexpr (KHI > 0) {
-#pragma unroll
-          for (int w = 0; w < 4; ++w) vadd<F>(v[w], hv[w]);
-        }
-#pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) {
-          // rotate the replica order by g so the 8 lanes of a store phase hit 8 different banks
-          const int copy = (part * CPT + cc + g) & (COPIES - 1);
-#pragma unroll
-          for (int d = 0; d < R; ++d)
-            tab[d * TPL + g * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
-        }
-      }
-    }
-    cp_async_wait<1>();
-    __syncthreads();
-    // ---- phase 3: lookups and accumulation for this k-block
-    {
+      for (int i = 0; i < NI; ++i) e[i] = __byte_perm(x, 0u, 0x4440u | (u32)(b0 + i)) * ENTRY_BYTES;
+    } else {
       const int col0 = s * K;
       const int w0 = col0 >> 5, sh = col0 & 31;
       const u32* aw0 = ast + (w0 & 1) * R * ROWS;
       const u32* aw1 = ast + ((w0 + 1) & 1) * R * ROWS;
-      const u32 sel = 0x4440u | (u32)(sh >> 3);  // PRMT: byte sh/8 of x, zero-extended
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int lr = t * NT + tid;
-        u32 e[3] = {0u, 0u, 0u};
-#pragma unroll
-        for (int d = 0; d < R; ++d) {
-          u32 x = aw0[d * ROWS + lr];
-          if constexpr (K == 8) {
-            x = __byte_perm(x, 0u, sel);
-          } else if constexpr (32 % K == 0) {
-            x = (x >> sh) & (E - 1);
-          } else {
-            x = ((sh + K > 32) ? __funnelshift_r(x, aw1[d * ROWS + lr], sh) : (x >> sh)) & (E - 1);
-          }
-          e[d] = x * ENTRY_BYTES;
+      for (int d = 0; d < R; ++d) {
+        u32 x = aw0[d * ROWS + lr];
+        if constexpr (32 % K == 0) {
+          x = (x >> sh) & (E - 1);
+        } else {
+          x = ((sh + K > 32) ? __funnelshift_r(x, aw1[d * ROWS + lr], sh) : (x >> sh)) & (E - 1);
         }
-        accumulate<F, TPL>(c[t], tl, e);
+        e[d] = x * ENTRY_BYTES;
       }
+    }
+  };
+
+  // lookups for block s from table buffer tb, software-pipelined one row-slot ahead
+  // (entries of t+1 and table rows of t in flight while t accumulates); `between(t)` runs
+  // after row-slot t.
+  auto lookups = [&](int s, int tb, auto&& between) {
+    const unsigned char* tl = tl0 + tb * R * TPLANE;
+    u32 e[3];
+    entries(s, 0, e);
+    Rows<F> cur;
+    load_rows<F, TPL>(cur, tl, e);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      Rows<F> nxt;
+      if (t + 1 < RT) {
+        entries(s, t + 1, e);
+        load_rows<F, TPL>(nxt, tl, e);
+      }
+      accumulate<F>(c[t], cur);
+      between(t);
+      if (t + 1 < RT) cur = nxt;
+    }
+  };
+
+  if constexpr (!PIPE) {
+    for (int i = 0; i < PD; ++i) issue(s_begin + i);
+    cp_async_wait<PD - 1>();
+    __syncthreads();
+    for (int s = s_begin; s < s_end; ++s) {
+      phase1(s);
+      __syncthreads();
+      issue(s + PD);
+      {
+        V<F> v[4];
+        phase2_compute(s, v);
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) phase2_store(tab, v, cc);
+      }
+      cp_async_wait<PD - 1>();
+      __syncthreads();
+      lookups(s, 0, [](int) {});
+    }
+  } else {
+    for (int i = 0; i < PD; ++i) issue(s_begin + i);
+    cp_async_wait<0>();
+    __syncthreads();
+    phase1(s_begin);
+    __syncthreads();
+    {
+      V<F> v[4];
+      phase2_compute(s_begin, v);
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) phase2_store(tab + (s_begin & 1) * R * TPL, v, cc);
+    }
+    if (s_begin + 1 < s_end) phase1(s_begin + 1);
+    __syncthreads();
+    for (int s = s_begin; s < s_end; ++s) {
+      issue(s + PD);
+      const bool nxt = s + 1 < s_end;
+      V<F> v[4];
+      if (nxt) phase2_compute(s + 1, v);
+      uint4* tnext = tab + ((s + 1) & 1) * R * TPL;
+      // spread the next table's replica stores over the row-slot loop
+      lookups(s, s & 1, [&](int t) {
+        if (nxt) {
+          if constexpr (RT >= CPT) {
+            if (t % (RT / CPT) == 0) phase2_store(tnext, v, t / (RT / CPT));
+          } else {
+#pragma unroll
+            for (int q = 0; q < CPT / RT; ++q) phase2_store(tnext, v, t * (CPT / RT) + q);
+          }
+        }
+      });
+      if (s + 2 < s_end) phase1(s + 2);
+      cp_async_wait<0>();
+      __syncthreads();
     }
   }
 
@@ -321,6 +405,54 @@ __global__ void transpose_a_kernel(const u32* __restrict__ A, u32* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ k = 8 index-word pre-pass
+// A planes [R][m][wa32] -> IW [nwords][mpad]: for k-block s (column byte s of each plane) the
+// NI basis index bytes (F3: A0^A1 then A1; F5/F7: planes 0..2; GF4: planes 0..1; F2: plane 0)
+// form one record of NIP bytes; RPW = 4/NIP records per 32-bit word.  A 32-row x 32-word tile
+// of each plane is staged through shared memory so both reads and writes are coalesced.
+template <int F>
+__global__ void index_words_kernel(const u32* __restrict__ A, u32* __restrict__ IW, int64_t m, int64_t mpad,
+                                   int wa32, int nwords) {
+  constexpr int R = Traits<F>::R, NI = Traits<F>::NI;
+  constexpr int NIP = NI == 3 ? 4 : NI, RPW = 4 / NIP;
+  __shared__ u32 tile[R][32][33];
+  const int64_t rbase = (int64_t)blockIdx.y * 32;
+  const int wbase = blockIdx.x * 32;  // A words wbase.. (= k-blocks 4*wbase ..)
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int d = 0; d < R; ++d)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = rbase + ty + 8 * i;
+      const int w = wbase + tx;
+      tile[d][ty + 8 * i][tx] = (row < m && w < wa32) ? A[((int64_t)d * m + row) * wa32 + w] : 0u;
+    }
+  __syncthreads();
+  // 128 k-blocks per tile -> 128 / RPW output words
+  for (int q = ty; q < 128 / RPW; q += 8) {
+    const int oq = (wbase * 4) / RPW + q;
+    const int64_t row = rbase + tx;
+    if (oq >= nwords || row >= mpad) continue;
+    u32 v = 0;
+#pragma unroll
+    for (int b = 0; b < RPW; ++b) {
+      const int sl = q * RPW + b;  // k-block within the tile
+      const int aw = sl >> 2, sh = 8 * (sl & 3);
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        u32 byte;
+        if constexpr (F == F3) {
+          byte = i == 0 ? ((tile[0][tx][aw] ^ tile[1][tx][aw]) >> sh) : (tile[1][tx][aw] >> sh);
+        } else {
+          byte = tile[i][tx][aw] >> sh;
+        }
+        v |= (byte & 0xFFu) << (8 * (b * NIP + i));
+      }
+    }
+    IW[(int64_t)oq * mpad + row] = v;
+  }
+}
+
 // ------------------------------------------------------------------ split-K reduction
 template <int F>
 __global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict__ C, int64_t m,
@@ -348,20 +480,33 @@ __global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict_
 }
 
 // ------------------------------------------------------------------ registry
-template <int F, int K, int RT>
+template <int F, int K, int RT, bool PIPE, int NT>
 constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
-  return R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 2 * K * R * 4 * 4 + 2 * R * RT * THREADS * 4;
+  constexpr int NSLOT = K == 8 ? (PIPE ? 4 : 3) : 2;
+  constexpr int NAP = K == 8 ? 1 : R;
+  return (PIPE ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
+         NSLOT * NAP * RT * NT * 4;
 }
 
-#define SG_K(F, K, RT) {m4rm_kernel<F, K, RT>, F, K, RT, THREADS, smem_bytes_for<F, K, RT>(), 0, 0}
-#define SG_KSET8(F) SG_K(F, 8, 1), SG_K(F, 8, 2), SG_K(F, 8, 4), SG_K(F, 8, 8)
-#define SG_KLOW(F) SG_K(F, 1, 1), SG_K(F, 2, 1), SG_K(F, 3, 1), SG_K(F, 4, 1), SG_K(F, 5, 1), SG_K(F, 6, 1), SG_K(F, 7, 1)
+#define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, P, smem_bytes_for<F, K, RT, P, NT>(), 0, 0}
+// k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
+#define SG_KSET8(F)                                                                                 \
+  SG_K(F, 8, 1, false, 256), SG_K(F, 8, 2, false, 256), SG_K(F, 8, 4, false, 256), SG_K(F, 8, 8, false, 256), \
+  SG_K(F, 8, 1, true, 256), SG_K(F, 8, 2, true, 256), SG_K(F, 8, 4, true, 256),                      \
+  SG_K(F, 8, 2, false, 512), SG_K(F, 8, 4, false, 512), SG_K(F, 8, 2, true, 512)
+#define SG_KSET8_2PLANE(F)                                                                          \
+  SG_K(F, 8, 16, false, 256), SG_K(F, 8, 8, true, 256), SG_K(F, 8, 16, true, 256),                  \
+  SG_K(F, 8, 8, false, 512), SG_K(F, 8, 4, true, 512), SG_K(F, 8, 8, true, 512)
+// k < 8: parity and generality (k-invariance), one variant each + a pipelined k=5
+#define SG_KLOW(F)                                                                                  \
+  SG_K(F, 1, 1, false, 256), SG_K(F, 2, 1, false, 256), SG_K(F, 3, 1, false, 256), SG_K(F, 4, 1, false, 256), \
+  SG_K(F, 5, 1, false, 256), SG_K(F, 6, 1, false, 256), SG_K(F, 7, 1, false, 256), SG_K(F, 5, 1, true, 256)
 
 static KernelInfo g_kernels[] = {
-    SG_KSET8(F2), SG_K(F2, 8, 16), SG_KLOW(F2),
-    SG_KSET8(F3), SG_K(F3, 8, 16), SG_KLOW(F3),
-    SG_KSET8(GF4), SG_K(GF4, 8, 16), SG_KLOW(GF4),
+    SG_KSET8(F2), SG_KSET8_2PLANE(F2), SG_KLOW(F2),
+    SG_KSET8(F3), SG_KSET8_2PLANE(F3), SG_KLOW(F3),
+    SG_KSET8(GF4), SG_KSET8_2PLANE(GF4), SG_KLOW(GF4),
     SG_KSET8(F5), SG_KLOW(F5),
     SG_KSET8(F7), SG_KLOW(F7),
 };
@@ -374,8 +519,19 @@ cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_transpose_a(int field, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
-                               int wa32, cudaStream_t st) {
+cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
+                               int wa32, int nwords, cudaStream_t st) {
+  if (k == 8) {
+    dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), 1);
+    switch (field) {
+      case F2: index_words_kernel<F2><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
+      case F3: index_words_kernel<F3><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
+      case F5: index_words_kernel<F5><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
+      case F7: index_words_kernel<F7><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
+      default: index_words_kernel<GF4><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
+    }
+    return cudaGetLastError();
+  }
   const int R = field == F2 ? 1 : (field == F5 || field == F7) ? 3 : 2;
   dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), R);
   transpose_a_kernel<<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, field == F3);

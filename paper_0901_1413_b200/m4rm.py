@@ -110,14 +110,15 @@ def plan(field, m: int, l: int, n: int, k: int = 8) -> dict:
     from .fields import by_name
     if isinstance(field, str):
         field = by_name(field)
-    rows, splits, ctas, idx = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rows, splits, ctas, idx, pipe, thr = (ctypes.c_int() for _ in range(6))
     _lib.check(_lib.load().sg_plan(field.code, m, l, n, k, ctypes.byref(rows), ctypes.byref(splits),
-                                   ctypes.byref(ctas), ctypes.byref(idx)))
-    return {"rows_per_cta": rows.value, "splits": splits.value, "ctas": ctas.value, "kernel": idx.value}
+                                   ctypes.byref(ctas), ctypes.byref(idx), ctypes.byref(pipe), ctypes.byref(thr)))
+    return {"rows_per_cta": rows.value, "splits": splits.value, "ctas": ctas.value, "kernel": idx.value,
+            "pipelined": bool(pipe.value), "threads": thr.value}
 
 
-def set_plan_override(rows_per_thread: int = 0, splits: int = 0):
-    _lib.check(_lib.load().sg_set_plan_override(rows_per_thread, splits))
+def set_plan_override(rows_per_thread: int = 0, splits: int = 0, pipe: int = -1, threads: int = 0):
+    _lib.check(_lib.load().sg_set_plan_override(rows_per_thread, splits, pipe, threads))
 
 
 def last_timing() -> dict:

@@ -117,21 +117,34 @@ def test_k_invariance(fname):
 
 @pytest.mark.parametrize("fname", list(FIELDS))
 def test_every_compiled_plan(fname):
-    """Force every rows-per-thread variant and several k-splits (split-K partial + reduce)."""
+    """Force every rows-per-thread variant, both schedules and several k-splits."""
     A = oracle.random_dense(fname, 700, 1000, 7)
     B = oracle.random_dense(fname, 1000, 777, 8)
     want = expect(fname, A, B)
+    ran = 0
     for rt in (1, 2, 4, 8, 16):
-        for splits in (1, 2, 5, 16):
-            m4rm_mod.set_plan_override(rt, splits)
-            try:
-                C = gpu_multiply(fname, A, B)
-            except ValueError:
-                raise
-            except RuntimeError as e:
-                assert "no compiled" in str(e)
-                continue
-            assert np.array_equal(C.planes_numpy(), want), (fname, rt, splits)
+        for pipe in (0, 1):
+            for nt in (256, 512):
+                for splits in (1, 2, 5, 16):
+                    m4rm_mod.set_plan_override(rt, splits, pipe, nt)
+                    try:
+                        C = gpu_multiply(fname, A, B)
+                    except RuntimeError as e:
+                        assert "no compiled" in str(e)
+                        continue
+                    ran += 1
+                    assert np.array_equal(C.planes_numpy(), want), (fname, rt, pipe, nt, splits)
+    assert ran >= 32
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_general_k_pipelined_straddle(fname):
+    """k = 5 (blocks straddle 32-bit words) through the pipelined schedule."""
+    A = oracle.random_dense(fname, 300, 333, 17)
+    B = oracle.random_dense(fname, 333, 200, 18)
+    m4rm_mod.set_plan_override(1, 0, 1, 256)
+    C = gpu_multiply(fname, A, B, k=5)
+    assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
 
 
 @pytest.mark.parametrize("fname,m,l,n", [("f3", 1024, 1024, 1024), ("f5", 1000, 3000, 700), ("f7", 513, 2049, 1500),

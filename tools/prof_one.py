@@ -18,13 +18,15 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--rt", type=int, default=0)
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--m", type=int, default=0)
+ap.add_argument("--pipe", type=int, default=-1)
+ap.add_argument("--threads", type=int, default=0)
 a = ap.parse_args()
 name, field, m, l, n = bench.CONFIGS[a.config]
 if a.m:
     m = a.m
 dev = torch.device("cuda", 0)
 f, A, B = bench.make_inputs(field, m, l, n, 0, dev, True)
-M.set_plan_override(a.rt, a.splits)
+M.set_plan_override(a.rt, a.splits, a.pipe, a.threads)
 print(name, sg.plan(f, m, l, n, 8))
 for _ in range(a.reps):
     C = sg.m4rm_multiply(A, B, sg.M4rmParams(8))
