@@ -134,6 +134,10 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
  * schedule (-1 = automatic) */
 int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads);
 int sg_set_timing(int enable);                              /* event-time each internal launch */
+/* performance experiments only: select kernel variants with parts of the work removed
+ * (bit 0: table-replica stores, bit 1: field arithmetic, bit 2: lookups); results are WRONG
+ * while a nonzero mask is set.  0 restores normal operation. */
+int sg_debug_ablation(int mask);
 int sg_last_timing(double* transpose_ms, double* m4rm_ms, double* reduce_ms);
 int64_t sg_launch_count(void);                              /* kernels launched by this library */
 int sg_probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_sm,

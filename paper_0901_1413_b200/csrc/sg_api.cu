@@ -20,7 +20,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
-int g_override_rt = 0, g_override_splits = 0, g_override_pipe = -1, g_override_threads = 0;
+int g_override_rt = 0, g_override_splits = 0, g_override_pipe = -1, g_override_threads = 0, g_ablation = 0;
 bool g_timing = false;
 double g_last_ms[3] = {0, 0, 0};
 std::mutex g_mu;
@@ -59,7 +59,7 @@ DevState& dev_state(int device) {
       cudaFuncAttributes fa;
       if (cudaFuncGetAttributes(&fa, k->fn) == cudaSuccess) k->regs = fa.numRegs;
       int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->threads, k->smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->launch_threads, k->smem_bytes);
       k->occupancy = occ;
     }
     cudaGetLastError();
@@ -139,8 +139,9 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
     KernelInfo* ki = m4rm_kernel_at(i);
     if (ki->field != field || ki->k != K) continue;
     if (g_override_rt && ki->rt != g_override_rt) continue;
-    if (g_override_pipe >= 0 && (int)ki->pipe != g_override_pipe) continue;
+    if (g_override_pipe >= 0 && ki->sched != g_override_pipe) continue;
     if (g_override_threads && ki->threads != g_override_threads) continue;
+    if (ki->ablation != g_ablation) continue;
     if (ki->occupancy < 1) continue;  // does not fit this device
     const int rows = ki->rt * ki->threads;
     const int64_t rgroups = (m + rows - 1) / rows;
@@ -148,8 +149,10 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
     const double alu_l = rows * lane_alu / 64.0, alu_t = E * entry_alu / 64.0;
     const double smem_l = (rows * lane_smem + rows * R * 4.0) / 128.0, smem_t = E * R * ENTRY_BYTES / 128.0;
     // serialized schedule: table build, then lookups; pipelined: both share the pipes
-    const double t_block = ki->pipe ? std::max(alu_l + alu_t, smem_l + smem_t) + 150.0
-                                    : std::max(alu_l, smem_l) + std::max(alu_t, smem_t) + 400.0;
+    // serial: table build then lookups; pipelined / warp-specialized: both share the pipes
+    const double t_block = ki->sched == 2   ? std::max(alu_l + alu_t, smem_l + smem_t) + 100.0
+                           : ki->sched == 1 ? std::max(alu_l + alu_t, smem_l + smem_t) + 250.0
+                                            : std::max(alu_l, smem_l) + std::max(alu_t, smem_t) + 400.0;
     const int occ = std::max(1, ki->occupancy);
     const int max_splits = std::max(1, std::min(nblocks, 64));
     for (int sp = 1; sp <= max_splits; ++sp) {
@@ -227,7 +230,13 @@ int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads)
   g_override_threads = threads;
   g_override_rt = rows_per_thread;
   g_override_splits = splits;
-  g_override_pipe = pipe < 0 ? -1 : (pipe ? 1 : 0);
+  g_override_pipe = pipe < 0 ? -1 : pipe;
+  return SG_OK;
+}
+
+int sg_debug_ablation(int mask) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_ablation = mask;
   return SG_OK;
 }
 
@@ -362,7 +371,7 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
   if (splits) *splits = p.splits;
   if (ctas) *ctas = (int)(p.grid.x * p.grid.y * p.grid.z);
   if (kernel_index) *kernel_index = p.kernel_index;
-  if (pipelined) *pipelined = p.ki->pipe ? 1 : 0;
+  if (pipelined) *pipelined = p.ki->sched;
   if (threads) *threads = p.ki->threads;
   return SG_OK;
 }

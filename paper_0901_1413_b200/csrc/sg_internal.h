@@ -25,11 +25,13 @@ struct M4rmArgs {
 
 struct KernelInfo {
   void (*fn)(M4rmArgs);
-  int field, k, rt, threads;
-  bool pipe;           // double-buffered table, one barrier per k-block
+  int field, k, rt, threads;  // threads = lookup threads (rows = rt * threads)
+  int launch_threads;  // threads + 32 for the warp-specialized schedule
+  int sched;           // 0 serial, 1 pipelined (double-buffered table), 2 warp-specialized
   int smem_bytes;
   int regs;            // filled in lazily from cudaFuncGetAttributes
   int occupancy;       // CTAs per SM, filled lazily
+  int ablation;        // experiments only: never planned unless sg_set_ablation selects it
 };
 
 // Registry of compiled M4RM instantiations (sg_m4rm.cu).

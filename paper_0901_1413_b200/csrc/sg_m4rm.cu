@@ -117,8 +117,24 @@ template <int F> __device__ __forceinline__ void finish(const u32 (&q)[Traits<F>
 // PIPE = false: per k-block  phase1 | sync | phase2 | sync | lookups   (one table buffer)
 // PIPE = true : per k-block  lookups(s) + phase2(s+1) + phase1(s+2) | sync  (two table buffers):
 //               the next table is written while the current one is read, one barrier per block.
-template <int F, int K, int RT, bool PIPE, int NT>
-__global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
+// Named barriers (id 0 is __syncthreads) for the warp-specialized schedule.
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// SCHED 0: per k-block  phase1 | sync | phase2 | sync | lookups   (one table buffer)
+// SCHED 1: per k-block  lookups(s) + phase2(s+1) + phase1(s+2) | sync  (two table buffers)
+// SCHED 2: warp-specialized (k = 8): NT lookup threads + 4 builder warps that stage B and A
+//          with cp.async and builds block s+1's table into the other buffer while the lookup warps
+//          consume block s; FULL/EMPTY named barriers hand the two buffers back and forth.
+// ABL (experiments only, 0 in production): bit 0 skips the table-replica stores, bit 1 replaces
+// the field update by a plain XOR of the looked-up rows, bit 2 skips the lookups.
+constexpr int WS_BUILDERS = 128;  // builder threads (4 warps) of the warp-specialized schedule
+
+template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
+__global__ void __launch_bounds__(SCHED == 2 ? NT + WS_BUILDERS : NT, 1) m4rm_kernel(const M4rmArgs a) {
+  constexpr bool PIPE = SCHED == 1;
+  constexpr bool WS = SCHED == 2;
+  static_assert(!WS || K == 8, "the warp-specialized schedule is k = 8 only");
   constexpr int R = Traits<F>::R;
   constexpr int E = 1 << K;
   constexpr int KLO = K < 4 ? K : 4;
@@ -127,8 +143,9 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
   constexpr int TPLANE = E * ENTRY_BYTES;  // bytes per table plane
   constexpr int TPL = TPLANE / 16;         // uint4 per table plane
   constexpr int HALF = 16 * R * 4;         // u32 per half table
-  constexpr int NTAB = PIPE ? 2 : 1;
-  constexpr int PD = PIPE ? 3 : 2;         // cp.async prefetch distance in k-blocks
+  constexpr int NTAB = SCHED >= 1 ? 2 : 1;
+  constexpr int PD = PIPE ? 3 : 2;         // cp.async prefetch distance of B rows in k-blocks
+  constexpr int PDA = 2;                   // ... and of A's index words
   // k = 8: A's index bytes arrive pre-packed as one record of NIP bytes per k-block (the
   // index_words pre-pass), RPW records per 32-bit word, NSLOT staging slots of ROWS words.
   // k < 8: A^T bit planes, R planes x 2 slots.
@@ -136,7 +153,7 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
   constexpr int NI = Traits<F>::NI;
   constexpr int NIP = NI == 3 ? 4 : NI;
   constexpr int RPW = 4 / NIP;
-  constexpr int NSLOT = IW ? PD + 1 : 2;
+  constexpr int NSLOT = IW ? 3 : 2;       // A words in use + two blocks in flight
   constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
   constexpr int TPE_RAW = NT / E;
   constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
@@ -156,11 +173,12 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
   if (s_begin >= s_end) return;
 
   int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
-  // Stage block s's B rows (K x R x 16 B) and any A^T words it needs that are not yet staged.
-  auto issue = [&](int s) {
+  // Stage block s's B rows (K x R x 16 B) into bst[s % 3].
+  auto issue_b = [&](int s, int t0 = -1, int nthr = NT) {
+    if (t0 < 0) t0 = tid;
     if (s < s_end) {
       u32* bdst = bst + (s % 3) * K * R * 4;
-      for (int q = tid; q < K * R * 2; q += NT) {
+      for (int q = t0; q < K * R * 2; q += nthr) {
         const int i = q / (R * 2), d = (q >> 1) % R, half = q & 1;
         const int64_t row = (int64_t)s * K + i;
         const int w = word0 + 2 * half;
@@ -168,18 +186,23 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
         const u32* src = ok ? a.B + ((int64_t)d * a.l + row) * a.wc32 + w : a.B;
         cp_async8(bdst + (i * R + d) * 4 + 2 * half, src, ok ? 8 : 0);
       }
+    }
+  };
+  // Stage the index words block s needs that are not yet staged.
+  auto issue_a = [&](int s, int t0 = -1, int nthr = NT) {
+    if (t0 < 0) t0 = tid;
+    if (s < s_end) {
       const int whi = IW ? s / RPW : (s * K + K - 1) >> 5;
       for (; next_word <= whi; ++next_word) {
         u32* adst = ast + (next_word % NSLOT) * NAP * ROWS;
         const bool ok = next_word < a.wa32;
-        for (int q = tid; q < NAP * ROWS / 4; q += NT) {
+        for (int q = t0; q < NAP * ROWS / 4; q += nthr) {
           const int d = q / (ROWS / 4), r4 = q % (ROWS / 4);
           const u32* src = ok ? a.AT + ((int64_t)d * a.wa32 + next_word) * a.mpad + row0 + 4 * r4 : a.AT;
           cp_async16(adst + d * ROWS + 4 * r4, src, ok ? 16 : 0);
         }
       }
     }
-    cp_async_commit();
   };
 
   // phase 1: the two 16-entry half tables of block s (rows 0..KLO-1 and KLO..K-1)
@@ -229,7 +252,7 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
   // phase 2b: write replica number cc (of this thread's CPT) of entry g_own into table buffer tb.
   // The replica order is rotated by g so the 8 lanes of a store phase hit 8 different banks.
   auto phase2_store = [&](uint4* tb, const V<F> (&v)[4], int cc) {
-    if (g_own < E) {
+    if (!(ABL & 1) && g_own < E) {
       const int copy = (part * CPT + cc + g_own) & (COPIES - 1);
 #pragma unroll
       for (int d = 0; d < R; ++d)
@@ -274,36 +297,137 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
     }
   };
 
-  // lookups for block s from table buffer tb, software-pipelined one row-slot ahead
-  // (entries of t+1 and table rows of t in flight while t accumulates); `between(t)` runs
-  // after row-slot t.
+  // lookups for block s from table buffer tb, software-pipelined LA row-slots ahead (entries
+  // and table rows of t+1..t+LA in flight while t accumulates); `between(t)` runs after t.
+  constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4) ? 2 : 1;
   auto lookups = [&](int s, int tb, auto&& between) {
+    if constexpr (ABL & 4) {
+#pragma unroll
+      for (int t = 0; t < RT; ++t) between(t);
+      return;
+    }
     const unsigned char* tl = tl0 + tb * R * TPLANE;
-    u32 e[3];
-    entries(s, 0, e);
-    Rows<F> cur;
-    load_rows<F, TPL>(cur, tl, e);
+    Rows<F> ring[LA + 1];
+#pragma unroll
+    for (int t = 0; t < LA && t < RT; ++t) {
+      u32 e[3];
+      entries(s, t, e);
+      load_rows<F, TPL>(ring[t], tl, e);
+    }
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
-      Rows<F> nxt;
-      if (t + 1 < RT) {
-        entries(s, t + 1, e);
-        load_rows<F, TPL>(nxt, tl, e);
+      if (t + LA < RT) {
+        u32 e[3];
+        entries(s, t + LA, e);
+        load_rows<F, TPL>(ring[(t + LA) % (LA + 1)], tl, e);
       }
-      accumulate<F>(c[t], cur);
+      if constexpr (ABL & 2) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+#pragma unroll
+          for (int d = 0; d < Traits<F>::R; ++d) c[t].w[w][d] ^= comp(ring[t % (LA + 1)].v[0][d], w) ^ comp(ring[t % (LA + 1)].v[Traits<F>::NI - 1][d], w);
+      } else {
+        accumulate<F>(c[t], ring[t % (LA + 1)]);
+      }
       between(t);
-      if (t + 1 < RT) cur = nxt;
     }
   };
 
-  if constexpr (!PIPE) {
-    for (int i = 0; i < PD; ++i) issue(s_begin + i);
+  if constexpr (WS) {
+    constexpr int NB = NT + WS_BUILDERS;  // all threads take part in every FULL / EMPTY barrier
+    constexpr int NBT = WS_BUILDERS;
+    auto FULL = [](int s) { return 1 + (s & 1); };
+    auto EMPTY = [](int s) { return 3 + (s & 1); };
+    if (tid >= NT) {
+      // ------------------------------------------------ builder warps
+      const int bt = tid - NT;
+      auto bsync = [] { nbar_sync(5, NBT); };
+      issue_b(s_begin, bt, NBT);
+      issue_a(s_begin, bt, NBT);
+      cp_async_commit();
+      issue_b(s_begin + 1, bt, NBT);
+      cp_async_commit();
+      for (int s = s_begin; s < s_end; ++s) {
+        if (s >= s_begin + 2) nbar_sync(EMPTY(s), NB);  // lookups of block s-2 left tab[s & 1]
+        issue_b(s + 2, bt, NBT);
+        issue_a(s + 1, bt, NBT);
+        cp_async_commit();
+        cp_async_wait<1>();  // B rows of s and A words of s have landed (this thread's copies)
+        bsync();
+        // phase 1: 2 halves x 16 entries x 4 words = 128 items
+        {
+          const u32* bs = bst + (s % 3) * K * R * 4;
+          for (int item = bt; item < 128; item += NBT) {
+            const int h = item >> 6, e = (item >> 2) & 15, w = item & 3;
+            const int nrows = h ? KHI : KLO;
+            if (e < (1 << nrows)) {
+              V<F> acc = vzero<F>();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (i < nrows && ((e >> i) & 1)) {
+                  V<F> b;
+#pragma unroll
+                  for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
+                  vadd<F>(acc, b);
+                }
+              }
+#pragma unroll
+              for (int d = 0; d < R; ++d) thalf[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
+            }
+          }
+        }
+        bsync();
+        // phase 2: 256 entries x 8 replicas
+        uint4* tb = tab + (s & 1) * R * TPL;
+#pragma unroll
+        for (int it = 0; it < E / NBT; ++it) {
+          const int g = bt + NBT * it;
+          const uint4* lo = reinterpret_cast<const uint4*>(thalf + (g & ((1 << KLO) - 1)) * R * 4);
+          const uint4* hi = reinterpret_cast<const uint4*>(thalf + HALF + (g >> KLO) * R * 4);
+          V<F> v[4], hv[4];
+#pragma unroll
+          for (int d = 0; d < R; ++d) {
+            const uint4 L = lo[d], H = hi[d];
+            v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
+            hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
+          }
+#pragma unroll
+          for (int w = 0; w < 4; ++w) vadd<F>(v[w], hv[w]);
+          if constexpr (!(ABL & 1)) {
+#pragma unroll
+            for (int cc = 0; cc < COPIES; ++cc) {
+              const int copy = (cc + g) & (COPIES - 1);
+#pragma unroll
+              for (int d = 0; d < R; ++d)
+                tb[d * TPL + g * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
+            }
+          }
+        }
+        nbar_arrive(FULL(s), NB);  // table of block s (and A words of s) ready
+      }
+      cp_async_wait<0>();
+      return;
+    }
+    // ------------------------------------------------ lookup warps
+    for (int s = s_begin; s < s_end; ++s) {
+      nbar_sync(FULL(s), NB);
+      lookups(s, s & 1, [](int) {});
+      if (s + 2 < s_end) nbar_arrive(EMPTY(s), NB);
+    }
+  } else if constexpr (!PIPE) {
+    for (int i = 0; i < PD; ++i) {
+      issue_b(s_begin + i);
+      issue_a(s_begin + i);
+      cp_async_commit();
+    }
     cp_async_wait<PD - 1>();
     __syncthreads();
     for (int s = s_begin; s < s_end; ++s) {
       phase1(s);
       __syncthreads();
-      issue(s + PD);
+      issue_b(s + PD);
+      issue_a(s + PDA);
+      cp_async_commit();
       {
         V<F> v[4];
         phase2_compute(s, v);
@@ -315,7 +439,9 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
       lookups(s, 0, [](int) {});
     }
   } else {
-    for (int i = 0; i < PD; ++i) issue(s_begin + i);
+    for (int i = 0; i < PD; ++i) issue_b(s_begin + i);
+    for (int i = 0; i < PDA; ++i) issue_a(s_begin + i);
+    cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     phase1(s_begin);
@@ -329,7 +455,9 @@ __global__ void __launch_bounds__(NT, 1) m4rm_kernel(const M4rmArgs a) {
     if (s_begin + 1 < s_end) phase1(s_begin + 1);
     __syncthreads();
     for (int s = s_begin; s < s_end; ++s) {
-      issue(s + PD);
+      issue_b(s + PD);
+      issue_a(s + PDA);
+      cp_async_commit();
       const bool nxt = s + 1 < s_end;
       V<F> v[4];
       if (nxt) phase2_compute(s + 1, v);
@@ -480,42 +608,54 @@ __global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict_
 }
 
 // ------------------------------------------------------------------ registry
-template <int F, int K, int RT, bool PIPE, int NT>
+template <int F, int K, int RT, int SCHED, int NT>
 constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
-  constexpr int NSLOT = K == 8 ? (PIPE ? 4 : 3) : 2;
+  constexpr int NSLOT = K == 8 ? 3 : 2;
   constexpr int NAP = K == 8 ? 1 : R;
-  return (PIPE ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
+  return (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
          NSLOT * NAP * RT * NT * 4;
 }
 
-#define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, P, smem_bytes_for<F, K, RT, P, NT>(), 0, 0}
+#define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (P) == 2 ? (NT) + WS_BUILDERS : (NT), P, \
+                               smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0}
+#define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (P) == 2 ? (NT) + WS_BUILDERS : (NT), P, \
+                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A}
 // k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
 #define SG_KSET8(F)                                                                                 \
-  SG_K(F, 8, 1, false, 256), SG_K(F, 8, 2, false, 256), SG_K(F, 8, 4, false, 256), SG_K(F, 8, 8, false, 256), \
-  SG_K(F, 8, 1, true, 256), SG_K(F, 8, 2, true, 256), SG_K(F, 8, 4, true, 256),                      \
-  SG_K(F, 8, 2, false, 512), SG_K(F, 8, 4, false, 512), SG_K(F, 8, 2, true, 512)
+  SG_K(F, 8, 1, 0, 256), SG_K(F, 8, 2, 0, 256), SG_K(F, 8, 4, 0, 256), SG_K(F, 8, 8, 0, 256), \
+  SG_K(F, 8, 1, 1, 256), SG_K(F, 8, 2, 1, 256), SG_K(F, 8, 4, 1, 256),                      \
+  SG_K(F, 8, 2, 0, 512), SG_K(F, 8, 4, 0, 512), SG_K(F, 8, 2, 1, 512)
 #define SG_KSET8_2PLANE(F)                                                                          \
-  SG_K(F, 8, 16, false, 256), SG_K(F, 8, 8, true, 256), SG_K(F, 8, 16, true, 256),                  \
-  SG_K(F, 8, 8, false, 512), SG_K(F, 8, 4, true, 512), SG_K(F, 8, 8, true, 512)
+  SG_K(F, 8, 16, 0, 256), SG_K(F, 8, 8, 1, 256), SG_K(F, 8, 16, 1, 256),                  \
+  SG_K(F, 8, 8, 0, 512), SG_K(F, 8, 4, 1, 512), SG_K(F, 8, 8, 1, 512)
 // k < 8: parity and generality (k-invariance), one variant each + a pipelined k=5
 #define SG_KLOW(F)                                                                                  \
-  SG_K(F, 1, 1, false, 256), SG_K(F, 2, 1, false, 256), SG_K(F, 3, 1, false, 256), SG_K(F, 4, 1, false, 256), \
-  SG_K(F, 5, 1, false, 256), SG_K(F, 6, 1, false, 256), SG_K(F, 7, 1, false, 256), SG_K(F, 5, 1, true, 256)
+  SG_K(F, 1, 1, 0, 256), SG_K(F, 2, 1, 0, 256), SG_K(F, 3, 1, 0, 256), SG_K(F, 4, 1, 0, 256), \
+  SG_K(F, 5, 1, 0, 256), SG_K(F, 6, 1, 0, 256), SG_K(F, 7, 1, 0, 256), SG_K(F, 5, 1, 1, 256)
 
 static KernelInfo g_kernels[] = {
+    SG_K(F2, 8, 16, 2, 256), SG_K(F3, 8, 16, 2, 256), SG_K(GF4, 8, 16, 2, 256), SG_K(F3, 8, 8, 2, 256),
+    SG_K(GF4, 8, 8, 2, 256), SG_K(F5, 8, 8, 2, 256), SG_K(F7, 8, 8, 2, 256), SG_K(F5, 8, 4, 2, 256),
+    SG_K(F7, 8, 4, 2, 256),
     SG_KSET8(F2), SG_KSET8_2PLANE(F2), SG_KLOW(F2),
     SG_KSET8(F3), SG_KSET8_2PLANE(F3), SG_KLOW(F3),
     SG_KSET8(GF4), SG_KSET8_2PLANE(GF4), SG_KLOW(GF4),
-    SG_KSET8(F5), SG_KLOW(F5),
-    SG_KSET8(F7), SG_KLOW(F7),
+    SG_KSET8(F5), SG_K(F5, 8, 8, 1, 256), SG_K(F5, 8, 4, 1, 512), SG_KLOW(F5),
+    SG_KSET8(F7), SG_K(F7, 8, 8, 1, 256), SG_K(F7, 8, 4, 1, 512), SG_KLOW(F7),
+    // ablation variants (never chosen by the planner; selected by sg_set_ablation)
+    SG_KA(F3, 8, 16, 0, 256, 1), SG_KA(F3, 8, 16, 0, 256, 2), SG_KA(F3, 8, 16, 0, 256, 4),
+    SG_KA(F3, 8, 16, 0, 256, 3), SG_KA(F3, 8, 16, 1, 256, 1), SG_KA(F3, 8, 16, 1, 256, 2),
+    SG_KA(F3, 8, 16, 1, 256, 4), SG_KA(F7, 8, 8, 1, 256, 1), SG_KA(F7, 8, 8, 1, 256, 2),
+    SG_KA(F7, 8, 8, 1, 256, 4), SG_KA(F3, 8, 16, 2, 256, 1), SG_KA(F3, 8, 16, 2, 256, 2),
+    SG_KA(F3, 8, 16, 2, 256, 4), SG_KA(F7, 8, 8, 2, 256, 2), SG_KA(F7, 8, 8, 2, 256, 4),
 };
 
 int m4rm_kernel_count() { return (int)(sizeof(g_kernels) / sizeof(g_kernels[0])); }
 KernelInfo* m4rm_kernel_at(int i) { return &g_kernels[i]; }
 
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st) {
-  ki.fn<<<grid, ki.threads, ki.smem_bytes, st>>>(a);
+  ki.fn<<<grid, ki.launch_threads, ki.smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
 

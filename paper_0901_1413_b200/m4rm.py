@@ -114,7 +114,7 @@ def plan(field, m: int, l: int, n: int, k: int = 8) -> dict:
     _lib.check(_lib.load().sg_plan(field.code, m, l, n, k, ctypes.byref(rows), ctypes.byref(splits),
                                    ctypes.byref(ctas), ctypes.byref(idx), ctypes.byref(pipe), ctypes.byref(thr)))
     return {"rows_per_cta": rows.value, "splits": splits.value, "ctas": ctas.value, "kernel": idx.value,
-            "pipelined": bool(pipe.value), "threads": thr.value}
+            "schedule": ("serial", "pipelined", "warp-specialized")[pipe.value], "threads": thr.value}
 
 
 def set_plan_override(rows_per_thread: int = 0, splits: int = 0, pipe: int = -1, threads: int = 0):

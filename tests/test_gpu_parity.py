@@ -123,7 +123,7 @@ def test_every_compiled_plan(fname):
     want = expect(fname, A, B)
     ran = 0
     for rt in (1, 2, 4, 8, 16):
-        for pipe in (0, 1):
+        for pipe in (0, 1, 2):
             for nt in (256, 512):
                 for splits in (1, 2, 5, 16):
                     m4rm_mod.set_plan_override(rt, splits, pipe, nt)
@@ -134,7 +134,7 @@ def test_every_compiled_plan(fname):
                         continue
                     ran += 1
                     assert np.array_equal(C.planes_numpy(), want), (fname, rt, pipe, nt, splits)
-    assert ran >= 32
+    assert ran >= 40
 
 
 @pytest.mark.parametrize("fname", list(FIELDS))

@@ -31,7 +31,7 @@ for ci in [int(x) for x in a.configs.split(",")]:
     best = None
     for rt in (1, 2, 4, 8, 16):
         for nt in (256, 512):
-            for pipe in (0, 1):
+            for pipe in (0, 1, 2):
                 for sp in [int(x) for x in a.splits.split(",")]:
                     M.set_plan_override(rt, sp, pipe, nt)
                     try:
