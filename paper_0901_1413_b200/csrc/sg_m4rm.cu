@@ -87,14 +87,17 @@ __device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
       const u32 x0 = comp(r.v[0][0], w), x1 = comp(r.v[0][1], w), x2 = comp(r.v[0][2], w);
       const u32 y0 = comp(r.v[1][0], w), y1 = comp(r.v[1][1], w), y2 = comp(r.v[1][2], w);
       const u32 z0 = comp(r.v[2][0], w), z1 = comp(r.v[2][1], w), z2 = comp(r.v[2][2], w);
+      // (x + 2y) does not depend on C: only two adds sit on the accumulator's dependency chain.
       if constexpr (F == F7) {  // 2y = (y2, y0, y1), 4z = (z1, z2, z0) mod 7; 3 x 8 LOP3
-        f7_add(q[0], q[1], q[2], x0, x1, x2);
-        f7_add(q[0], q[1], q[2], y2, y0, y1);
+        u32 s0 = x0, s1 = x1, s2 = x2;
+        f7_add(s0, s1, s2, y2, y0, y1);
         f7_add(q[0], q[1], q[2], z1, z2, z0);
+        f7_add(q[0], q[1], q[2], s0, s1, s2);
       } else {  // mod 15: x = (x0,x1,x2,0), 2y = (0,y0,y1,y2), 4z = (z2,0,z0,z1)
-        add15(q[0], q[1], q[2], q[3], x0, x1, x2, 0u);
-        add15(q[0], q[1], q[2], q[3], 0u, y0, y1, y2);
+        u32 s0 = x0, s1 = x1, s2 = x2, s3 = 0u;
+        add15(s0, s1, s2, s3, 0u, y0, y1, y2);
         add15(q[0], q[1], q[2], q[3], z2, 0u, z0, z1);
+        add15(q[0], q[1], q[2], q[3], s0, s1, s2, s3);
       }
     }
   }

@@ -46,23 +46,31 @@ def exact_gpu_product(fname, A, B):
     return out
 
 
-def freivalds(fname, A, B, C, trials=2):
+def _matvec(M, x, p, step=2048):
+    """(M @ x) mod p in int64, row-chunked (no full-size int64 temporaries)."""
+    out = np.empty(M.shape[0], dtype=np.int64)
+    for r0 in range(0, M.shape[0], step):
+        out[r0:r0 + step] = (M[r0:r0 + step].astype(np.int64) @ x) % p
+    return out
+
+
+def freivalds(fname, A, B, C, trials=6):
     rng = np.random.default_rng(0)
-    p = 2 if fname == "gf4" else oracle.ORDER[fname]
-    if fname == "gf4":  # check both coefficient planes as F2 products of the closed form
-        a0, a1 = (A & 1).astype(np.int64), (A >> 1).astype(np.int64)
-        b0, b1 = (B & 1).astype(np.int64), (B >> 1).astype(np.int64)
-        c0, c1 = (C & 1).astype(np.int64), (C >> 1).astype(np.int64)
+    if fname == "gf4":  # both coefficient planes of the closed form, over F2
+        a0, a1 = A & 1, A >> 1
+        b0, b1 = B & 1, B >> 1
+        c0, c1 = C & 1, C >> 1
         for _ in range(trials):
             x = rng.integers(0, 2, size=B.shape[1], dtype=np.int64)
-            bx0, bx1 = b0 @ x, b1 @ x
-            assert np.array_equal((c0 @ x) % 2, (a0 @ bx0 + a1 @ bx1) % 2)
-            assert np.array_equal((c1 @ x) % 2, (a0 @ bx1 + a1 @ bx0 + a1 @ bx1) % 2)
+            bx0, bx1 = _matvec(b0, x, 2), _matvec(b1, x, 2)
+            assert np.array_equal(_matvec(c0, x, 2), (_matvec(a0, bx0, 2) + _matvec(a1, bx1, 2)) % 2)
+            assert np.array_equal(_matvec(c1, x, 2),
+                                  (_matvec(a0, bx1, 2) + _matvec(a1, bx0, 2) + _matvec(a1, bx1, 2)) % 2)
         return
+    p = oracle.ORDER[fname]
     for _ in range(trials):
         x = rng.integers(0, p, size=B.shape[1], dtype=np.int64)
-        bx = (B.astype(np.int64) @ x) % p
-        assert np.array_equal((C.astype(np.int64) @ x) % p, (A.astype(np.int64) @ bx) % p)
+        assert np.array_equal(_matvec(C, x, p), _matvec(A, _matvec(B, x, p), p))
 
 
 @pytest.mark.parametrize("fname,m,l,n", CONFIGS)
