@@ -41,12 +41,21 @@ CONFIGS = [
     ("F3 32768x32768x32768 k=8", "f3", 32768, 32768, 32768),
 ]
 HEADLINE = 1
+# dram__bytes_read.sum + dram__bytes_write.sum of the M4RM kernel per launch, from the committed
+# `ncu --set full` captures (profiles/*_traffic.json, written by tools/traffic_from_ncu.py)
+TRAFFIC = {}
+for _f in sorted(os.listdir(os.path.join(ROOT, "profiles"))) if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
+    if _f.endswith("_traffic.json"):
+        with open(os.path.join(ROOT, "profiles", _f)) as _fh:
+            TRAFFIC.update(json.load(_fh))
 METRIC = "field mul-adds/sec (m*l*n/t) for C=A*B over F3/F5/F7/GF(4), % of roofline"
 UNIT = "mul-adds/s"
 
 # Algorithmic work per field mul-add for the accumulate phase: LOP3 count of
 # the reference formulas and shared-memory table bytes; plus the table build once per GPU.
 LOP3_PER_MULADD = {"f2": 1 / 256, "f3": 9 / 256, "f5": 42 / 256, "f7": 32 / 256, "gf4": 3 / 256}
+# ... and the LOP3 count of this kernel's own networks (csrc/sg_field.cuh)
+OWN_LOP3_PER_MULADD = {"f2": 1 / 256, "f3": 6 / 256, "f5": 20 / 256, "f7": 18 / 256, "gf4": 3 / 256}
 SMEM_PER_MULADD = {"f2": 4 / 256, "f3": 16 / 256, "f5": 36 / 256, "f7": 36 / 256, "gf4": 16 / 256}
 TABLE_LOP3_PER_WORD = {"f2": 1, "f3": 5, "f5": 12, "f7": 10, "gf4": 2}  # one field add, 32-bit word
 PLANES = {"f2": 1, "f3": 2, "f5": 3, "f7": 3, "gf4": 2}
@@ -190,22 +199,32 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
     p_smem = peaks["lds_bytes_per_clk_per_sm"] * sms * clk_hz
     words32 = 2 * ((n + 63) // 64)
     table_lop3 = (l / 8.0) * 255 * words32 * TABLE_LOP3_PER_WORD[field]
-    lop3 = work * LOP3_PER_MULADD[field] + table_lop3
-    smem = work * SMEM_PER_MULADD[field]
-    lop3_bound, smem_bound = lop3 / p_lop3, smem / p_smem
-    bound = "lop3" if lop3_bound >= smem_bound else "smem"
-    if bound == "lop3":
-        roof = {"bound": "lop3 (integer-logic pipe)", "achieved": lop3 / (k_ms * 1e-3) / 1e12, "peak": p_lop3 / 1e12,
-                "unit": "TLOP3/s"}
-    else:
-        roof = {"bound": "smem (LDS bandwidth)", "achieved": smem / (k_ms * 1e-3) / 1e12, "peak": p_smem / 1e12,
-                "unit": "TB/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+
+    def roofline(c_lop3):
+        lop3 = work * c_lop3 + table_lop3
+        smem = work * SMEM_PER_MULADD[field]
+        lop3_t, smem_t = lop3 / p_lop3, smem / p_smem
+        if lop3_t >= smem_t:
+            r = {"bound": "lop3 (integer-logic pipe)", "achieved": lop3 / (k_ms * 1e-3) / 1e12, "peak": p_lop3 / 1e12,
+                 "unit": "TLOP3/s"}
+        else:
+            r = {"bound": "smem (LDS bandwidth)", "achieved": smem / (k_ms * 1e-3) / 1e12, "peak": p_smem / 1e12,
+                 "unit": "TB/s"}
+        r["frac"] = r["achieved"] / r["peak"]
+        r["roofline_muladds_per_s"] = work / max(lop3_t, smem_t)
+        return r
+
+    roof = roofline(LOP3_PER_MULADD[field])
+    own = roofline(OWN_LOP3_PER_MULADD[field])
+    roof["definition"] = ("SURVEY.md 8d: algorithmic LOP3 = the reference formulas' SASS count per mul-add "
+                          "(+ one table build per GPU), LDS bytes = table lookups; binding = the slower of the two")
+    roof["own_ops"] = {"bound": own["bound"], "frac": own["frac"], "roofline_muladds_per_s": own["roofline_muladds_per_s"],
+                       "definition": "same, with this kernel's own LOP3 networks (fewer ops than the reference's)"}
+    roof["traffic"] = TRAFFIC.get(name)
+    roof["traffic_source"] = TRAFFIC.get("_source") if name in TRAFFIC else None
     roof["kernel_ms"] = k_ms
     roof["kernel_share_of_step"] = k_ms / ms_per_step if world == 1 else None
     roof["achieved_muladds_per_s"] = work / (k_ms * 1e-3)
-    roof["roofline_muladds_per_s"] = work / max(lop3_bound, smem_bound)
     roof["peak_source"] = ("sg_probe_peaks on this GPU: %.1f LOP3/clk/SM, %.1f LDS B/clk/SM, x %d SMs x %.0f MHz (%s)"
                            % (peaks["lop3_per_clk_per_sm"], peaks["lds_bytes_per_clk_per_sm"], sms,
                               peaks["clock_mhz_for_peak"], peaks["clock_note"]))
@@ -367,6 +386,7 @@ def main():
             r = run_config(cfg, args, world, rank, device, peaks, e2e=False)
             per_config[cfg[0]] = {"value": r["value"], "ms_per_step": r["ms_per_step"],
                                   "roofline_frac": r["roofline"]["frac"], "bound": r["roofline"]["bound"],
+                                  "own_ops_frac": r["roofline"]["own_ops"]["frac"],
                                   "kernel_ms": r["roofline"]["kernel_ms"],
                                   "achieved_muladds_per_s": r["roofline"]["achieved_muladds_per_s"],
                                   "plan": r["plan"], "clocks": r["clocks"]}

@@ -112,6 +112,87 @@ struct Plan {
   double est_clk = 0;
 };
 
+// Measured per-CTA cost of the k = 8 variants on B200 (tools/tune.py over BASELINE.json's
+// configs, least-squares fit of  time = waves * (blocks_per_cta * blk + cta), max error 2 %):
+// {field, rows per thread, lookup threads, schedule, clocks per k-block, clocks per CTA}.
+struct Calib {
+  int field, rt, threads, sched;
+  double blk, cta;
+};
+const Calib g_calib[] = {
+    {1, 1, 256, 0, 981, 2000},
+    {1, 1, 256, 1, 1370, 2000},
+    {1, 2, 256, 0, 1128, 3599},
+    {1, 2, 256, 1, 1464, 2000},
+    {1, 2, 512, 0, 1923, 10250},
+    {1, 2, 512, 1, 1743, 9667},
+    {1, 4, 256, 0, 1473, 7689},
+    {1, 4, 256, 1, 1918, 13176},
+    {1, 4, 512, 0, 2440, 16050},
+    {1, 4, 512, 1, 2440, 19580},
+    {1, 8, 256, 0, 2415, 16466},
+    {1, 8, 256, 1, 2319, 18520},
+    {1, 8, 256, 2, 2120, 19139},
+    {1, 8, 512, 0, 3704, 18719},
+    {1, 8, 512, 1, 3858, 35806},
+    {1, 16, 256, 0, 3590, 26509},
+    {1, 16, 256, 1, 3614, 29204},
+    {1, 16, 256, 2, 3294, 31731},
+    {2, 1, 256, 0, 1831, 2161},
+    {2, 1, 256, 1, 2313, 6120},
+    {2, 2, 256, 0, 2253, 4755},
+    {2, 2, 256, 1, 2598, 10576},
+    {2, 2, 512, 0, 3872, 17275},
+    {2, 2, 512, 1, 3707, 19021},
+    {2, 4, 256, 0, 3581, 16786},
+    {2, 4, 256, 1, 3246, 17972},
+    {2, 4, 256, 2, 2874, 18294},
+    {2, 4, 512, 0, 5395, 35211},
+    {2, 4, 512, 1, 5482, 37901},
+    {2, 8, 256, 0, 5032, 35651},
+    {2, 8, 256, 1, 4735, 38088},
+    {2, 8, 256, 2, 6609, 38362},
+    {3, 1, 256, 0, 1695, 4137},
+    {3, 1, 256, 1, 2256, 5876},
+    {3, 2, 256, 0, 2005, 7299},
+    {3, 2, 256, 1, 2505, 9759},
+    {3, 2, 512, 0, 3548, 14336},
+    {3, 2, 512, 1, 3454, 17003},
+    {3, 4, 256, 0, 3309, 15053},
+    {3, 4, 256, 1, 3146, 16990},
+    {3, 4, 256, 2, 2791, 16104},
+    {3, 4, 512, 0, 4881, 26995},
+    {3, 4, 512, 1, 4886, 31968},
+    {3, 8, 256, 0, 4594, 29216},
+    {3, 8, 256, 1, 4532, 31535},
+    {3, 8, 256, 2, 4203, 31339},
+    {4, 1, 256, 0, 986, 2000},
+    {4, 1, 256, 1, 1301, 4015},
+    {4, 2, 256, 0, 1138, 2693},
+    {4, 2, 256, 1, 1414, 6175},
+    {4, 2, 512, 0, 1765, 9289},
+    {4, 2, 512, 1, 1746, 10665},
+    {4, 4, 256, 0, 1494, 6096},
+    {4, 4, 256, 1, 1717, 9997},
+    {4, 4, 512, 0, 2471, 17760},
+    {4, 4, 512, 1, 2415, 19116},
+    {4, 8, 256, 0, 2338, 18147},
+    {4, 8, 256, 1, 2291, 18981},
+    {4, 8, 256, 2, 2186, 18743},
+    {4, 8, 512, 0, 3663, 35513},
+    {4, 8, 512, 1, 3651, 35671},
+    {4, 16, 256, 0, 3558, 35759},
+    {4, 16, 256, 1, 3542, 36911},
+    {4, 16, 256, 2, 3314, 37255},
+};
+
+const Calib* calib_for(const KernelInfo* ki) {
+  if (ki->k != 8) return nullptr;
+  for (const Calib& c : g_calib)
+    if (c.field == ki->field && c.rt == ki->rt && c.threads == ki->threads && c.sched == ki->sched) return &c;
+  return nullptr;
+}
+
 // Per-lane (4 words) ALU instructions and shared-memory bytes per (row, k-block), and the
 // table-build ALU work per entry; see DESIGN.md "Planner".
 void field_costs(int f, double* lane_alu, double* lane_smem, double* entry_alu) {
@@ -153,6 +234,7 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
     const double t_block = ki->sched == 2   ? std::max(alu_l + alu_t, smem_l + smem_t) + 100.0
                            : ki->sched == 1 ? std::max(alu_l + alu_t, smem_l + smem_t) + 250.0
                                             : std::max(alu_l, smem_l) + std::max(alu_t, smem_t) + 400.0;
+    const Calib* cal = calib_for(ki);
     const int occ = std::max(1, ki->occupancy);
     const int max_splits = std::max(1, std::min(nblocks, 64));
     for (int sp = 1; sp <= max_splits; ++sp) {
@@ -161,7 +243,9 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
       const int splits = (nblocks + bps - 1) / bps;
       if (splits != sp) continue;
       const double ctas = (double)slabs * rgroups * splits;
-      const double t_cta = bps * t_block + 3000.0;
+      // calibrated variants: measured per-block and per-CTA clocks; others: the analytic
+      // model with a 25 % penalty, so a measured variant wins unless clearly worse
+      const double t_cta = cal ? bps * cal->blk + cal->cta : 1.25 * (bps * t_block + 3000.0);
       const double waves = std::ceil(ctas / (ds.sms * occ));
       double est = waves * t_cta * std::min<double>(occ, ctas / ds.sms > 1 ? occ : 1);
       if (splits > 1) {

@@ -29,11 +29,11 @@ constexpr int LOP_XOR3 = 0x96, LOP_MAJ = 0xE8, LOP_AND2 = 0xC0;
 
 template <int F> struct Traits;
 // R = bit planes per element; NI = table lookups per (row, k-block) = basis size;
-// RS = planes of the M4RM kernel's row accumulator (F5 accumulates mod 15 in 4 planes).
+// RS = planes of the M4RM kernel's row accumulator (carry-save: F5 5 planes mod 15, F7 4).
 template <> struct Traits<F2>  { static constexpr int R = 1, NI = 1, RS = 1; };
 template <> struct Traits<F3>  { static constexpr int R = 2, NI = 2, RS = 2; };
-template <> struct Traits<F5>  { static constexpr int R = 3, NI = 3, RS = 4; };
-template <> struct Traits<F7>  { static constexpr int R = 3, NI = 3, RS = 3; };
+template <> struct Traits<F5>  { static constexpr int R = 3, NI = 3, RS = 5; };
+template <> struct Traits<F7>  { static constexpr int R = 3, NI = 3, RS = 4; };
 template <> struct Traits<GF4> { static constexpr int R = 2, NI = 2, RS = 2; };
 
 // ---------------------------------------------------------------- F3
@@ -157,6 +157,64 @@ __device__ __forceinline__ void mod15_to_f5(u32 v0, u32 v1, u32 v2, u32 v3, u32&
   r0 = lop3<0x29>(v2, w4, w6);
   r1 = lop3<0x14>(v1, v3, w5);
   r2 = lop3<0x24>(v0, v2, w6);
+}
+
+// ---------------------------------------------------------------- carry-save row accumulators
+// C += x + 2y + 4z as ONE multi-operand carry-save addition (full adder = xor3 + majority, a
+// carry out of the top column re-enters column 0), generated and verified lane-exactly by
+// tools/lop3/csa_gen.py from the adder schedule found by tools/lop3/csa_plan.py.
+// F7: 18 LOP3 per (row, k-block, word) against 3 x 8 for three sequential mod-7 adds; the
+//     accumulator keeps two bits in column 0: value = q0 + k0 + 2 q1 + 4 q2 (mod 7).
+__device__ __forceinline__ void f7_acc(u32& q_0, u32& k_0, u32& q_1, u32& q_2, u32 x0, u32 x1, u32 x2,
+                                       u32 y0, u32 y1, u32 y2, u32 z0, u32 z1, u32 z2) {
+  const u32 t1 = lop3<0x96>(q_0, k_0, x0);
+  const u32 t2 = lop3<0xe8>(q_0, k_0, x0);
+  const u32 t3 = lop3<0x96>(y2, z1, t1);
+  const u32 t4 = lop3<0xe8>(y2, z1, t1);
+  const u32 t5 = lop3<0x96>(q_1, x1, y0);
+  const u32 t6 = lop3<0xe8>(q_1, x1, y0);
+  const u32 t7 = lop3<0x96>(q_2, x2, y1);
+  const u32 t8 = lop3<0xe8>(q_2, x2, y1);
+  const u32 t9 = lop3<0x96>(z0, t6, t7);
+  const u32 t10 = lop3<0xe8>(z0, t6, t7);
+  const u32 t11 = lop3<0x96>(t8, t3, t10);
+  const u32 t12 = lop3<0xe8>(t8, t3, t10);
+  const u32 t13 = lop3<0x96>(z2, t2, t5);
+  const u32 t14 = lop3<0xe8>(z2, t2, t5);
+  const u32 t15 = lop3<0x96>(t4, t13, t12);
+  const u32 t16 = lop3<0xe8>(t4, t13, t12);
+  const u32 t17 = lop3<0x96>(t9, t14, t16);
+  const u32 t18 = lop3<0xe8>(t9, t14, t16);
+  q_0 = t11; k_0 = t18; q_1 = t15; q_2 = t17;
+}
+// F5, accumulated mod 15 (5 | 15): 4z is replaced by -z (4 == -1 mod 5) and -z = ~z - 8 in
+// 4-bit one's complement, so the complemented z bits are free LOP3 input inversions and each
+// k-block adds x + 2y + (7 - z) == x + 2y + 4z + 2 (mod 5); the kernel pre-pays -2 per k-block
+// in the accumulator's initial value.  20 LOP3 against 32 for three one's-complement adds.
+// value = q0 + 2 q1 + 4 q2 + 4 k2 + 8 q3 (mod 15).
+__device__ __forceinline__ void f5_acc(u32& q_0, u32& q_1, u32& q_2, u32& k_2, u32& q_3, u32 x0, u32 x1,
+                                       u32 x2, u32 y0, u32 y1, u32 y2, u32 z0, u32 z1, u32 z2) {
+  const u32 t1 = lop3<0x69>(q_0, x0, z0);
+  const u32 t2 = lop3<0xd4>(q_0, x0, z0);
+  const u32 t3 = lop3<0x96>(q_1, x1, y0);
+  const u32 t4 = lop3<0xe8>(q_1, x1, y0);
+  const u32 t5 = lop3<0x69>(z1, t2, t3);
+  const u32 t6 = lop3<0x8e>(z1, t2, t3);
+  const u32 t7 = lop3<0x96>(q_2, k_2, x2);
+  const u32 t8 = lop3<0xe8>(q_2, k_2, x2);
+  const u32 t9 = lop3<0x69>(y1, z2, t4);
+  const u32 t10 = lop3<0xb2>(y1, z2, t4);
+  const u32 t11 = lop3<0x96>(t7, t6, t9);
+  const u32 t12 = lop3<0xe8>(t7, t6, t9);
+  const u32 t13 = lop3<0x96>(q_3, y2, t8);
+  const u32 t14 = lop3<0xe8>(q_3, y2, t8);
+  const u32 t15 = lop3<0x96>(t10, t13, t12);
+  const u32 t16 = lop3<0xe8>(t10, t13, t12);
+  const u32 t17 = lop3<0x96>(t1, t14, t16);
+  const u32 t18 = lop3<0xe8>(t1, t14, t16);
+  const u32 t19 = lop3<0x96>(t5, t18, 0u);
+  const u32 t20 = lop3<0xe8>(t5, t18, 0u);
+  q_0 = t17; q_1 = t19; q_2 = t11; k_2 = t20; q_3 = t15;
 }
 
 // ---------------------------------------------------------------- generic row helpers

@@ -87,39 +87,34 @@ __device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
       const u32 x0 = comp(r.v[0][0], w), x1 = comp(r.v[0][1], w), x2 = comp(r.v[0][2], w);
       const u32 y0 = comp(r.v[1][0], w), y1 = comp(r.v[1][1], w), y2 = comp(r.v[1][2], w);
       const u32 z0 = comp(r.v[2][0], w), z1 = comp(r.v[2][1], w), z2 = comp(r.v[2][2], w);
-      // (x + 2y) does not depend on C: only two adds sit on the accumulator's dependency chain.
-      if constexpr (F == F7) {  // 2y = (y2, y0, y1), 4z = (z1, z2, z0) mod 7; 3 x 8 LOP3
-        u32 s0 = x0, s1 = x1, s2 = x2;
-        f7_add(s0, s1, s2, y2, y0, y1);
-        f7_add(q[0], q[1], q[2], z1, z2, z0);
-        f7_add(q[0], q[1], q[2], s0, s1, s2);
-      } else {  // mod 15: x = (x0,x1,x2,0), 2y = (0,y0,y1,y2), 4z = (z2,0,z0,z1)
-        u32 s0 = x0, s1 = x1, s2 = x2, s3 = 0u;
-        add15(s0, s1, s2, s3, 0u, y0, y1, y2);
-        add15(q[0], q[1], q[2], q[3], z2, 0u, z0, z1);
-        add15(q[0], q[1], q[2], q[3], s0, s1, s2, s3);
+      if constexpr (F == F7) {
+        f7_acc(q[0], q[1], q[2], q[3], x0, x1, x2, y0, y1, y2, z0, z1, z2);
+      } else {
+        f5_acc(q[0], q[1], q[2], q[3], q[4], x0, x1, x2, y0, y1, y2, z0, z1, z2);
       }
     }
   }
 }
 
-// Accumulator -> output planes (canonical for the final C; F5 always leaves mod 15 here).
+// Accumulator -> output planes (canonical for the final C and for split-K partials of F5).
+// F7 accumulator (q0, k0, q1, q2): value = (q0,q1,q2) + k0 mod 7.  F5 (q0, q1, q2, k2, q3):
+// value = (q0,q1,q2,q3) + 4 k2 mod 15, then mod 5.
 template <int F> __device__ __forceinline__ void finish(const u32 (&q)[Traits<F>::RS], u32 (&o)[Traits<F>::R],
                                                         bool canonical) {
   if constexpr (F == F5) {
-    mod15_to_f5(q[0], q[1], q[2], q[3], o[0], o[1], o[2]);
+    u32 v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[4];
+    add15(v0, v1, v2, v3, 0u, 0u, q[3], 0u);
+    mod15_to_f5(v0, v1, v2, v3, o[0], o[1], o[2]);
+  } else if constexpr (F == F7) {
+    o[0] = q[0]; o[1] = q[2]; o[2] = q[3];
+    f7_add(o[0], o[1], o[2], q[1], 0u, 0u);
+    if (canonical) f7_reduce(o[0], o[1], o[2]);
   } else {
 #pragma unroll
     for (int d = 0; d < Traits<F>::R; ++d) o[d] = q[d];
-    if constexpr (F == F7) {
-      if (canonical) f7_reduce(o[0], o[1], o[2]);
-    }
   }
 }
 
-// PIPE = false: per k-block  phase1 | sync | phase2 | sync | lookups   (one table buffer)
-// PIPE = true : per k-block  lookups(s) + phase2(s+1) + phase1(s+2) | sync  (two table buffers):
-//               the next table is written while the current one is read, one barrier per block.
 // Named barriers (id 0 is __syncthreads) for the warp-specialized schedule.
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -264,12 +259,20 @@ __global__ void __launch_bounds__(SCHED == 2 ? NT + WS_BUILDERS : NT, 1) m4rm_ke
   };
 
   Acc<F> c[RT];
+  // F5: every k-block adds x + 2y + 4z + 2 (mod 5) (see f5_acc); start from -2 * blocks mod 5.
+  u32 init[5] = {0u, 0u, 0u, 0u, 0u};
+  if constexpr (F == F5) {
+    const int v = (5 - (2 * (s_end - s_begin)) % 5) % 5;
+    init[0] = (v & 1) ? ~0u : 0u;
+    init[1] = (v & 2) ? ~0u : 0u;
+    init[2] = (v & 4) ? ~0u : 0u;
+  }
 #pragma unroll
   for (int t = 0; t < RT; ++t)
 #pragma unroll
     for (int w = 0; w < 4; ++w)
 #pragma unroll
-      for (int d = 0; d < Traits<F>::RS; ++d) c[t].w[w][d] = 0u;
+      for (int d = 0; d < Traits<F>::RS; ++d) c[t].w[w][d] = init[d];
 
   const unsigned char* tl0 = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
 
