@@ -540,36 +540,72 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   if (m == 0 || n == 0) return SG_OK;
   SG_CUDA(cudaSetDevice(device), "sg_m4rm_host set device");
   const int R = planes(field);
-  const size_t a_bytes = (size_t)R * m * w64_of(l) * 8, b_bytes = (size_t)R * l * w64_of(n) * 8,
-               c_bytes = (size_t)R * m * w64_of(n) * 8;
-  static std::map<int, std::pair<cudaStream_t, Buf>> io;  // per device: stream + staging buffer
+  const int64_t wa = w64_of(l), wc = w64_of(n);
+  const size_t a_bytes = (size_t)R * m * wa * 8, b_bytes = (size_t)R * l * wc * 8, c_bytes = (size_t)R * m * wc * 8;
+  // Row-chunked pipeline: B goes up first, then chunk i's rows of A go up while chunk i-1 is
+  // multiplied and chunk i-2's rows of C come down (three streams, events between them).
+  const int P = (int)std::max<int64_t>(1, std::min<int64_t>(4, m / 2048));
+  struct Io {
+    cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+    cudaEvent_t ev_in[4], ev_comp[4];
+    Buf buf;
+  };
+  static std::map<int, Io> io;
+  Io* d;
   char* dbuf = nullptr;
-  cudaStream_t st;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    auto& slot = io[device];
-    if (!slot.first) SG_CUDA(cudaStreamCreateWithFlags(&slot.first, cudaStreamNonBlocking), "sg_m4rm_host stream");
-    st = slot.first;
-    const size_t need = a_bytes + b_bytes + c_bytes + 3 * 256;
-    if (slot.second.bytes < need) {
-      if (slot.second.p) cudaFree(slot.second.p);
-      slot.second.p = nullptr;
-      slot.second.bytes = 0;
-      SG_CUDA(cudaMalloc(&slot.second.p, need), "sg_m4rm_host alloc");
-      slot.second.bytes = need;
+    d = &io[device];
+    if (!d->in) {
+      SG_CUDA(cudaStreamCreateWithFlags(&d->in, cudaStreamNonBlocking), "sg_m4rm_host stream");
+      SG_CUDA(cudaStreamCreateWithFlags(&d->comp, cudaStreamNonBlocking), "sg_m4rm_host stream");
+      SG_CUDA(cudaStreamCreateWithFlags(&d->out, cudaStreamNonBlocking), "sg_m4rm_host stream");
+      for (int i = 0; i < 4; ++i) {
+        SG_CUDA(cudaEventCreateWithFlags(&d->ev_in[i], cudaEventDisableTiming), "sg_m4rm_host event");
+        SG_CUDA(cudaEventCreateWithFlags(&d->ev_comp[i], cudaEventDisableTiming), "sg_m4rm_host event");
+      }
     }
-    dbuf = (char*)slot.second.p;
+    const size_t need = a_bytes + b_bytes + c_bytes + 16 * 256;
+    if (d->buf.bytes < need) {
+      if (d->buf.p) {
+        cudaDeviceSynchronize();
+        cudaFree(d->buf.p);
+      }
+      d->buf.p = nullptr;
+      d->buf.bytes = 0;
+      SG_CUDA(cudaMalloc(&d->buf.p, need), "sg_m4rm_host alloc");
+      d->buf.bytes = need;
+    }
+    dbuf = (char*)d->buf.p;
   }
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  uint64_t* dA = (uint64_t*)dbuf;
-  uint64_t* dB = (uint64_t*)(dbuf + up(a_bytes));
-  uint64_t* dC = (uint64_t*)(dbuf + up(a_bytes) + up(b_bytes));
-  if (a_bytes) SG_CUDA(cudaMemcpyAsync(dA, A, a_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D A");
-  if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D B");
-  rc = sg_m4rm(field, dA, dB, dC, m, l, n, k, nullptr, 0, st);
-  if (rc != SG_OK) return rc;
-  SG_CUDA(cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st), "sg_m4rm_host D2H C");
-  SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
+  uint64_t* dB = (uint64_t*)dbuf;
+  char* cur = dbuf + up(b_bytes);
+  if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, d->in), "sg_m4rm_host H2D B");
+  for (int i = 0; i < P; ++i) {
+    const int64_t r0 = m * i / P, r1 = m * (i + 1) / P, rows = r1 - r0;
+    uint64_t* dA = (uint64_t*)cur;
+    cur += up((size_t)R * rows * wa * 8);
+    uint64_t* dC = (uint64_t*)cur;
+    cur += up((size_t)R * rows * wc * 8);
+    if (rows == 0) continue;
+    // this chunk's rows of every plane of A: R rows of rows*wa words, pitch m*wa
+    if (wa)
+      SG_CUDA(cudaMemcpy2DAsync(dA, rows * wa * 8, A + r0 * wa, m * wa * 8, rows * wa * 8, R, cudaMemcpyHostToDevice,
+                                d->in),
+              "sg_m4rm_host H2D A");
+    SG_CUDA(cudaEventRecord(d->ev_in[i], d->in), "sg_m4rm_host event");
+    SG_CUDA(cudaStreamWaitEvent(d->comp, d->ev_in[i], 0), "sg_m4rm_host wait");
+    rc = sg_m4rm(field, dA, dB, dC, rows, l, n, k, nullptr, 0, d->comp);
+    if (rc != SG_OK) return rc;
+    SG_CUDA(cudaEventRecord(d->ev_comp[i], d->comp), "sg_m4rm_host event");
+    SG_CUDA(cudaStreamWaitEvent(d->out, d->ev_comp[i], 0), "sg_m4rm_host wait");
+    SG_CUDA(cudaMemcpy2DAsync(C + r0 * wc, m * wc * 8, dC, rows * wc * 8, rows * wc * 8, R, cudaMemcpyDeviceToHost,
+                              d->out),
+            "sg_m4rm_host D2H C");
+  }
+  SG_CUDA(cudaStreamSynchronize(d->out), "sg_m4rm_host sync");
+  SG_CUDA(cudaStreamSynchronize(d->comp), "sg_m4rm_host sync");
   return SG_OK;
 }
 

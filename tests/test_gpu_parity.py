@@ -197,6 +197,17 @@ def test_host_buffers_e2e_path():
         assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
 
 
+def test_host_buffers_pipelined_chunks():
+    """m >= 4096 runs sg_m4rm_host's row-chunked copy/compute pipeline (2..4 chunks)."""
+    for fname, m in (("f7", 5000), ("f3", 9001)):
+        A = oracle.random_dense(fname, m, 300, 5)
+        B = oracle.random_dense(fname, 300, 200, 6)
+        Ah = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, A), 300, device="cpu")
+        Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), 200, device="cpu")
+        C = sg.m4rm_multiply(Ah, Bh)
+        assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
+
+
 def test_elementwise_ops_match_dense():
     for fname in ("f2", "f3", "f5", "f7", "gf4"):
         f = FIELDS[fname]
