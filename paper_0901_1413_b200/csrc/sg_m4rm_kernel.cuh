@@ -1,0 +1,541 @@
+// sg_m4rm_kernel.cuh -- the bitsliced Method-of-Four-Russians kernel C = A*B on sm_100a
+// (instantiated per field in sg_m4rm_<field>.cu; launched by sg_m4rm.cu).
+//
+// Reference path (what this replaces): m4rm_multiply = for each k-block s,
+// build_table then _core.active().m4rm_block_<f> (_core_py.py:205-281),
+// whose per-row loop does  C_i += sum_d alpha_d * T[phi_d(a_i, block s)].
+//
+// B200 design:
+//  * One CTA owns a 128-column slab of C (4 x 32-bit words per plane) and ROWS = RT*256 rows,
+//    and walks the k-blocks of its split of the inner dimension.  C lives in registers for
+//    the whole walk: lane (t, tid) holds rows t*256+tid, one uint4 per plane.
+//  * Per k-block the CTA builds the 2^K-entry table of its slab in shared memory:
+//    phase 1: two half tables (rows 0..3 and 4..7 of the block, 16 entries each) from the B
+//    rows that cp.async staged two blocks ahead; phase 2: T[g] = Thi[g>>4] + Tlo[g&15],
+//    one bitsliced field add per word, written as 8 replicas (see COPIES).
+//  * Lookups: the 8 lanes of each LDS.128 phase hold 8 different rows, i.e. 8 random table
+//    entries.  Replica j of every entry sits at bank offset 4j and lane (tid&7) reads replica
+//    tid&7, so each phase touches all 32 banks exactly once: conflict-free for any indices.
+//  * Index bytes come from A^T (A's planes transposed to [plane][word][row] by a pre-pass, F3's
+//    plane 0 pre-XORed to A0^A1), staged per 32-bit word into shared memory by cp.async: one
+//    conflict-free LDS.32 per (row, block, plane).
+//  * Epilogue: canonical reduce (F5/F7) and store, or raw partial sums for split-K.
+#pragma once
+#include <cstdio>
+
+#include "sg_field.cuh"
+#include "sg_internal.h"
+
+namespace sg {
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int F> __device__ __forceinline__ V<F> vzero() {
+  V<F> v;
+#pragma unroll
+  for (int d = 0; d < Traits<F>::R; ++d) v.p[d] = 0u;
+  return v;
+}
+
+// Row accumulator of one lane: 4 words x RS planes.
+template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
+
+// Table rows of one (row, k-block): NI lookups x R planes, one uint4 (4 words) each.
+template <int F> struct Rows { uint4 v[Traits<F>::NI][Traits<F>::R]; };
+
+// Load the table rows at byte offsets e[] (entry * ENTRY_BYTES) from this lane's replica base.
+template <int F, int TPL>
+__device__ __forceinline__ void load_rows(Rows<F>& r, const unsigned char* __restrict__ tl, const u32 (&e)[3]) {
+#pragma unroll
+  for (int i = 0; i < Traits<F>::NI; ++i)
+#pragma unroll
+    for (int d = 0; d < Traits<F>::R; ++d)
+      r.v[i][d] = *reinterpret_cast<const uint4*>(tl + e[i] + d * TPL * 16);
+}
+
+__device__ __forceinline__ u32 comp(const uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
+
+// One (row, k-block) update of the 4 C words a lane owns from its loaded table rows.
+template <int F>
+__device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    u32* q = c.w[w];
+    if constexpr (F == F2) {
+      q[0] ^= comp(r.v[0][0], w);
+    } else if constexpr (F == F3) {
+      // basis {1, -1}: C += T[pos]; C -= T[neg]   (_core_py.py:213-222), 6 LOP3 per word
+      f3_add(q[0], q[1], comp(r.v[0][0], w), comp(r.v[0][1], w));
+      f3_sub(q[0], q[1], comp(r.v[1][0], w), comp(r.v[1][1], w));
+    } else if constexpr (F == GF4) {
+      // power basis {1, x}: C += T[g0] + x*T[g1],  x*(t0, t1) = (t1, t0 ^ t1)
+      const u32 q1 = comp(r.v[1][1], w);
+      q[0] ^= comp(r.v[0][0], w) ^ q1;
+      q[1] ^= comp(r.v[0][1], w) ^ comp(r.v[1][0], w) ^ q1;
+    } else {
+      // F5 / F7, basis {1, 2, 4}: C += T[g0] + 2*T[g1] + 4*T[g2] (the reference's Horner form,
+      // _core_py.py:241-255, reassociated); doubling is a plane rotation in both accumulators.
+      const u32 x0 = comp(r.v[0][0], w), x1 = comp(r.v[0][1], w), x2 = comp(r.v[0][2], w);
+      const u32 y0 = comp(r.v[1][0], w), y1 = comp(r.v[1][1], w), y2 = comp(r.v[1][2], w);
+      const u32 z0 = comp(r.v[2][0], w), z1 = comp(r.v[2][1], w), z2 = comp(r.v[2][2], w);
+      if constexpr (F == F7) {
+        f7_acc(q[0], q[1], q[2], q[3], x0, x1, x2, y0, y1, y2, z0, z1, z2);
+      } else {
+        f5_acc(q[0], q[1], q[2], q[3], q[4], x0, x1, x2, y0, y1, y2, z0, z1, z2);
+      }
+    }
+  }
+}
+
+// Accumulator -> output planes (canonical for the final C and for split-K partials of F5).
+// F7 accumulator (q0, k0, q1, q2): value = (q0,q1,q2) + k0 mod 7.  F5 (q0, q1, q2, k2, q3):
+// value = (q0,q1,q2,q3) + 4 k2 mod 15, then mod 5.
+template <int F> __device__ __forceinline__ void finish(const u32 (&q)[Traits<F>::RS], u32 (&o)[Traits<F>::R],
+                                                        bool canonical) {
+  if constexpr (F == F5) {
+    u32 v0 = q[0], v1 = q[1], v2 = q[2], v3 = q[4];
+    add15(v0, v1, v2, v3, 0u, 0u, q[3], 0u);
+    mod15_to_f5(v0, v1, v2, v3, o[0], o[1], o[2]);
+  } else if constexpr (F == F7) {
+    o[0] = q[0]; o[1] = q[2]; o[2] = q[3];
+    f7_add(o[0], o[1], o[2], q[1], 0u, 0u);
+    if (canonical) f7_reduce(o[0], o[1], o[2]);
+  } else {
+#pragma unroll
+    for (int d = 0; d < Traits<F>::R; ++d) o[d] = q[d];
+  }
+}
+
+// Named barriers (id 0 is __syncthreads) for the warp-specialized schedule.
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// SCHED 0: per k-block  phase1 | sync | phase2 | sync | lookups   (one table buffer)
+// SCHED 1: per k-block  lookups(s) + phase2(s+1) + phase1(s+2) | sync  (two table buffers)
+// SCHED 2: warp-specialized (k = 8): NT lookup threads + 4 builder warps that stage B and A
+//          with cp.async and builds block s+1's table into the other buffer while the lookup warps
+//          consume block s; FULL/EMPTY named barriers hand the two buffers back and forth.
+// ABL (experiments only, 0 in production): bit 0 skips the table-replica stores, bit 1 replaces
+// the field update by a plain XOR of the looked-up rows, bit 2 skips the lookups.
+constexpr int WS_BUILDERS = 128;  // builder threads (4 warps) of the warp-specialized schedule
+
+template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
+__global__ void __launch_bounds__(SCHED == 2 ? NT + WS_BUILDERS : NT, 1) m4rm_kernel(const M4rmArgs a) {
+  constexpr bool PIPE = SCHED == 1;
+  constexpr bool WS = SCHED == 2;
+  static_assert(!WS || K == 8, "the warp-specialized schedule is k = 8 only");
+  constexpr int R = Traits<F>::R;
+  constexpr int E = 1 << K;
+  constexpr int KLO = K < 4 ? K : 4;
+  constexpr int KHI = K - KLO;
+  constexpr int ROWS = RT * NT;
+  constexpr int TPLANE = E * ENTRY_BYTES;  // bytes per table plane
+  constexpr int TPL = TPLANE / 16;         // uint4 per table plane
+  constexpr int HALF = 16 * R * 4;         // u32 per half table
+  constexpr int NTAB = SCHED >= 1 ? 2 : 1;
+  constexpr int PD = PIPE ? 3 : 2;         // cp.async prefetch distance of B rows in k-blocks
+  constexpr int PDA = 2;                   // ... and of A's index words
+  // k = 8: A's index bytes arrive pre-packed as one record of NIP bytes per k-block (the
+  // index_words pre-pass), RPW records per 32-bit word, NSLOT staging slots of ROWS words.
+  // k < 8: A^T bit planes, R planes x 2 slots.
+  constexpr bool IW = (K == 8);
+  constexpr int NI = Traits<F>::NI;
+  constexpr int NIP = NI == 3 ? 4 : NI;
+  constexpr int RPW = 4 / NIP;
+  constexpr int NSLOT = IW ? 3 : 2;       // A words in use + two blocks in flight
+  constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
+  constexpr int TPE_RAW = NT / E;
+  constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
+  constexpr int CPT = COPIES / TPE;        // replicas written per thread
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][R][E][COPIES] uint4
+  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][16][R][4]
+  u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
+  u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
+
+  const int tid = threadIdx.x;
+  const int word0 = blockIdx.x * SLAB_WORDS;
+  const int64_t row0 = (int64_t)blockIdx.y * ROWS;
+  const int s_begin = blockIdx.z * a.bps;
+  const int s_end = min(a.nblocks, s_begin + a.bps);
+  if (s_begin >= s_end) return;
+
+  int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
+  // Stage block s's B rows (K x R x 16 B) into bst[s % 3].
+  auto issue_b = [&](int s, int t0 = -1, int nthr = NT) {
+    if (t0 < 0) t0 = tid;
+    if (s < s_end) {
+      u32* bdst = bst + (s % 3) * K * R * 4;
+      for (int q = t0; q < K * R * 2; q += nthr) {
+        const int i = q / (R * 2), d = (q >> 1) % R, half = q & 1;
+        const int64_t row = (int64_t)s * K + i;
+        const int w = word0 + 2 * half;
+        const bool ok = row < a.l && w < a.wc32;
+        const u32* src = ok ? a.B + ((int64_t)d * a.l + row) * a.wc32 + w : a.B;
+        cp_async8(bdst + (i * R + d) * 4 + 2 * half, src, ok ? 8 : 0);
+      }
+    }
+  };
+  // Stage the index words block s needs that are not yet staged.
+  auto issue_a = [&](int s, int t0 = -1, int nthr = NT) {
+    if (t0 < 0) t0 = tid;
+    if (s < s_end) {
+      const int whi = IW ? s / RPW : (s * K + K - 1) >> 5;
+      for (; next_word <= whi; ++next_word) {
+        u32* adst = ast + (next_word % NSLOT) * NAP * ROWS;
+        const bool ok = next_word < a.wa32;
+        for (int q = t0; q < NAP * ROWS / 4; q += nthr) {
+          const int d = q / (ROWS / 4), r4 = q % (ROWS / 4);
+          const u32* src = ok ? a.AT + ((int64_t)d * a.wa32 + next_word) * a.mpad + row0 + 4 * r4 : a.AT;
+          cp_async16(adst + d * ROWS + 4 * r4, src, ok ? 16 : 0);
+        }
+      }
+    }
+  };
+
+  // phase 1: the two 16-entry half tables of block s (rows 0..KLO-1 and KLO..K-1)
+  auto phase1 = [&](int s) {
+    const u32* bs = bst + (s % 3) * K * R * 4;
+    u32* th = thalf + (s & 1) * 2 * HALF;
+    if (tid < 128) {
+      const int h = tid >> 6, e = (tid >> 2) & 15, w = tid & 3;
+      const int nrows = h ? KHI : KLO;
+      if (e < (1 << nrows)) {
+        V<F> acc = vzero<F>();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < nrows && ((e >> i) & 1)) {
+            V<F> b;
+#pragma unroll
+            for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
+            vadd<F>(acc, b);
+          }
+        }
+#pragma unroll
+        for (int d = 0; d < R; ++d) th[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
+      }
+    }
+  };
+
+  // phase 2a: this thread's table entry g = Thi[g >> KLO] + Tlo[g & (2^KLO - 1)] (4 words x R)
+  const int g_own = tid / TPE, part = tid % TPE;
+  auto phase2_compute = [&](int s, V<F> (&v)[4]) {
+    const u32* th = thalf + (s & 1) * 2 * HALF;
+    if (g_own < E) {
+      const uint4* lo = reinterpret_cast<const uint4*>(th + (g_own & ((1 << KLO) - 1)) * R * 4);
+      const uint4* hi = reinterpret_cast<const uint4*>(th + HALF + (g_own >> KLO) * R * 4);
+      V<F> hv[4];
+#pragma unroll
+      for (int d = 0; d < R; ++d) {
+        const uint4 L = lo[d], H = hi[d];
+        v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
+        hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
+      }
+      if constexpr (KHI > 0) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) vadd<F>(v[w], hv[w]);
+      }
+    }
+  };
+  // phase 2b: write replica number cc (of this thread's CPT) of entry g_own into table buffer tb.
+  // The replica order is rotated by g so the 8 lanes of a store phase hit 8 different banks.
+  auto phase2_store = [&](uint4* tb, const V<F> (&v)[4], int cc) {
+    if (!(ABL & 1) && g_own < E) {
+      const int copy = (part * CPT + cc + g_own) & (COPIES - 1);
+#pragma unroll
+      for (int d = 0; d < R; ++d)
+        tb[d * TPL + g_own * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
+    }
+  };
+
+  Acc<F> c[RT];
+  // F5: every k-block adds x + 2y + 4z + 2 (mod 5) (see f5_acc); start from -2 * blocks mod 5.
+  u32 init[5] = {0u, 0u, 0u, 0u, 0u};
+  if constexpr (F == F5) {
+    const int v = (5 - (2 * (s_end - s_begin)) % 5) % 5;
+    init[0] = (v & 1) ? ~0u : 0u;
+    init[1] = (v & 2) ? ~0u : 0u;
+    init[2] = (v & 4) ? ~0u : 0u;
+  }
+#pragma unroll
+  for (int t = 0; t < RT; ++t)
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int d = 0; d < Traits<F>::RS; ++d) c[t].w[w][d] = init[d];
+
+  const unsigned char* tl0 = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
+
+  // Byte offsets of row-slot t's table entries for block s.
+  auto entries = [&](int s, int t, u32 (&e)[3]) {
+    const int lr = t * NT + tid;
+    e[0] = e[1] = e[2] = 0u;
+    if constexpr (IW) {
+      const u32 x = ast[((s / RPW) % NSLOT) * ROWS + lr];
+      const int b0 = (s % RPW) * NIP;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) e[i] = __byte_perm(x, 0u, 0x4440u | (u32)(b0 + i)) * ENTRY_BYTES;
+    } else {
+      const int col0 = s * K;
+      const int w0 = col0 >> 5, sh = col0 & 31;
+      const u32* aw0 = ast + (w0 & 1) * R * ROWS;
+      const u32* aw1 = ast + ((w0 + 1) & 1) * R * ROWS;
+#pragma unroll
+      for (int d = 0; d < R; ++d) {
+        u32 x = aw0[d * ROWS + lr];
+        if constexpr (32 % K == 0) {
+          x = (x >> sh) & (E - 1);
+        } else {
+          x = ((sh + K > 32) ? __funnelshift_r(x, aw1[d * ROWS + lr], sh) : (x >> sh)) & (E - 1);
+        }
+        e[d] = x * ENTRY_BYTES;
+      }
+    }
+  };
+
+  // lookups for block s from table buffer tb, software-pipelined LA row-slots ahead (entries
+  // and table rows of t+1..t+LA in flight while t accumulates); `between(t)` runs after t.
+  constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4) ? 2 : 1;
+  auto lookups = [&](int s, int tb, auto&& between) {
+    if constexpr (ABL & 4) {
+#pragma unroll
+      for (int t = 0; t < RT; ++t) between(t);
+      return;
+    }
+    const unsigned char* tl = tl0 + tb * R * TPLANE;
+    Rows<F> ring[LA + 1];
+#pragma unroll
+    for (int t = 0; t < LA && t < RT; ++t) {
+      u32 e[3];
+      entries(s, t, e);
+      load_rows<F, TPL>(ring[t], tl, e);
+    }
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      if (t + LA < RT) {
+        u32 e[3];
+        entries(s, t + LA, e);
+        load_rows<F, TPL>(ring[(t + LA) % (LA + 1)], tl, e);
+      }
+      if constexpr (ABL & 2) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+#pragma unroll
+          for (int d = 0; d < Traits<F>::R; ++d) c[t].w[w][d] ^= comp(ring[t % (LA + 1)].v[0][d], w) ^ comp(ring[t % (LA + 1)].v[Traits<F>::NI - 1][d], w);
+      } else {
+        accumulate<F>(c[t], ring[t % (LA + 1)]);
+      }
+      between(t);
+    }
+  };
+
+  if constexpr (WS) {
+    constexpr int NB = NT + WS_BUILDERS;  // all threads take part in every FULL / EMPTY barrier
+    constexpr int NBT = WS_BUILDERS;
+    auto FULL = [](int s) { return 1 + (s & 1); };
+    auto EMPTY = [](int s) { return 3 + (s & 1); };
+    if (tid >= NT) {
+      // ------------------------------------------------ builder warps
+      const int bt = tid - NT;
+      auto bsync = [] { nbar_sync(5, NBT); };
+      issue_b(s_begin, bt, NBT);
+      issue_a(s_begin, bt, NBT);
+      cp_async_commit();
+      issue_b(s_begin + 1, bt, NBT);
+      cp_async_commit();
+      for (int s = s_begin; s < s_end; ++s) {
+        if (s >= s_begin + 2) nbar_sync(EMPTY(s), NB);  // lookups of block s-2 left tab[s & 1]
+        issue_b(s + 2, bt, NBT);
+        issue_a(s + 1, bt, NBT);
+        cp_async_commit();
+        cp_async_wait<1>();  // B rows of s and A words of s have landed (this thread's copies)
+        bsync();
+        // phase 1: 2 halves x 16 entries x 4 words = 128 items
+        {
+          const u32* bs = bst + (s % 3) * K * R * 4;
+          for (int item = bt; item < 128; item += NBT) {
+            const int h = item >> 6, e = (item >> 2) & 15, w = item & 3;
+            const int nrows = h ? KHI : KLO;
+            if (e < (1 << nrows)) {
+              V<F> acc = vzero<F>();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (i < nrows && ((e >> i) & 1)) {
+                  V<F> b;
+#pragma unroll
+                  for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
+                  vadd<F>(acc, b);
+                }
+              }
+#pragma unroll
+              for (int d = 0; d < R; ++d) thalf[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
+            }
+          }
+        }
+        bsync();
+        // phase 2: 256 entries x 8 replicas
+        uint4* tb = tab + (s & 1) * R * TPL;
+#pragma unroll
+        for (int it = 0; it < E / NBT; ++it) {
+          const int g = bt + NBT * it;
+          const uint4* lo = reinterpret_cast<const uint4*>(thalf + (g & ((1 << KLO) - 1)) * R * 4);
+          const uint4* hi = reinterpret_cast<const uint4*>(thalf + HALF + (g >> KLO) * R * 4);
+          V<F> v[4], hv[4];
+#pragma unroll
+          for (int d = 0; d < R; ++d) {
+            const uint4 L = lo[d], H = hi[d];
+            v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
+            hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
+          }
+#pragma unroll
+          for (int w = 0; w < 4; ++w) vadd<F>(v[w], hv[w]);
+          if constexpr (!(ABL & 1)) {
+#pragma unroll
+            for (int cc = 0; cc < COPIES; ++cc) {
+              const int copy = (cc + g) & (COPIES - 1);
+#pragma unroll
+              for (int d = 0; d < R; ++d)
+                tb[d * TPL + g * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
+            }
+          }
+        }
+        nbar_arrive(FULL(s), NB);  // table of block s (and A words of s) ready
+      }
+      cp_async_wait<0>();
+      return;
+    }
+    // ------------------------------------------------ lookup warps
+    for (int s = s_begin; s < s_end; ++s) {
+      nbar_sync(FULL(s), NB);
+      lookups(s, s & 1, [](int) {});
+      if (s + 2 < s_end) nbar_arrive(EMPTY(s), NB);
+    }
+  } else if constexpr (!PIPE) {
+    for (int i = 0; i < PD; ++i) {
+      issue_b(s_begin + i);
+      issue_a(s_begin + i);
+      cp_async_commit();
+    }
+    cp_async_wait<PD - 1>();
+    __syncthreads();
+    for (int s = s_begin; s < s_end; ++s) {
+      phase1(s);
+      __syncthreads();
+      issue_b(s + PD);
+      issue_a(s + PDA);
+      cp_async_commit();
+      {
+        V<F> v[4];
+        phase2_compute(s, v);
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) phase2_store(tab, v, cc);
+      }
+      cp_async_wait<PD - 1>();
+      __syncthreads();
+      lookups(s, 0, [](int) {});
+    }
+  } else {
+    for (int i = 0; i < PD; ++i) issue_b(s_begin + i);
+    for (int i = 0; i < PDA; ++i) issue_a(s_begin + i);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    phase1(s_begin);
+    __syncthreads();
+    {
+      V<F> v[4];
+      phase2_compute(s_begin, v);
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) phase2_store(tab + (s_begin & 1) * R * TPL, v, cc);
+    }
+    if (s_begin + 1 < s_end) phase1(s_begin + 1);
+    __syncthreads();
+    for (int s = s_begin; s < s_end; ++s) {
+      issue_b(s + PD);
+      issue_a(s + PDA);
+      cp_async_commit();
+      const bool nxt = s + 1 < s_end;
+      V<F> v[4];
+      if (nxt) phase2_compute(s + 1, v);
+      uint4* tnext = tab + ((s + 1) & 1) * R * TPL;
+      // spread the next table's replica stores over the row-slot loop
+      lookups(s, s & 1, [&](int t) {
+        if (nxt) {
+          if constexpr (RT >= CPT) {
+            if (t % (RT / CPT) == 0) phase2_store(tnext, v, t / (RT / CPT));
+          } else {
+#pragma unroll
+            for (int q = 0; q < CPT / RT; ++q) phase2_store(tnext, v, t * (CPT / RT) + q);
+          }
+        }
+      });
+      if (s + 2 < s_end) phase1(s + 2);
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+  }
+
+  // ---- epilogue
+  u32* out = a.C;
+  int64_t rows_out = a.m;
+  if (a.partial) {
+    out += (int64_t)blockIdx.z * R * a.mpad * a.wc32;
+    rows_out = a.mpad;
+  }
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    const int64_t row = row0 + t * NT + tid;
+    if (row < a.m) {
+      u32 o[4][R];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], !a.partial);
+#pragma unroll
+      for (int d = 0; d < R; ++d) {
+        u32* dst = out + ((int64_t)d * rows_out + row) * a.wc32 + word0;
+        if (word0 < a.wc32) *reinterpret_cast<uint2*>(dst) = make_uint2(o[0][d], o[1][d]);
+        if (word0 + 2 < a.wc32) *reinterpret_cast<uint2*>(dst + 2) = make_uint2(o[2][d], o[3][d]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ registry helpers
+template <int F, int K, int RT, int SCHED, int NT>
+constexpr int smem_bytes_for() {
+  constexpr int R = Traits<F>::R;
+  constexpr int NSLOT = K == 8 ? 3 : 2;
+  constexpr int NAP = K == 8 ? 1 : R;
+  return (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
+         NSLOT * NAP * RT * NT * 4;
+}
+
+#define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (P) == 2 ? (NT) + WS_BUILDERS : (NT), P, \
+                               smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0}
+#define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (P) == 2 ? (NT) + WS_BUILDERS : (NT), P, \
+                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A}
+// k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
+#define SG_KSET8(F)                                                                                 \
+  SG_K(F, 8, 1, 0, 256), SG_K(F, 8, 2, 0, 256), SG_K(F, 8, 4, 0, 256), SG_K(F, 8, 8, 0, 256), \
+  SG_K(F, 8, 1, 1, 256), SG_K(F, 8, 2, 1, 256), SG_K(F, 8, 4, 1, 256),                      \
+  SG_K(F, 8, 2, 0, 512), SG_K(F, 8, 4, 0, 512), SG_K(F, 8, 2, 1, 512)
+#define SG_KSET8_2PLANE(F)                                                                          \
+  SG_K(F, 8, 16, 0, 256), SG_K(F, 8, 8, 1, 256), SG_K(F, 8, 16, 1, 256),                  \
+  SG_K(F, 8, 8, 0, 512), SG_K(F, 8, 4, 1, 512), SG_K(F, 8, 8, 1, 512)
+// k < 8: parity and generality (k-invariance), one variant each + a pipelined k=5
+#define SG_KLOW(F)                                                                                  \
+  SG_K(F, 1, 1, 0, 256), SG_K(F, 2, 1, 0, 256), SG_K(F, 3, 1, 0, 256), SG_K(F, 4, 1, 0, 256), \
+  SG_K(F, 5, 1, 0, 256), SG_K(F, 6, 1, 0, 256), SG_K(F, 7, 1, 0, 256), SG_K(F, 5, 1, 1, 256)
+
+}  // namespace sg
