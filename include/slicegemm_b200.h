@@ -22,7 +22,8 @@
  * Data layout (identical bits to the reference's BitslicedMatrix planes):
  *   a matrix of `rows` x `n` over a field with R planes is R contiguous planes, each `rows` x
  *   W64 uint64 words, W64 = ceil(n / 64); column c lives in word c >> 6, bit c & 63 (little
- *   endian).  Padding lanes (columns >= n) must be zero.  R = 1 (F2), 2 (F3, GF4), 3 (F5, F7).
+ *   endian).  Padding lanes (columns >= n) must be zero.  R = 1 (F2), 2 (F3, GF4, Z4),
+ *   3 (F5, F7, GF8, Z8).
  *   F3: plane 0 = unit, plane 1 = sign (0 = 00, 1 = 01, -1 = 11, fields.py:88-101).
  *   F5 / F7: 3-bit binary value, residue = value mod p (redundant, fields.py:103-129).
  *   GF4 = F2[x]/(x^2+x+1): plane 0 = coefficient of 1, plane 1 = coefficient of x (fields.py:215).
@@ -47,8 +48,9 @@ extern "C" {
 
 #define SG_ABI_VERSION 1
 
-/* fields */
-enum { SG_F2 = 0, SG_F3 = 1, SG_F5 = 2, SG_F7 = 3, SG_GF4 = 4 };
+/* fields (GF4/GF8 = F2[x]/(x^2+x+1), F2[x]/(x^3+x+1) in power-basis planes, fields.py:215-216;
+ * Z4/Z8 = the reference's binary rings, fields.py:131-158) */
+enum { SG_F2 = 0, SG_F3 = 1, SG_F5 = 2, SG_F7 = 3, SG_GF4 = 4, SG_GF8 = 5, SG_Z4 = 6, SG_Z8 = 7 };
 
 /* status codes */
 enum {
@@ -83,7 +85,18 @@ enum {
   SG_OP_SCALAR_MUL_F3 = 17, /* BitslicedMatrix.scalar_mul, scalar = residue */
   SG_OP_SCALAR_MUL_F5 = 18,
   SG_OP_SCALAR_MUL_F7 = 19,
-  SG_OP_SCALAR_MUL_GF4 = 20
+  SG_OP_SCALAR_MUL_GF4 = 20,
+  SG_OP_Z4_ADD = 21,      /* _core_py.py:46 z4_add(d0, d1, s0, s1)          */
+  SG_OP_Z4_SUB = 22,      /* _core_py.py:53 z4_sub                           */
+  SG_OP_Z4_NEG = 23,      /* _core_py.py:61 z4_neg                           */
+  SG_OP_Z8_ADD = 24,      /* _core_py.py:100 z8_add                          */
+  SG_OP_Z8_SUB = 25,      /* _core_py.py:110 z8_sub                          */
+  SG_OP_Z8_NEG = 26,      /* _core_py.py:104 z8_neg                          */
+  SG_OP_GF8_ADD = 27,     /* coefficientwise F2 add                          */
+  SG_OP_GF8_MULX = 28,    /* multiply by x mod x^3+x+1                       */
+  SG_OP_SCALAR_MUL_Z4 = 29,
+  SG_OP_SCALAR_MUL_Z8 = 30,
+  SG_OP_SCALAR_MUL_GF8 = 31
 };
 
 int sg_abi_version(void);

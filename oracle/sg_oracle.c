@@ -19,6 +19,10 @@
  *                    row partition gives bit-identical output)
  *   GF(4) direct     power basis {1, x}: acc = x*T[g1] + T[g0], x*(c0,c1) = (c1, c0^c1)
  *                    (SURVEY.md 8a a8); decode-equal to oracle.py:192-215
+ *   GF(8) direct     power basis {1, x, x^2} mod x^3+x+1 (fields.py:216), Horner with x*c =
+ *                    (c2, c0^c2, c1); decode-equal to oracle_ext_multiply(F8)
+ *   Z/4, Z/8         _core_py.py:46-62, 100-113 (ring kernels), :225-238, 262-266, 284-286
+ *                    (block drivers: Horner over {1, 2[, 4]}, doubling = plane shift)
  * Parity pins: tests/golden/m4rm_<field>.npz, gf4.npz and kernel_cases.json, generated from the reference
  * itself by tests/golden/make_golden.py ("Oracle").
  */
@@ -34,8 +38,8 @@ typedef uint64_t w64;
 int sgo_planes(int field) {
   switch (field) {
     case SGO_F2: return 1;
-    case SGO_F3: case SGO_GF4: return 2;
-    case SGO_F5: case SGO_F7: return 3;
+    case SGO_F3: case SGO_GF4: case SGO_Z4: return 2;
+    case SGO_F5: case SGO_F7: case SGO_GF8: case SGO_Z8: return 3;
     default: return -1;
   }
 }
@@ -46,7 +50,8 @@ int sgo_order(int field) {
     case SGO_F3: return 3;
     case SGO_F5: return 5;
     case SGO_F7: return 7;
-    case SGO_GF4: return 4;
+    case SGO_GF4: case SGO_Z4: return 4;
+    case SGO_GF8: case SGO_Z8: return 8;
     default: return -1;
   }
 }
@@ -184,6 +189,31 @@ static inline void f7_reduce(w64* p) {
   p[0] ^= t; p[1] ^= t; p[2] ^= t;
 }
 
+static inline void z4_add(w64* x, const w64* y) {
+  w64 c = x[0] & y[0];
+  x[0] ^= y[0];
+  x[1] ^= y[1] ^ c;
+}
+static inline void z4_sub(w64* x, const w64* y) {
+  w64 n[2] = {y[0], y[0] ^ y[1]};
+  z4_add(x, n);
+}
+static inline void z8_add(w64* x, const w64* y) {
+  w64 s[4];
+  add3(x, y, s);
+  x[0] = s[0]; x[1] = s[1]; x[2] = s[2];
+}
+static inline void z8_sub(w64* x, const w64* y) {
+  w64 n[3] = {y[0], y[0] ^ y[1], (y[0] | y[1]) ^ y[2]};
+  z8_add(x, n);
+}
+static inline void gf8_mulx(w64* c) {
+  w64 t = c[2];
+  c[2] = c[1];
+  c[1] = c[0] ^ t;
+  c[0] = t;
+}
+
 void sgo_canonicalize(int field, w64* planes, int64_t rows, int64_t W) {
   int64_t N = rows * W;
   if (field != SGO_F5 && field != SGO_F7) return;
@@ -250,9 +280,11 @@ static void table_add(int field, w64* T, int64_t stride, int64_t dst, int64_t sr
       y[d] = B[(d * l + src_row_idx) * W + w];
     }
     switch (field) {
-      case SGO_F2: case SGO_GF4:
+      case SGO_F2: case SGO_GF4: case SGO_GF8:
         for (int d = 0; d < r; ++d) x[d] ^= y[d];
         break;
+      case SGO_Z4: if (sub) z4_sub(x, y); else z4_add(x, y); break;
+      case SGO_Z8: if (sub) z8_sub(x, y); else z8_add(x, y); break;
       case SGO_F3: if (sub) f3_sub(x, y); else f3_add(x, y); break;
       case SGO_F5: if (sub) f5_sub(x, y); else f5_add(x, y); break;
       case SGO_F7: if (sub) f7_sub(x, y, w == W - 1 ? tail : ~(w64)0); else f7_add(x, y); break;
@@ -310,6 +342,28 @@ static void* run_job(void* arg) {
             c[1] ^= p1 ^ q0 ^ q1;
             break;
           }
+          case SGO_GF8: /* Horner: acc = x*(x*T[g2] + T[g1]) + T[g0] */
+            for (int d = 0; d < 3; ++d) acc[d] = TE(d, gi[2]);
+            gf8_mulx(acc);
+            for (int d = 0; d < 3; ++d) acc[d] ^= TE(d, gi[1]);
+            gf8_mulx(acc);
+            for (int d = 0; d < 3; ++d) c[d] ^= acc[d] ^ TE(d, gi[0]);
+            break;
+          case SGO_Z4: /* acc = 2 T[g1] + T[g0] */
+            acc[0] = 0; acc[1] = TE(0, gi[1]);
+            t0[0] = TE(0, gi[0]); t0[1] = TE(1, gi[0]);
+            z4_add(acc, t0);
+            z4_add(c, acc);
+            break;
+          case SGO_Z8: /* Horner over {1, 2, 4}, doubling = plane shift */
+            acc[0] = 0; acc[1] = TE(0, gi[2]); acc[2] = TE(1, gi[2]);
+            for (int d = 0; d < 3; ++d) t0[d] = TE(d, gi[1]);
+            z8_add(acc, t0);
+            acc[2] = acc[1]; acc[1] = acc[0]; acc[0] = 0;
+            for (int d = 0; d < 3; ++d) t0[d] = TE(d, gi[0]);
+            z8_add(acc, t0);
+            z8_add(c, acc);
+            break;
           default: /* F5, F7: Horner over {1, 2, 4} */
             for (int d = 0; d < 3; ++d) acc[d] = TE(d, gi[2]);
             if (field == SGO_F5) f5_double(acc); else f7_double(acc);

@@ -5,7 +5,7 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
-enum { SGO_F2 = 0, SGO_F3 = 1, SGO_F5 = 2, SGO_F7 = 3, SGO_GF4 = 4 };
+enum { SGO_F2 = 0, SGO_F3 = 1, SGO_F5 = 2, SGO_F7 = 3, SGO_GF4 = 4, SGO_GF8 = 5, SGO_Z4 = 6, SGO_Z8 = 7 };
 int sgo_planes(int field);
 int sgo_order(int field);
 int sgo_pack(int field, const uint8_t* dense, int64_t m, int64_t n, uint64_t* planes);

@@ -77,6 +77,12 @@ def f7_add(d0, d1, d2, s0, s1, s2): _op("f7_add", [d0, d1, d2], [s0, s1, s2])
 def f7_sub(d0, d1, d2, s0, s1, s2, tail): _op("f7_sub", [d0, d1, d2], [s0, s1, s2], tail=tail)
 def f7_neg(p0, p1, p2, tail): _op("f7_neg", [p0, p1, p2], tail=tail)
 def f7_reduce(p0, p1, p2): _op("f7_reduce", [p0, p1, p2])
+def z4_add(d0, d1, s0, s1): _op("z4_add", [d0, d1], [s0, s1])
+def z4_sub(d0, d1, s0, s1): _op("z4_sub", [d0, d1], [s0, s1])
+def z4_neg(p0, p1): _op("z4_neg", [p0, p1])
+def z8_add(d0, d1, d2, s0, s1, s2): _op("z8_add", [d0, d1, d2], [s0, s1, s2])
+def z8_sub(d0, d1, d2, s0, s1, s2): _op("z8_sub", [d0, d1, d2], [s0, s1, s2])
+def z8_neg(p0, p1, p2): _op("z8_neg", [p0, p1, p2])
 
 
 def _block(field_code, C, A, col0, kp, T, row0, row1):
@@ -111,3 +117,15 @@ def m4rm_block_f7(C0, C1, C2, A0, A1, A2, col0, kp, T0, T1, T2, row0, row1):
 
 def m4rm_block_gf4(C0, C1, A0, A1, col0, kp, T0, T1, row0, row1):
     _block(_lib.SG_GF4, [C0, C1], [A0, A1], col0, kp, [T0, T1], row0, row1)
+
+
+def m4rm_block_gf8(C0, C1, C2, A0, A1, A2, col0, kp, T0, T1, T2, row0, row1):
+    _block(_lib.SG_GF8, [C0, C1, C2], [A0, A1, A2], col0, kp, [T0, T1, T2], row0, row1)
+
+
+def m4rm_block_z4(C0, C1, A0, A1, col0, kp, T0, T1, row0, row1):
+    _block(_lib.SG_Z4, [C0, C1], [A0, A1], col0, kp, [T0, T1], row0, row1)
+
+
+def m4rm_block_z8(C0, C1, C2, A0, A1, A2, col0, kp, T0, T1, T2, row0, row1):
+    _block(_lib.SG_Z8, [C0, C1, C2], [A0, A1, A2], col0, kp, [T0, T1, T2], row0, row1)

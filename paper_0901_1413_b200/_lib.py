@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libslicegemm_b200.so")
 
 # field codes (include/slicegemm_b200.h)
-SG_F2, SG_F3, SG_F5, SG_F7, SG_GF4 = 0, 1, 2, 3, 4
+SG_F2, SG_F3, SG_F5, SG_F7, SG_GF4, SG_GF8, SG_Z4, SG_Z8 = 0, 1, 2, 3, 4, 5, 6, 7
 
 # status codes
 SG_OK, SG_EINVAL, SG_ECUDA, SG_EUNSUPPORTED, SG_ERANGE, SG_EPATTERN, SG_ENOMEM = range(7)
@@ -23,7 +23,9 @@ OPS = {
     "f2_add": 0, "f3_add": 1, "f3_sub": 2, "f3_neg": 3, "f5_add": 4, "f5_sub": 5, "f5_neg": 6,
     "f5_double": 7, "f5_reduce": 8, "f7_add": 9, "f7_sub": 10, "f7_neg": 11, "f7_double": 12,
     "f7_reduce": 13, "gf4_add": 14, "gf4_mulx": 15, "f5_fold5": 16, "scalar_mul_f3": 17,
-    "scalar_mul_f5": 18, "scalar_mul_f7": 19, "scalar_mul_gf4": 20,
+    "scalar_mul_f5": 18, "scalar_mul_f7": 19, "scalar_mul_gf4": 20, "z4_add": 21, "z4_sub": 22, "z4_neg": 23,
+    "z8_add": 24, "z8_sub": 25, "z8_neg": 26, "gf8_add": 27, "gf8_mulx": 28, "scalar_mul_z4": 29,
+    "scalar_mul_z8": 30, "scalar_mul_gf8": 31,
 }
 
 # every symbol include/slicegemm_b200.h declares

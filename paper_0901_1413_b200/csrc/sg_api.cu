@@ -38,8 +38,8 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, where); \
   } while (0)
 
-bool valid_field(int f) { return f >= SG_F2 && f <= SG_GF4; }
-int planes(int f) { return f == SG_F2 ? 1 : (f == SG_F5 || f == SG_F7) ? 3 : 2; }
+bool valid_field(int f) { return f >= SG_F2 && f <= SG_Z8; }
+int planes(int f) { return f == SG_F2 ? 1 : (f == SG_F5 || f == SG_F7 || f == SG_GF8 || f == SG_Z8) ? 3 : 2; }
 int64_t w64_of(int64_t n) { return (n + 63) / 64; }
 
 // ---------------------------------------------------------------- per-device state
@@ -200,8 +200,11 @@ void field_costs(int f, double* lane_alu, double* lane_smem, double* entry_alu) 
     case SG_F2: *lane_alu = 4 + 3; *lane_smem = 16 + 4; *entry_alu = 4 + 8; break;
     case SG_F3: *lane_alu = 36 + 6; *lane_smem = 64 + 8; *entry_alu = 20 + 16; break;
     case SG_GF4: *lane_alu = 12 + 6; *lane_smem = 64 + 8; *entry_alu = 8 + 16; break;
-    case SG_F5: *lane_alu = 168 + 9; *lane_smem = 144 + 12; *entry_alu = 48 + 24; break;
-    default: *lane_alu = 128 + 9; *lane_smem = 144 + 12; *entry_alu = 40 + 24; break;
+    case SG_F5: *lane_alu = 80 + 9; *lane_smem = 144 + 12; *entry_alu = 48 + 24; break;
+    case SG_GF8: *lane_alu = 28 + 9; *lane_smem = 144 + 12; *entry_alu = 12 + 24; break;
+    case SG_Z4: *lane_alu = 12 + 6; *lane_smem = 64 + 8; *entry_alu = 12 + 16; break;
+    case SG_Z8: *lane_alu = 36 + 9; *lane_smem = 144 + 12; *entry_alu = 28 + 24; break;
+    default: *lane_alu = 72 + 9; *lane_smem = 144 + 12; *entry_alu = 40 + 24; break;
   }
 }
 
@@ -269,7 +272,7 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
   best.wa32 = (int)wa32;
   best.wc32 = (int)wc32;
   if (K == 8) {
-    const int rpw = field == SG_F2 ? 4 : (field == SG_F5 || field == SG_F7) ? 1 : 2;
+    const int rpw = field == SG_F2 ? 4 : planes(field) == 3 ? 1 : 2;
     best.at_words = (nblocks + rpw - 1) / rpw;
     best.at_planes = 1;
   } else {
@@ -396,7 +399,8 @@ static int op_plane_count(int op) {
   switch (op) {
     case SG_OP_F2_ADD: return 1;
     case SG_OP_F3_ADD: case SG_OP_F3_SUB: case SG_OP_F3_NEG: case SG_OP_GF4_ADD: case SG_OP_GF4_MULX:
-    case SG_OP_SCALAR_MUL_F3: case SG_OP_SCALAR_MUL_GF4: return 2;
+    case SG_OP_SCALAR_MUL_F3: case SG_OP_SCALAR_MUL_GF4: case SG_OP_Z4_ADD: case SG_OP_Z4_SUB:
+    case SG_OP_Z4_NEG: case SG_OP_SCALAR_MUL_Z4: return 2;
     default: return 3;
   }
 }
@@ -413,12 +417,14 @@ static bool fill_planes(Planes* out, const uint64_t* const* arr, int R) {
 
 int sg_plane_op(int op, uint64_t* const* dst, const uint64_t* const* src, int64_t rows, int64_t words,
                 uint64_t tail, int scalar, void* stream) {
-  if (op < SG_OP_F2_ADD || op > SG_OP_SCALAR_MUL_GF4) return fail(SG_EINVAL, "unknown plane op");
+  if (op < SG_OP_F2_ADD || op > SG_OP_SCALAR_MUL_GF8) return fail(SG_EINVAL, "unknown plane op");
   if (rows < 0 || words < 0) return fail(SG_EINVAL, "negative dimension");
   if (rows == 0 || words == 0) return SG_OK;
   const bool unary = op == SG_OP_F3_NEG || op == SG_OP_F5_NEG || op == SG_OP_F5_DOUBLE ||
                      op == SG_OP_F5_REDUCE || op == SG_OP_F7_NEG || op == SG_OP_F7_DOUBLE ||
-                     op == SG_OP_F7_REDUCE || op == SG_OP_GF4_MULX || op >= SG_OP_SCALAR_MUL_F3;
+                     op == SG_OP_F7_REDUCE || op == SG_OP_GF4_MULX ||
+                     (op >= SG_OP_SCALAR_MUL_F3 && op <= SG_OP_SCALAR_MUL_GF4) || op == SG_OP_Z4_NEG ||
+                     op == SG_OP_Z8_NEG || op == SG_OP_GF8_MULX || op >= SG_OP_SCALAR_MUL_Z4;
   const int R = op_plane_count(op);
   Planes d, s;
   if (!fill_planes(&d, (const uint64_t* const*)dst, R)) return fail(SG_EINVAL, "null dst plane");

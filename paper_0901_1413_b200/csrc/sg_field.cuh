@@ -7,6 +7,8 @@
 //   F7  (3-bit value, residue = value mod 7; 7 == 0)         _core_py.py:65-75, 84-88, 151-175
 //   F2  (1 plane, xor)                                        _core_py.py:24-25
 //   GF4 (F2[x]/(x^2+x+1), plane0 = coeff of 1, plane1 = coeff of x)   fields.py:215
+//   GF8 (F2[x]/(x^3+x+1), planes = coefficients of 1, x, x^2)           fields.py:216
+//   Z4 / Z8 (2 / 3-bit binary, unique)                _core_py.py:46-62, 100-113, kernels.py:121-136, 399-415
 // Exhaustive lane tables for each formula (kernels.py:466-509, 550-590) are replayed on the
 // device through sg_plane_op by tests/test_gpu_parity.py.
 #pragma once
@@ -14,7 +16,7 @@
 
 namespace sg {
 
-enum Field : int { F2 = 0, F3 = 1, F5 = 2, F7 = 3, GF4 = 4 };
+enum Field : int { F2 = 0, F3 = 1, F5 = 2, F7 = 3, GF4 = 4, GF8 = 5, Z4 = 6, Z8 = 7 };
 
 typedef uint32_t u32;
 
@@ -35,6 +37,9 @@ template <> struct Traits<F3>  { static constexpr int R = 2, NI = 2, RS = 2; };
 template <> struct Traits<F5>  { static constexpr int R = 3, NI = 3, RS = 5; };
 template <> struct Traits<F7>  { static constexpr int R = 3, NI = 3, RS = 4; };
 template <> struct Traits<GF4> { static constexpr int R = 2, NI = 2, RS = 2; };
+template <> struct Traits<GF8> { static constexpr int R = 3, NI = 3, RS = 3; };
+template <> struct Traits<Z4>  { static constexpr int R = 2, NI = 2, RS = 2; };
+template <> struct Traits<Z8>  { static constexpr int R = 3, NI = 3, RS = 3; };
 
 // ---------------------------------------------------------------- F3
 // x += y and x -= y in three LOP3 each (a minimum found by exhaustive search over LOP3
@@ -217,6 +222,35 @@ __device__ __forceinline__ void f5_acc(u32& q_0, u32& q_1, u32& q_2, u32& k_2, u
   q_0 = t17; q_1 = t19; q_2 = t11; k_2 = t20; q_3 = t15;
 }
 
+// ---------------------------------------------------------------- Z/4, Z/8, GF(8)
+// x += y mod 4 (3 LOP3: r1 = x1 ^ y1 ^ (x0 & y0))
+__device__ __forceinline__ void z4_add(u32& x0, u32& x1, u32 y0, u32 y1) {
+  x1 = x1 ^ y1 ^ (x0 & y0);
+  x0 ^= y0;
+}
+// -x mod 4 (two's complement: (x0, x0 ^ x1)), kernels.py:125-126
+__device__ __forceinline__ void z4_neg(u32& x0, u32& x1) { x1 ^= x0; }
+// x += y mod 8: grade-school chain without the final carry (kernels.py:399-401)
+__device__ __forceinline__ void z8_add(u32& x0, u32& x1, u32& x2, u32 y0, u32 y1, u32 y2) {
+  const u32 c1 = x0 & y0;
+  const u32 c2 = lop3<LOP_MAJ>(x1, y1, c1);
+  x2 = x2 ^ y2 ^ c2;
+  x1 = x1 ^ y1 ^ c1;
+  x0 ^= y0;
+}
+// -x mod 8 (two's complement: flip above the lowest set bit), kernels.py:404-406
+__device__ __forceinline__ void z8_neg(u32& x0, u32& x1, u32& x2) {
+  x2 ^= x0 | x1;
+  x1 ^= x0;
+}
+// multiply by x in GF(8) = F2[x]/(x^3+x+1): (c0, c1, c2) -> (c2, c0 ^ c2, c1)
+__device__ __forceinline__ void gf8_mulx(u32& c0, u32& c1, u32& c2) {
+  const u32 t = c2;
+  c2 = c1;
+  c1 = c0 ^ t;
+  c0 = t;
+}
+
 // ---------------------------------------------------------------- generic row helpers
 // Plane-vector types: V<F> holds the R plane words of one 32-lane group.
 template <int F> struct V { u32 p[Traits<F>::R]; };
@@ -226,6 +260,12 @@ template <int F> __device__ __forceinline__ void vadd(V<F>& x, const V<F>& y) {
     x.p[0] ^= y.p[0];
   } else if constexpr (F == GF4) {
     x.p[0] ^= y.p[0]; x.p[1] ^= y.p[1];
+  } else if constexpr (F == GF8) {
+    x.p[0] ^= y.p[0]; x.p[1] ^= y.p[1]; x.p[2] ^= y.p[2];
+  } else if constexpr (F == Z4) {
+    z4_add(x.p[0], x.p[1], y.p[0], y.p[1]);
+  } else if constexpr (F == Z8) {
+    z8_add(x.p[0], x.p[1], x.p[2], y.p[0], y.p[1], y.p[2]);
   } else if constexpr (F == F3) {
     f3_add(x.p[0], x.p[1], y.p[0], y.p[1]);
   } else if constexpr (F == F5) {

@@ -5,6 +5,20 @@
 
 namespace sg {
 
+// X(F) for every supported field (F2, F3, F5, F7, GF4, GF8, Z4, Z8), used to dispatch runtime
+// field codes to template instantiations.
+#define SG_FOR_EACH_FIELD_CASE(field, X) \
+  switch (field) {                       \
+    case 0: X(F2); break;                \
+    case 1: X(F3); break;                \
+    case 2: X(F5); break;                \
+    case 3: X(F7); break;                \
+    case 4: X(GF4); break;               \
+    case 5: X(GF8); break;               \
+    case 6: X(Z4); break;                \
+    default: X(Z8); break;               \
+  }
+
 // Column slab per CTA (32-bit words); each lane owns one uint4 (4 words = 128 lanes) of a row.
 constexpr int SLAB_WORDS = 4;
 // Table replicas: the 8 lanes of one LDS.128 phase read 8 different C rows, so entry g is

@@ -116,11 +116,14 @@ int kernels_f3(KernelInfo** out);
 int kernels_gf4(KernelInfo** out);
 int kernels_f5(KernelInfo** out);
 int kernels_f7(KernelInfo** out);
+int kernels_gf8(KernelInfo** out);
+int kernels_z4(KernelInfo** out);
+int kernels_z8(KernelInfo** out);
 
 static std::vector<KernelInfo*>& registry() {
   static std::vector<KernelInfo*> all = [] {
     std::vector<KernelInfo*> v;
-    for (auto fn : {kernels_f2, kernels_f3, kernels_gf4, kernels_f5, kernels_f7}) {
+    for (auto fn : {kernels_f2, kernels_f3, kernels_gf4, kernels_f5, kernels_f7, kernels_gf8, kernels_z4, kernels_z8}) {
       KernelInfo* t = nullptr;
       const int n = fn(&t);
       for (int i = 0; i < n; ++i) v.push_back(&t[i]);
@@ -141,16 +144,12 @@ cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT
                                int wa32, int nwords, cudaStream_t st) {
   if (k == 8) {
     dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), 1);
-    switch (field) {
-      case F2: index_words_kernel<F2><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
-      case F3: index_words_kernel<F3><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
-      case F5: index_words_kernel<F5><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
-      case F7: index_words_kernel<F7><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
-      default: index_words_kernel<GF4><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords); break;
-    }
+#define SG_IW(FF) index_words_kernel<FF><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords)
+    SG_FOR_EACH_FIELD_CASE(field, SG_IW)
+#undef SG_IW
     return cudaGetLastError();
   }
-  const int R = field == F2 ? 1 : (field == F5 || field == F7) ? 3 : 2;
+  const int R = field == F2 ? 1 : (field == F5 || field == F7 || field == GF8 || field == Z8) ? 3 : 2;
   dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), R);
   transpose_a_kernel<<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, field == F3);
   return cudaGetLastError();
@@ -163,13 +162,9 @@ cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int6
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  switch (field) {
-    case F2: reduce_splits_kernel<F2><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits); break;
-    case F3: reduce_splits_kernel<F3><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits); break;
-    case F5: reduce_splits_kernel<F5><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits); break;
-    case F7: reduce_splits_kernel<F7><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits); break;
-    default: reduce_splits_kernel<GF4><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits); break;
-  }
+#define SG_RS(FF) reduce_splits_kernel<FF><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits)
+  SG_FOR_EACH_FIELD_CASE(field, SG_RS)
+#undef SG_RS
   return cudaGetLastError();
 }
 

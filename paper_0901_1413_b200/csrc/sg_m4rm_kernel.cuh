@@ -83,6 +83,30 @@ __device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
       const u32 q1 = comp(r.v[1][1], w);
       q[0] ^= comp(r.v[0][0], w) ^ q1;
       q[1] ^= comp(r.v[0][1], w) ^ comp(r.v[1][0], w) ^ q1;
+    } else if constexpr (F == GF8) {
+      // power basis {1, x, x^2} mod x^3+x+1: C += a + x*b + x^2*d with
+      // x*b = (b2, b0^b2, b1) and x^2*d = (d1, d1^d2, d0^d2); 7 LOP3 per word
+      const u32 a0 = comp(r.v[0][0], w), a1 = comp(r.v[0][1], w), a2 = comp(r.v[0][2], w);
+      const u32 b0 = comp(r.v[1][0], w), b1 = comp(r.v[1][1], w), b2 = comp(r.v[1][2], w);
+      const u32 d0 = comp(r.v[2][0], w), d1 = comp(r.v[2][1], w), d2 = comp(r.v[2][2], w);
+      q[0] = q[0] ^ a0 ^ b2 ^ d1;
+      q[1] = (q[1] ^ a1 ^ b0) ^ (b2 ^ d1 ^ d2);
+      q[2] = q[2] ^ a2 ^ b1 ^ d0 ^ d2;
+    } else if constexpr (F == Z4) {
+      // basis {1, 2} (_core_py.py:225-238): C += x + 2y mod 4, 3 LOP3 per word
+      const u32 x0 = comp(r.v[0][0], w), x1 = comp(r.v[0][1], w), y0 = comp(r.v[1][0], w);
+      q[1] = q[1] ^ x1 ^ y0 ^ (q[0] & x0);
+      q[0] ^= x0;
+    } else if constexpr (F == Z8) {
+      // basis {1, 2, 4} (_core_py.py:284-286): C += x + 2y + 4z mod 8 as one carry-save sum
+      const u32 x0 = comp(r.v[0][0], w), x1 = comp(r.v[0][1], w), x2 = comp(r.v[0][2], w);
+      const u32 y0 = comp(r.v[1][0], w), y1 = comp(r.v[1][1], w), z0 = comp(r.v[2][0], w);
+      const u32 k1 = q[0] & x0;
+      const u32 a = q[1] ^ x1 ^ y0;
+      const u32 ma = lop3<LOP_MAJ>(q[1], x1, y0);
+      q[2] = (q[2] ^ x2 ^ y1) ^ (z0 ^ ma ^ (a & k1));
+      q[1] = a ^ k1;
+      q[0] ^= x0;
     } else {
       // F5 / F7, basis {1, 2, 4}: C += T[g0] + 2*T[g1] + 4*T[g2] (the reference's Horner form,
       // _core_py.py:241-255, reassociated); doubling is a plane rotation in both accumulators.

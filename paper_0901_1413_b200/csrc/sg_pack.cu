@@ -14,7 +14,17 @@
 namespace sg {
 
 __host__ __device__ inline int planes_of(int field) {
-  return field == F2 ? 1 : (field == F5 || field == F7) ? 3 : 2;
+  return field == F2 ? 1 : (field == F5 || field == F7 || field == GF8 || field == Z8) ? 3 : 2;
+}
+__host__ __device__ inline int order_of(int field) {
+  switch (field) {
+    case F2: return 2;
+    case F3: return 3;
+    case F5: return 5;
+    case F7: return 7;
+    case GF4: case Z4: return 4;
+    default: return 8;  // GF8, Z8
+  }
 }
 
 // 4 bytes of a word -> bit d of each byte gathered into a nibble (byte i -> bit i)
@@ -28,7 +38,7 @@ __device__ __forceinline__ u32 spread_nibble(u32 nib) { return (nib * 0x00204081
 __global__ void pack_kernel(int field, const uint8_t* __restrict__ dense, int64_t m, int64_t n,
                             int64_t ld, u32* __restrict__ planes, int wc32, int* err) {
   const int R = planes_of(field);
-  const int order = field == F2 ? 2 : field == F3 ? 3 : field == F5 ? 5 : field == F7 ? 7 : 4;
+  const int order = order_of(field);
   const int64_t total = m * wc32;
   const u32 lim = 0x01010101u * (u32)order;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -134,7 +144,8 @@ enum {
   OP_F2_ADD = 0, OP_F3_ADD, OP_F3_SUB, OP_F3_NEG, OP_F5_ADD, OP_F5_SUB, OP_F5_NEG, OP_F5_DOUBLE,
   OP_F5_REDUCE, OP_F7_ADD, OP_F7_SUB, OP_F7_NEG, OP_F7_DOUBLE, OP_F7_REDUCE, OP_GF4_ADD,
   OP_GF4_MULX, OP_F5_FOLD5, OP_SCALAR_MUL_F3, OP_SCALAR_MUL_F5, OP_SCALAR_MUL_F7,
-  OP_SCALAR_MUL_GF4, OP_COUNT
+  OP_SCALAR_MUL_GF4, OP_Z4_ADD, OP_Z4_SUB, OP_Z4_NEG, OP_Z8_ADD, OP_Z8_SUB, OP_Z8_NEG, OP_GF8_ADD,
+  OP_GF8_MULX, OP_SCALAR_MUL_Z4, OP_SCALAR_MUL_Z8, OP_SCALAR_MUL_GF8, OP_COUNT
 };
 
 __device__ __forceinline__ void apply_op(int op, u32* d, const u32* s, u32 tail, int scalar) {
@@ -169,6 +180,38 @@ __device__ __forceinline__ void apply_op(int op, u32* d, const u32* s, u32 tail,
       }
       d[0] = a0; d[1] = a1; d[2] = a2;
     } break;
+    case OP_Z4_ADD: z4_add(d[0], d[1], s[0], s[1]); break;
+    case OP_Z4_SUB: { u32 a = s[0], b = s[1]; z4_neg(a, b); z4_add(d[0], d[1], a, b); } break;
+    case OP_Z4_NEG: z4_neg(d[0], d[1]); break;
+    case OP_Z8_ADD: z8_add(d[0], d[1], d[2], s[0], s[1], s[2]); break;
+    case OP_Z8_SUB: { u32 a = s[0], b = s[1], c = s[2]; z8_neg(a, b, c); z8_add(d[0], d[1], d[2], a, b, c); } break;
+    case OP_Z8_NEG: z8_neg(d[0], d[1], d[2]); break;
+    case OP_GF8_ADD: d[0] ^= s[0]; d[1] ^= s[1]; d[2] ^= s[2]; break;
+    case OP_GF8_MULX: gf8_mulx(d[0], d[1], d[2]); break;
+    case OP_SCALAR_MUL_Z4: {  // Horner over the bits of c
+      u32 a0 = 0, a1 = 0;
+      for (int b = 1; b >= 0; --b) {
+        a1 = a0; a0 = 0;
+        if ((scalar >> b) & 1) z4_add(a0, a1, d[0], d[1]);
+      }
+      d[0] = a0; d[1] = a1;
+    } break;
+    case OP_SCALAR_MUL_Z8: {
+      u32 a0 = 0, a1 = 0, a2 = 0;
+      for (int b = 2; b >= 0; --b) {
+        a2 = a1; a1 = a0; a0 = 0;
+        if ((scalar >> b) & 1) z8_add(a0, a1, a2, d[0], d[1], d[2]);
+      }
+      d[0] = a0; d[1] = a1; d[2] = a2;
+    } break;
+    case OP_SCALAR_MUL_GF8: {  // c = c0 + c1 x + c2 x^2
+      u32 x0 = d[0], x1 = d[1], x2 = d[2], r0 = 0, r1 = 0, r2 = 0;
+      for (int b = 0; b < 3; ++b) {
+        if ((scalar >> b) & 1) { r0 ^= x0; r1 ^= x1; r2 ^= x2; }
+        gf8_mulx(x0, x1, x2);
+      }
+      d[0] = r0; d[1] = r1; d[2] = r2;
+    } break;
     case OP_SCALAR_MUL_GF4: {  // c = c0 + c1 x
       const u32 x0 = d[0], x1 = d[1];
       u32 r0 = 0, r1 = 0;
@@ -183,7 +226,8 @@ __device__ __forceinline__ int op_planes(int op) {
   switch (op) {
     case OP_F2_ADD: return 1;
     case OP_F3_ADD: case OP_F3_SUB: case OP_F3_NEG: case OP_GF4_ADD: case OP_GF4_MULX:
-    case OP_SCALAR_MUL_F3: case OP_SCALAR_MUL_GF4: return 2;
+    case OP_SCALAR_MUL_F3: case OP_SCALAR_MUL_GF4: case OP_Z4_ADD: case OP_Z4_SUB: case OP_Z4_NEG:
+    case OP_SCALAR_MUL_Z4: return 2;
     default: return 3;
   }
 }
@@ -250,6 +294,22 @@ __global__ void block_driver_kernel(Planes C, int64_t wc64, Planes A, int64_t wa
         const u32 q1 = T_(1, g[1]);
         c.p[0] ^= T_(0, g[0]) ^ q1;
         c.p[1] ^= T_(1, g[0]) ^ T_(0, g[1]) ^ q1;
+      } else if constexpr (F == Z4) {  // acc = 2 T[g1] + T[g0]; C += acc  (_core_py.py:225-238)
+        u32 a0 = 0u, a1 = T_(0, g[1]);
+        z4_add(a0, a1, T_(0, g[0]), T_(1, g[0]));
+        z4_add(c.p[0], c.p[1], a0, a1);
+      } else if constexpr (F == GF8) {  // power basis: C += T[g0] + x T[g1] + x^2 T[g2]
+        u32 x0 = T_(0, g[2]), x1 = T_(1, g[2]), x2 = T_(2, g[2]);
+        gf8_mulx(x0, x1, x2);
+        x0 ^= T_(0, g[1]); x1 ^= T_(1, g[1]); x2 ^= T_(2, g[1]);
+        gf8_mulx(x0, x1, x2);
+        c.p[0] ^= x0 ^ T_(0, g[0]); c.p[1] ^= x1 ^ T_(1, g[0]); c.p[2] ^= x2 ^ T_(2, g[0]);
+      } else if constexpr (F == Z8) {  // Horner over {1, 2, 4} with doubling = shift (_core_py.py:262-286)
+        u32 x0 = 0u, x1 = T_(0, g[2]), x2 = T_(1, g[2]);
+        z8_add(x0, x1, x2, T_(0, g[1]), T_(1, g[1]), T_(2, g[1]));
+        x2 = x1; x1 = x0; x0 = 0u;
+        z8_add(x0, x1, x2, T_(0, g[0]), T_(1, g[0]), T_(2, g[0]));
+        z8_add(c.p[0], c.p[1], c.p[2], x0, x1, x2);
       } else {
         u32 x0 = T_(0, g[2]), x1 = T_(1, g[2]), x2 = T_(2, g[2]);
         if constexpr (F == F5) {
@@ -336,13 +396,16 @@ cudaError_t launch_plane_op(int op, Planes dst, Planes src, int64_t rows, int64_
   return cudaGetLastError();
 }
 
-#define SG_FIELD_SWITCH(field, KERNEL, ...)                                              \
-  switch (field) {                                                                      \
-    case F2: KERNEL<F2><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
-    case F3: KERNEL<F3><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
-    case F5: KERNEL<F5><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
-    case F7: KERNEL<F7><<<g, 256, 0, st>>>(__VA_ARGS__); break;                         \
-    default: KERNEL<GF4><<<g, 256, 0, st>>>(__VA_ARGS__); break;                        \
+#define SG_FIELD_SWITCH(field, KERNEL, ...)                                   \
+  switch (field) {                                                            \
+    case F2: KERNEL<F2><<<g, 256, 0, st>>>(__VA_ARGS__); break;               \
+    case F3: KERNEL<F3><<<g, 256, 0, st>>>(__VA_ARGS__); break;               \
+    case F5: KERNEL<F5><<<g, 256, 0, st>>>(__VA_ARGS__); break;               \
+    case F7: KERNEL<F7><<<g, 256, 0, st>>>(__VA_ARGS__); break;               \
+    case GF4: KERNEL<GF4><<<g, 256, 0, st>>>(__VA_ARGS__); break;             \
+    case GF8: KERNEL<GF8><<<g, 256, 0, st>>>(__VA_ARGS__); break;             \
+    case Z4: KERNEL<Z4><<<g, 256, 0, st>>>(__VA_ARGS__); break;               \
+    default: KERNEL<Z8><<<g, 256, 0, st>>>(__VA_ARGS__); break;               \
   }
 
 cudaError_t launch_block_driver(int field, Planes C, int64_t wc64, Planes A, int64_t wa64, int64_t col0, int kp,

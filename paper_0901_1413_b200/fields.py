@@ -1,10 +1,11 @@
 """Field descriptors for the B200 path (a restatement of the reference's FieldSpec data).
 
 Names, orders and encodings follow slicegemm/fields.py: F2 (:78-86), F3 unit/sign planes
-(:88-101), F5 and F7 plain 3-bit redundant patterns (:103-129), and F4 = GF(4) as
-F2[x]/(x^2+x+1) (:215), which this path stores directly as a 2-plane matrix (plane 0 =
-coefficient of 1, plane 1 = coefficient of x).  Z4/Z8 and F8/F9/F25/F27 are not on this
-path (SURVEY.md 8f lists them as next).
+(:88-101), F5 and F7 plain 3-bit redundant patterns (:103-129), the rings Z4 / Z8 (:131-158).
+GF4 / GF8 are GF(4) = F2[x]/(x^2+x+1) and GF(8) = F2[x]/(x^3+x+1) (:215-216) stored directly as
+2- / 3-plane matrices whose plane i is the coefficient of x^i (an element's residue code r in
+[0, q) is the polynomial sum_i ((r >> i) & 1) x^i).  The reference's extension-field objects
+(F4, F8, F9, F25, F27 as ExtFieldSpec) live in extension.py.
 """
 
 from __future__ import annotations
@@ -43,13 +44,14 @@ F2 = FieldSpec("f2", 2, 2, 1, _lib.SG_F2, (0, 1), (0, 1))
 F3 = FieldSpec("f3", 3, 3, 2, _lib.SG_F3, (0, 1, None, 2), (0, 1, 3))
 F5 = FieldSpec("f5", 5, 5, 3, _lib.SG_F5, (0, 1, 2, 3, 4, 0, 1, 2), (0, 1, 2, 3, 4))
 F7 = FieldSpec("f7", 7, 7, 3, _lib.SG_F7, (0, 1, 2, 3, 4, 5, 6, 0), (0, 1, 2, 3, 4, 5, 6))
-# GF(4) = F2[x]/(x^2 + x + 1): the residue r in [0, 4) is the polynomial (r & 1) + (r >> 1) x.
-F4 = FieldSpec("f4", 4, 2, 2, _lib.SG_GF4, (0, 1, 2, 3), (0, 1, 2, 3))
-GF4 = F4
+Z4 = FieldSpec("z4", 4, 4, 2, _lib.SG_Z4, (0, 1, 2, 3), (0, 1, 2, 3))
+Z8 = FieldSpec("z8", 8, 8, 3, _lib.SG_Z8, tuple(range(8)), tuple(range(8)))
+# GF(4) / GF(8) power-basis matrices: residue code r <-> polynomial sum ((r >> i) & 1) x^i.
+GF4 = FieldSpec("gf4", 4, 2, 2, _lib.SG_GF4, (0, 1, 2, 3), (0, 1, 2, 3))
+GF8 = FieldSpec("gf8", 8, 2, 3, _lib.SG_GF8, tuple(range(8)), tuple(range(8)))
 
-FIELDS = {f.name: f for f in (F2, F3, F5, F7)}
-EXT_FIELDS = {"f4": F4}
-ALL_FIELDS = {**FIELDS, **EXT_FIELDS, "gf4": F4}
+FIELDS = {f.name: f for f in (F2, F3, F5, F7, Z4, Z8)}
+ALL_FIELDS = {**FIELDS, "gf4": GF4, "gf8": GF8, "f4": GF4, "f8": GF8}
 
 
 def by_name(name: str) -> FieldSpec:

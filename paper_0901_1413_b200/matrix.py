@@ -210,21 +210,27 @@ class BitslicedMatrix:
                                                    tmask, scalar, _lib.current_stream_handle(dst.device)))
         return dst
 
+    _ADD = {"f2": "f2_add", "f3": "f3_add", "f5": "f5_add", "f7": "f7_add", "gf4": "gf4_add", "gf8": "gf8_add",
+            "z4": "z4_add", "z8": "z8_add"}
+    _SUB = {"f2": "f2_add", "f3": "f3_sub", "f5": "f5_sub", "f7": "f7_sub", "gf4": "gf4_add", "gf8": "gf8_add",
+            "z4": "z4_sub", "z8": "z8_sub"}
+    _NEG = {"f3": "f3_neg", "f5": "f5_neg", "f7": "f7_neg", "z4": "z4_neg", "z8": "z8_neg"}
+    _SMUL = {"f3": "scalar_mul_f3", "f5": "scalar_mul_f5", "f7": "scalar_mul_f7", "gf4": "scalar_mul_gf4",
+             "gf8": "scalar_mul_gf8", "z4": "scalar_mul_z4", "z8": "scalar_mul_z8"}
+
     def add(self, other: "BitslicedMatrix") -> "BitslicedMatrix":
         self._check_same(other)
-        name = {"f2": "f2_add", "f3": "f3_add", "f5": "f5_add", "f7": "f7_add", "f4": "gf4_add"}[self.field.name]
-        return self._plane_op(name, other)
+        return self._plane_op(self._ADD[self.field.name], other)
 
     def sub(self, other: "BitslicedMatrix") -> "BitslicedMatrix":
         self._check_same(other)
-        name = {"f2": "f2_add", "f3": "f3_sub", "f5": "f5_sub", "f7": "f7_sub", "f4": "gf4_add"}[self.field.name]
-        return self._plane_op(name, other)
+        return self._plane_op(self._SUB[self.field.name], other)
 
     def neg(self) -> "BitslicedMatrix":
         name = self.field.name
-        if name in ("f2", "f4"):
+        if name not in self._NEG:  # characteristic 2: -x = x
             return self._on_gpu().copy()
-        return self._plane_op({"f3": "f3_neg", "f5": "f5_neg", "f7": "f7_neg"}[name])
+        return self._plane_op(self._NEG[name])
 
     def scalar_mul(self, c: int) -> "BitslicedMatrix":
         if not 0 <= c < self.field.order:
@@ -233,8 +239,7 @@ class BitslicedMatrix:
         if name == "f2":
             return self._on_gpu().copy() if c else BitslicedMatrix.zero(self.field, self.nrows, self.ncols,
                                                                        self._on_gpu().device)
-        op = {"f3": "scalar_mul_f3", "f5": "scalar_mul_f5", "f7": "scalar_mul_f7", "f4": "scalar_mul_gf4"}[name]
-        return self._plane_op(op, scalar=c)
+        return self._plane_op(self._SMUL[name], scalar=c)
 
     def reduce_canonical(self) -> "BitslicedMatrix":
         out = self._on_gpu().copy()

@@ -7,7 +7,7 @@ import numpy as np
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 FIELD_FILES = {"f2": "m4rm_f2.npz", "f3": "m4rm_f3.npz", "f5": "m4rm_f5.npz", "f7": "m4rm_f7.npz",
-               "gf4": "gf4.npz"}
+               "gf4": "gf4.npz", "z4": "m4rm_z4.npz", "z8": "m4rm_z8.npz"}
 
 
 def cases(field):

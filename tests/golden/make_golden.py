@@ -21,6 +21,9 @@ Outputs (all small, committed):
                      oracle_multiply's dense result (oracle.py:74-79)
   gf4.npz            GF(4) inputs/outputs via Karatsuba over the reference F2 driver and
                      oracle_ext_multiply (oracle.py:192-215)
+  m4rm_z4/z8.npz     the reference's ring drivers m4rm_block_z4/z8 (_core_py.py:225-238, 284-286)
+  ext_<f>.npz        oracle_ext_multiply over F8, F9, F25, F27 (fields.py:216-219) on seeded
+                     coefficient matrices: the targets of the GPU extension-field paths
 
 Usage:  python tests/golden/make_golden.py     (from the repo root, in this container)
 """
@@ -103,6 +106,10 @@ def row_add(field, T, dst, src, n, sub=False):
             core.f7_sub(d[0], d[1], d[2], src[0], src[1], src[2], tail_mask(n))
         else:
             core.f7_add(d[0], d[1], d[2], src[0], src[1], src[2])
+    elif name == "z4":
+        (core.z4_sub if sub else core.z4_add)(d[0], d[1], src[0], src[1])
+    elif name == "z8":
+        (core.z8_sub if sub else core.z8_add)(d[0], d[1], d[2], src[0], src[1], src[2])
     else:
         raise ValueError(name)
 
@@ -249,9 +256,48 @@ def gf4_fixture():
     return recs
 
 
+def ext_fixture(spec, cases):
+    """oracle_ext_multiply over `spec` on seeded coefficient matrices (oracle.py:192-215)."""
+    recs = {}
+    base = spec.base
+    for idx, (m, l, n, sa, sb) in enumerate(cases):
+        Ac = [oracle.DenseMatrix.random(base, m, l, sa + 17 * i) for i in range(spec.degree)]
+        Bc = [oracle.DenseMatrix.random(base, l, n, sb + 17 * i) for i in range(spec.degree)]
+        Cc = oracle.oracle_ext_multiply(spec, Ac, Bc)
+        key = f"c{idx}"
+        recs[key + "_shape"] = np.array([m, l, n, sa, sb], dtype=np.int64)
+        recs[key + "_A"] = np.stack([a.entries for a in Ac]).astype(np.uint8)
+        recs[key + "_B"] = np.stack([b.entries for b in Bc]).astype(np.uint8)
+        recs[key + "_C"] = np.stack([c.entries for c in Cc]).astype(np.uint8)
+    recs["count"] = np.array(len(cases))
+    recs["degree"] = np.array(spec.degree)
+    recs["modulus"] = np.array(spec.modulus)
+    recs["p"] = np.array(base.order)
+    # 1x1 products: the whole multiplication table of the field (SPEC.md:650, acceptance #4)
+    q = base.order
+    elems = list(__import__("itertools").product(range(q), repeat=spec.degree))
+    table = np.zeros((len(elems), len(elems), spec.degree), dtype=np.uint8)
+    for i, a in enumerate(elems):
+        for j, b in enumerate(elems):
+            table[i, j] = oracle.poly_mul_mod(spec, a, b)
+    recs["elems"] = np.array(elems, dtype=np.uint8)
+    recs["mul_table"] = table
+    return recs
+
+
 def main():
     with open(os.path.join(OUT, "kernel_cases.json"), "w") as f:
         json.dump(kernel_cases(), f, indent=0)
+    for i, fname in enumerate(("z4", "z8")):
+        field = fields.FIELDS[fname]
+        recs = m4rm_fixture(field, shape_grid(10 + i)[:40] + shape_grid(10 + i)[60:70])
+        np.savez_compressed(os.path.join(OUT, f"m4rm_{fname}.npz"), **recs)
+        print(fname, "cases", int(recs["count"]))
+    ext_cases = [(1, 1, 1, 1, 2), (5, 7, 9, 3, 4), (32, 32, 32, 5, 6), (65, 70, 33, 7, 8), (100, 100, 100, 9, 10)]
+    for name in ("f8", "f9", "f25", "f27"):
+        recs = ext_fixture(fields.EXT_FIELDS[name], ext_cases)
+        np.savez_compressed(os.path.join(OUT, f"ext_{name}.npz"), **recs)
+        print(name, "ext cases", int(recs["count"]))
     for i, fname in enumerate(("f2", "f3", "f5", "f7")):
         field = fields.FIELDS[fname]
         recs = m4rm_fixture(field, shape_grid(i))

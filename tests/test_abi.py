@@ -34,14 +34,14 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_planes():
     L = _lib.load()
     assert L.sg_abi_version() == 1
-    assert [L.sg_field_planes(f) for f in range(5)] == [1, 2, 3, 3, 2]
+    assert [L.sg_field_planes(f) for f in range(8)] == [1, 2, 3, 3, 2, 3, 2, 3]
     assert L.sg_field_planes(9) == -1
 
 
 def test_invalid_arguments_are_rejected_before_cuda():
     L = _lib.load()
     vp = ctypes.c_void_p
-    rc = L.sg_m4rm(7, vp(1), vp(1), vp(1), 4, 4, 4, 8, None, 0, None)
+    rc = L.sg_m4rm(99, vp(1), vp(1), vp(1), 4, 4, 4, 8, None, 0, None)
     assert rc == _lib.SG_EINVAL and b"field" in L.sg_last_error()
     rc = L.sg_m4rm(1, vp(1), vp(1), vp(1), 4, 4, 4, 0, None, 0, None)
     assert rc == _lib.SG_EINVAL and b"k must be" in L.sg_last_error()

@@ -25,7 +25,7 @@ def _free_port():
 def _oracle_multiply(A, B):
     import oracle
     import paper_0901_1413_b200 as sg
-    name = "gf4" if A.field is sg.F4 else A.field.name
+    name = A.field.name
     C = oracle.m4rm(name, A.planes_numpy(), B.planes_numpy(), A.ncols, B.ncols, 8)
     return sg.BitslicedMatrix.from_planes(A.field, C, B.ncols, device="cpu")
 
@@ -39,7 +39,7 @@ def _worker(rank, world, port, field_name, m, l, n, out_q):
         import paper_0901_1413_b200 as sg
         from paper_0901_1413_b200 import dist as sgdist
         field = sg.by_name(field_name)
-        oname = "gf4" if field is sg.F4 else field.name
+        oname = field.name
         A_full = oracle.random_dense(oname, m, l, 0)
         r0, r1 = sgdist.row_partition(m, world)[rank]
         A_shard = sg.BitslicedMatrix.from_planes(field, oracle.pack(oname, A_full[r0:r1]), l, device="cpu")

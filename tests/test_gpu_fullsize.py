@@ -18,7 +18,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 CONFIGS = [("f3", 1024, 1024, 1024), ("f5", 4096, 4096, 4096), ("gf4", 8192, 8192, 8192),
            ("f7", 16384, 8192, 16384), ("f3", 32768, 32768, 32768)]
-FIELDS = {"f3": sg.F3, "f5": sg.F5, "f7": sg.F7, "gf4": sg.F4}
+FIELDS = {"f3": sg.F3, "f5": sg.F5, "f7": sg.F7, "gf4": sg.GF4}
 
 
 def exact_gpu_product(fname, A, B):

