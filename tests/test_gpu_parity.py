@@ -337,3 +337,20 @@ def test_stream_ordering_on_side_stream():
         C = sg.m4rm_multiply(Ag, Bg)
     s.synchronize()
     assert np.array_equal(C.planes_numpy(), expect("f7", A, B))
+
+
+def test_cli_verify_bench_ffops(capsys):
+    """The reference CLI's subcommands on the GPU path."""
+    from paper_0901_1413_b200 import cli
+    assert cli.main(["verify", "--fields", "f3,f7,z8,f4,f8,f9,f25,f27", "--max-dim", "33", "--trials", "5"]) == 0
+    out = capsys.readouterr().out
+    assert "40 products, 0 failures" in out
+    assert cli.main(["bench", "--fields", "f3,f5", "--dims", "64,100", "--reps", "2"]) == 0
+    lines = [l for l in capsys.readouterr().out.splitlines() if l and not l.startswith("#")]
+    assert lines[0] == "field,n,algorithm,ms,gffops" and len(lines) == 5
+    for l in lines[1:]:
+        f, n, alg, ms, gff = l.split(",")
+        assert abs(float(gff) - 2 * int(n) ** 3 / (float(ms) * 1e-3) / 1e9) <= 1e-3 * float(gff) + 1e-3
+    assert cli.main(["ffops", "--field", "f3", "--min", "64", "--max", "80", "--reps", "1"]) == 0
+    rows = [l for l in capsys.readouterr().out.splitlines() if l and not l.startswith("#")]
+    assert len(rows) == 1 + 17  # header + 64..80 (SPEC.md:613 example)
