@@ -41,6 +41,9 @@ CONFIGS = [
     ("F3 32768x32768x32768 k=8", "f3", 32768, 32768, 32768),
 ]
 HEADLINE = 1
+# configs whose BASELINE text shards a fixed problem over the GPUs ("row-sharded over 1/2/4/8
+# GPUs"): strong scaling; the others run the same per-GPU problem on every rank (weak scaling)
+STRONG = {"F7 16384x8192x16384 k=8", "F3 32768x32768x32768 k=8"}
 # dram__bytes_read.sum + dram__bytes_write.sum of the M4RM kernel per launch, from the committed
 # `ncu --set full` captures (profiles/*_traffic.json, written by tools/traffic_from_ncu.py)
 TRAFFIC = {}
@@ -143,6 +146,11 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
     from paper_0901_1413_b200 import m4rm as M
 
     name, field, m, l, n = cfg
+    strong = name in STRONG and world > 1
+    if strong:  # BASELINE.json configs 3-4: A/C rows sharded over the GPUs (fixed total work)
+        from paper_0901_1413_b200.dist import row_partition
+        r0, r1 = row_partition(m, world)[rank]
+        m_total, m = m, r1 - r0
     f, A, B = make_inputs(field, m, l, n, rank, device, with_b=(rank == 0))
     C = sg.BitslicedMatrix.zero(f, m, n, device=device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -178,7 +186,7 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     work = float(m) * l * n
-    value = world * work / (ms_per_step * 1e-3)
+    value = (float(m_total) * l * n if strong else world * work) / (ms_per_step * 1e-3)
 
     # dominant-kernel duration (events around each internal launch, on the launching stream)
     M.set_timing(True)
@@ -229,6 +237,7 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
                            % (peaks["lop3_per_clk_per_sm"], peaks["lds_bytes_per_clk_per_sm"], sms,
                               peaks["clock_mhz_for_peak"], peaks["clock_note"]))
     out = {"value": value, "ms_per_step": ms_per_step, "gpu_launches": launches, "clocks": clk.summary(),
+           "scaling": "strong" if name in STRONG else "weak", "m_per_gpu": m,
            "roofline": roof, "plan": plan, "transpose_ms": statistics.median(tr), "reduce_ms": statistics.median(red)}
 
     if e2e:
@@ -412,6 +421,7 @@ def main():
             per_config[cfg[0]] = {"value": r["value"], "ms_per_step": r["ms_per_step"],
                                   "roofline_frac": r["roofline"]["frac"], "bound": r["roofline"]["bound"],
                                   "own_ops_frac": r["roofline"]["own_ops"]["frac"],
+                                  "scaling": r["scaling"], "m_per_gpu": r["m_per_gpu"],
                                   "kernel_ms": r["roofline"]["kernel_ms"],
                                   "achieved_muladds_per_s": r["roofline"]["achieved_muladds_per_s"],
                                   "plan": r["plan"], "clocks": r["clocks"]}

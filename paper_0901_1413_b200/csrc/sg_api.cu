@@ -120,70 +120,70 @@ struct Calib {
   double blk, cta;
 };
 const Calib g_calib[] = {
-    {1, 1, 256, 0, 981, 2000},
-    {1, 1, 256, 1, 1370, 2000},
-    {1, 2, 256, 0, 1128, 3599},
-    {1, 2, 256, 1, 1464, 2000},
-    {1, 2, 512, 0, 1923, 10250},
-    {1, 2, 512, 1, 1743, 9667},
-    {1, 4, 256, 0, 1473, 7689},
-    {1, 4, 256, 1, 1918, 13176},
-    {1, 4, 512, 0, 2440, 16050},
-    {1, 4, 512, 1, 2440, 19580},
-    {1, 8, 256, 0, 2415, 16466},
-    {1, 8, 256, 1, 2319, 18520},
-    {1, 8, 256, 2, 2120, 19139},
-    {1, 8, 512, 0, 3704, 18719},
-    {1, 8, 512, 1, 3858, 35806},
-    {1, 16, 256, 0, 3590, 26509},
-    {1, 16, 256, 1, 3614, 29204},
-    {1, 16, 256, 2, 3294, 31731},
-    {2, 1, 256, 0, 1831, 2161},
-    {2, 1, 256, 1, 2313, 6120},
-    {2, 2, 256, 0, 2253, 4755},
-    {2, 2, 256, 1, 2598, 10576},
-    {2, 2, 512, 0, 3872, 17275},
-    {2, 2, 512, 1, 3707, 19021},
-    {2, 4, 256, 0, 3581, 16786},
-    {2, 4, 256, 1, 3246, 17972},
-    {2, 4, 256, 2, 2874, 18294},
-    {2, 4, 512, 0, 5395, 35211},
-    {2, 4, 512, 1, 5482, 37901},
-    {2, 8, 256, 0, 5032, 35651},
-    {2, 8, 256, 1, 4735, 38088},
-    {2, 8, 256, 2, 6609, 38362},
-    {3, 1, 256, 0, 1695, 4137},
-    {3, 1, 256, 1, 2256, 5876},
-    {3, 2, 256, 0, 2005, 7299},
-    {3, 2, 256, 1, 2505, 9759},
-    {3, 2, 512, 0, 3548, 14336},
-    {3, 2, 512, 1, 3454, 17003},
-    {3, 4, 256, 0, 3309, 15053},
-    {3, 4, 256, 1, 3146, 16990},
-    {3, 4, 256, 2, 2791, 16104},
-    {3, 4, 512, 0, 4881, 26995},
-    {3, 4, 512, 1, 4886, 31968},
-    {3, 8, 256, 0, 4594, 29216},
-    {3, 8, 256, 1, 4532, 31535},
-    {3, 8, 256, 2, 4203, 31339},
-    {4, 1, 256, 0, 986, 2000},
-    {4, 1, 256, 1, 1301, 4015},
-    {4, 2, 256, 0, 1138, 2693},
-    {4, 2, 256, 1, 1414, 6175},
-    {4, 2, 512, 0, 1765, 9289},
-    {4, 2, 512, 1, 1746, 10665},
-    {4, 4, 256, 0, 1494, 6096},
-    {4, 4, 256, 1, 1717, 9997},
-    {4, 4, 512, 0, 2471, 17760},
-    {4, 4, 512, 1, 2415, 19116},
-    {4, 8, 256, 0, 2338, 18147},
-    {4, 8, 256, 1, 2291, 18981},
-    {4, 8, 256, 2, 2186, 18743},
-    {4, 8, 512, 0, 3663, 35513},
-    {4, 8, 512, 1, 3651, 35671},
-    {4, 16, 256, 0, 3558, 35759},
-    {4, 16, 256, 1, 3542, 36911},
-    {4, 16, 256, 2, 3314, 37255},
+    {1, 1, 256, 0, 981, 2000},  // max err 0%
+    {1, 1, 256, 1, 1370, 2000},  // max err 1%
+    {1, 2, 256, 0, 1129, 3617},  // max err 0%
+    {1, 2, 256, 1, 1464, 2000},  // max err 1%
+    {1, 2, 512, 0, 1924, 10081},  // max err 0%
+    {1, 2, 512, 1, 1743, 9596},  // max err 0%
+    {1, 4, 256, 0, 1473, 7734},  // max err 0%
+    {1, 4, 256, 1, 1918, 13221},  // max err 0%
+    {1, 4, 512, 0, 2441, 16015},  // max err 0%
+    {1, 4, 512, 1, 2440, 19552},  // max err 0%
+    {1, 8, 256, 0, 2415, 16468},  // max err 0%
+    {1, 8, 256, 1, 2319, 18453},  // max err 0%
+    {1, 8, 256, 2, 2123, 18847},  // max err 0%
+    {1, 8, 512, 0, 3703, 19088},  // max err 1%
+    {1, 8, 512, 1, 3860, 35949},  // max err 0%
+    {1, 16, 256, 0, 3592, 26712},  // max err 0%
+    {1, 16, 256, 1, 3613, 29265},  // max err 0%
+    {1, 16, 256, 2, 3299, 32254},  // max err 0%
+    {2, 1, 256, 0, 1826, 2174},  // max err 1%
+    {2, 1, 256, 1, 2333, 5903},  // max err 1%
+    {2, 2, 256, 0, 2224, 4963},  // max err 1%
+    {2, 2, 256, 1, 2569, 10700},  // max err 0%
+    {2, 2, 512, 0, 3859, 16994},  // max err 1%
+    {2, 2, 512, 1, 3687, 19251},  // max err 1%
+    {2, 4, 256, 0, 3552, 16921},  // max err 0%
+    {2, 4, 256, 1, 3204, 18621},  // max err 0%
+    {2, 4, 256, 2, 2895, 17950},  // max err 0%
+    {2, 4, 512, 0, 5397, 35088},  // max err 2%
+    {2, 4, 512, 1, 5208, 39246},  // max err 2%
+    {2, 8, 256, 0, 5051, 35463},  // max err 2%
+    {2, 8, 256, 1, 4742, 38123},  // max err 2%
+    {2, 8, 256, 2, 5575, 39612},  // max err 2%
+    {3, 1, 256, 0, 1689, 4212},  // max err 0%
+    {3, 1, 256, 1, 2255, 6002},  // max err 0%
+    {3, 2, 256, 0, 2006, 7342},  // max err 0%
+    {3, 2, 256, 1, 2507, 9571},  // max err 0%
+    {3, 2, 512, 0, 3547, 14538},  // max err 0%
+    {3, 2, 512, 1, 3320, 17115},  // max err 0%
+    {3, 4, 256, 0, 3311, 15066},  // max err 0%
+    {3, 4, 256, 1, 3167, 17247},  // max err 0%
+    {3, 4, 256, 2, 2779, 16263},  // max err 0%
+    {3, 4, 512, 0, 4885, 27384},  // max err 1%
+    {3, 4, 512, 1, 4916, 32669},  // max err 0%
+    {3, 8, 256, 0, 4587, 29211},  // max err 0%
+    {3, 8, 256, 1, 4506, 32100},  // max err 0%
+    {3, 8, 256, 2, 4042, 32361},  // max err 0%
+    {4, 1, 256, 0, 986, 2000},  // max err 0%
+    {4, 1, 256, 1, 1301, 4015},  // max err 0%
+    {4, 2, 256, 0, 1138, 2693},  // max err 1%
+    {4, 2, 256, 1, 1414, 6175},  // max err 0%
+    {4, 2, 512, 0, 1765, 9289},  // max err 0%
+    {4, 2, 512, 1, 1746, 10665},  // max err 0%
+    {4, 4, 256, 0, 1494, 6096},  // max err 0%
+    {4, 4, 256, 1, 1717, 9997},  // max err 0%
+    {4, 4, 512, 0, 2471, 17760},  // max err 0%
+    {4, 4, 512, 1, 2415, 19116},  // max err 0%
+    {4, 8, 256, 0, 2338, 18147},  // max err 0%
+    {4, 8, 256, 1, 2291, 18981},  // max err 0%
+    {4, 8, 256, 2, 2186, 18743},  // max err 0%
+    {4, 8, 512, 0, 3663, 35513},  // max err 0%
+    {4, 8, 512, 1, 3651, 35671},  // max err 1%
+    {4, 16, 256, 0, 3558, 35759},  // max err 0%
+    {4, 16, 256, 1, 3542, 36911},  // max err 0%
+    {4, 16, 256, 2, 3314, 37255},  // max err 0%
 };
 
 const Calib* calib_for(const KernelInfo* ki) {

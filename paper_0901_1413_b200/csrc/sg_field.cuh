@@ -222,6 +222,143 @@ __device__ __forceinline__ void f5_acc(u32& q_0, u32& q_1, u32& q_2, u32& k_2, u
   q_0 = t17; q_1 = t19; q_2 = t11; k_2 = t20; q_3 = t15;
 }
 
+// 4-word interleaved form of f7_acc: each adder is issued for all four words in turn
+__device__ __forceinline__ void f7_acc4(u32 (&q)[4][4], const u32 (&in)[4][9]) {
+  u32 t1[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t1[w] = lop3<0x96>(q[w][0], q[w][1], in[w][0]);
+  u32 t2[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t2[w] = lop3<0xe8>(q[w][0], q[w][1], in[w][0]);
+  u32 t3[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t3[w] = lop3<0x96>(in[w][5], in[w][7], t1[w]);
+  u32 t4[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t4[w] = lop3<0xe8>(in[w][5], in[w][7], t1[w]);
+  u32 t5[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t5[w] = lop3<0x96>(q[w][2], in[w][1], in[w][3]);
+  u32 t6[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t6[w] = lop3<0xe8>(q[w][2], in[w][1], in[w][3]);
+  u32 t7[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t7[w] = lop3<0x96>(q[w][3], in[w][2], in[w][4]);
+  u32 t8[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t8[w] = lop3<0xe8>(q[w][3], in[w][2], in[w][4]);
+  u32 t9[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t9[w] = lop3<0x96>(in[w][6], t6[w], t7[w]);
+  u32 t10[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t10[w] = lop3<0xe8>(in[w][6], t6[w], t7[w]);
+  u32 t11[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t11[w] = lop3<0x96>(t8[w], t3[w], t10[w]);
+  u32 t12[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t12[w] = lop3<0xe8>(t8[w], t3[w], t10[w]);
+  u32 t13[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t13[w] = lop3<0x96>(in[w][8], t2[w], t5[w]);
+  u32 t14[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t14[w] = lop3<0xe8>(in[w][8], t2[w], t5[w]);
+  u32 t15[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t15[w] = lop3<0x96>(t4[w], t13[w], t12[w]);
+  u32 t16[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t16[w] = lop3<0xe8>(t4[w], t13[w], t12[w]);
+  u32 t17[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t17[w] = lop3<0x96>(t9[w], t14[w], t16[w]);
+  u32 t18[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t18[w] = lop3<0xe8>(t9[w], t14[w], t16[w]);
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    q[w][0] = t11[w];
+    q[w][1] = t18[w];
+    q[w][2] = t15[w];
+    q[w][3] = t17[w];
+  }
+}
+
+// 4-word interleaved form of f5_acc: each adder is issued for all four words in turn
+__device__ __forceinline__ void f5_acc4(u32 (&q)[4][5], const u32 (&in)[4][9]) {
+  u32 t1[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t1[w] = lop3<0x69>(q[w][0], in[w][0], in[w][6]);
+  u32 t2[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t2[w] = lop3<0xd4>(q[w][0], in[w][0], in[w][6]);
+  u32 t3[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t3[w] = lop3<0x96>(q[w][1], in[w][1], in[w][3]);
+  u32 t4[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t4[w] = lop3<0xe8>(q[w][1], in[w][1], in[w][3]);
+  u32 t5[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t5[w] = lop3<0x69>(in[w][7], t2[w], t3[w]);
+  u32 t6[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t6[w] = lop3<0x8e>(in[w][7], t2[w], t3[w]);
+  u32 t7[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t7[w] = lop3<0x96>(q[w][2], q[w][3], in[w][2]);
+  u32 t8[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t8[w] = lop3<0xe8>(q[w][2], q[w][3], in[w][2]);
+  u32 t9[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t9[w] = lop3<0x69>(in[w][4], in[w][8], t4[w]);
+  u32 t10[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t10[w] = lop3<0xb2>(in[w][4], in[w][8], t4[w]);
+  u32 t11[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t11[w] = lop3<0x96>(t7[w], t6[w], t9[w]);
+  u32 t12[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t12[w] = lop3<0xe8>(t7[w], t6[w], t9[w]);
+  u32 t13[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t13[w] = lop3<0x96>(q[w][4], in[w][5], t8[w]);
+  u32 t14[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t14[w] = lop3<0xe8>(q[w][4], in[w][5], t8[w]);
+  u32 t15[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t15[w] = lop3<0x96>(t10[w], t13[w], t12[w]);
+  u32 t16[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t16[w] = lop3<0xe8>(t10[w], t13[w], t12[w]);
+  u32 t17[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t17[w] = lop3<0x96>(t1[w], t14[w], t16[w]);
+  u32 t18[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t18[w] = lop3<0xe8>(t1[w], t14[w], t16[w]);
+  u32 t19[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t19[w] = lop3<0x96>(t5[w], t18[w], 0u);
+  u32 t20[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) t20[w] = lop3<0xe8>(t5[w], t18[w], 0u);
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    q[w][0] = t17[w];
+    q[w][1] = t19[w];
+    q[w][2] = t11[w];
+    q[w][3] = t20[w];
+    q[w][4] = t15[w];
+  }
+}
+
 // ---------------------------------------------------------------- Z/4, Z/8, GF(8)
 // x += y mod 4 (3 LOP3: r1 = x1 ^ y1 ^ (x0 & y0))
 __device__ __forceinline__ void z4_add(u32& x0, u32& x1, u32 y0, u32 y1) {

@@ -69,6 +69,18 @@ __device__ __forceinline__ u32 comp(const uint4& v, int w) { return w == 0 ? v.x
 // One (row, k-block) update of the 4 C words a lane owns from its loaded table rows.
 template <int F>
 __device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
+  if constexpr (F == F5 || F == F7) {
+    // carry-save networks issued adder by adder across the four words (ILP 4 per step)
+    u32 in[4][9];
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) in[w][3 * i + d] = comp(r.v[i][d], w);
+    if constexpr (F == F7) f7_acc4(c.w, in); else f5_acc4(c.w, in);
+    return;
+  }
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     u32* q = c.w[w];
@@ -497,12 +509,10 @@ __global__ void __launch_bounds__(SCHED == 2 ? NT + WS_BUILDERS : NT, 1) m4rm_ke
       // spread the next table's replica stores over the row-slot loop
       lookups(s, s & 1, [&](int t) {
         if (nxt) {
-          if constexpr (RT >= CPT) {
-            if (t % (RT / CPT) == 0) phase2_store(tnext, v, t / (RT / CPT));
-          } else {
+          // replica cc goes out after row-slot floor(cc * RT / CPT): all CPT, spread evenly
 #pragma unroll
-            for (int q = 0; q < CPT / RT; ++q) phase2_store(tnext, v, t * (CPT / RT) + q);
-          }
+          for (int cc = 0; cc < CPT; ++cc)
+            if ((cc * RT) / CPT == t) phase2_store(tnext, v, cc);
         }
       });
       if (s + 2 < s_end) phase1(s + 2);
