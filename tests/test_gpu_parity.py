@@ -354,3 +354,36 @@ def test_cli_verify_bench_ffops(capsys):
     assert cli.main(["ffops", "--field", "f3", "--min", "64", "--max", "80", "--reps", "1"]) == 0
     rows = [l for l in capsys.readouterr().out.splitlines() if l and not l.startswith("#")]
     assert len(rows) == 1 + 17  # header + 64..80 (SPEC.md:613 example)
+
+
+def test_no_writes_outside_c():
+    """Guard words around C stay untouched for ragged shapes and every schedule (stand-in for a
+    memcheck run: compute-sanitizer is closed on this pool)."""
+    import ctypes
+    from paper_0901_1413_b200 import _lib
+    L = _lib.load()
+    guard = 4096
+    for fname, (m, l, n) in (("f3", (77, 301, 130)), ("f7", (513, 257, 65)), ("gf4", (1, 9, 1)), ("f5", (300, 1000, 700))):
+        f = FIELDS[fname]
+        A = sg.BitslicedMatrix.from_dense(f, oracle.random_dense(fname, m, l, 1))
+        B = sg.BitslicedMatrix.from_dense(f, oracle.random_dense(fname, l, n, 2))
+        want = expect(fname, oracle.unpack(fname, A.planes_numpy(), l), oracle.unpack(fname, B.planes_numpy(), n))
+        words = f.bits * m * ((n + 63) // 64)
+        for rt, sched, splits in ((1, 0, 1), (2, 1, 3), (4, 2, 2), (8, 2, 1)):
+            m4rm_mod.set_plan_override(rt, splits, sched, 256)
+            buf = torch.full((words + 2 * guard,), 0x5A5A5A5A5A5A5A5A - (1 << 64), dtype=torch.int64, device="cuda")
+            try:
+                rc = L.sg_m4rm(f.code, ctypes.c_void_p(A.planes.data_ptr()), ctypes.c_void_p(B.planes.data_ptr()),
+                               ctypes.c_void_p(buf.data_ptr() + guard * 8), m, l, n, 8, None, 0,
+                               _lib.current_stream_handle())
+            finally:
+                m4rm_mod.set_plan_override(0, 0, -1, 0)
+            if rc == _lib.SG_EUNSUPPORTED:
+                continue
+            _lib.check(rc)
+            torch.cuda.synchronize()
+            g = buf.cpu().numpy().view(np.uint64)
+            assert (g[:guard] == 0x5A5A5A5A5A5A5A5A).all() and (g[guard + words:] == 0x5A5A5A5A5A5A5A5A).all(), \
+                (fname, rt, sched, splits)
+            got = g[guard:guard + words].reshape(f.bits, m, -1)
+            assert np.array_equal(got, want), (fname, rt, sched, splits)
