@@ -371,7 +371,7 @@ def test_no_writes_outside_c():
         words = f.bits * m * ((n + 63) // 64)
         for rt, sched, splits in ((1, 0, 1), (2, 1, 3), (4, 2, 2), (8, 2, 1)):
             m4rm_mod.set_plan_override(rt, splits, sched, 256)
-            buf = torch.full((words + 2 * guard,), 0x5A5A5A5A5A5A5A5A - (1 << 64), dtype=torch.int64, device="cuda")
+            buf = torch.full((words + 2 * guard,), 0x5A5A5A5A5A5A5A5A, dtype=torch.int64, device="cuda")
             try:
                 rc = L.sg_m4rm(f.code, ctypes.c_void_p(A.planes.data_ptr()), ctypes.c_void_p(B.planes.data_ptr()),
                                ctypes.c_void_p(buf.data_ptr() + guard * 8), m, l, n, 8, None, 0,
