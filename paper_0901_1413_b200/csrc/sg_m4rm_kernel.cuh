@@ -159,18 +159,19 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 
 // SCHED 0: per k-block  phase1 | sync | phase2 | sync | lookups   (one table buffer)
 // SCHED 1: per k-block  lookups(s) + phase2(s+1) + phase1(s+2) | sync  (two table buffers)
-// SCHED 2: warp-specialized (k = 8): NT lookup threads + 4 builder warps that stage B and A
+// SCHED 2/3/4: warp-specialized (k = 8): NT lookup threads + 4/1/2 builder warps that stage B and A
 //          with cp.async and builds block s+1's table into the other buffer while the lookup warps
 //          consume block s; FULL/EMPTY named barriers hand the two buffers back and forth.
 // ABL (experiments only, 0 in production): bit 0 skips the table-replica stores, bit 1 replaces
 // the field update by a plain XOR of the looked-up rows, bit 2 skips the lookups.
-constexpr int WS_BUILDERS = 128;  // builder threads (4 warps) of the warp-specialized schedule
+// builder threads of the warp-specialized schedules: SCHED 2 -> 4 warps, 3 -> 1 warp, 4 -> 2 warps
+__host__ __device__ constexpr int ws_builders(int sched) { return sched == 2 ? 128 : sched == 3 ? 32 : sched == 4 ? 64 : 0; }
 
 template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
-__global__ void __launch_bounds__(SCHED == 2 ? NT + WS_BUILDERS : NT, 1) m4rm_kernel(const M4rmArgs a) {
+__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a) {
   constexpr bool PIPE = SCHED == 1;
-  constexpr bool WS = SCHED == 2;
-  static_assert(!WS || K == 8, "the warp-specialized schedule is k = 8 only");
+  constexpr bool WS = SCHED >= 2;
+  static_assert(!WS || K == 8, "the warp-specialized schedules are k = 8 only");
   constexpr int R = Traits<F>::R;
   constexpr int E = 1 << K;
   constexpr int KLO = K < 4 ? K : 4;
@@ -378,8 +379,8 @@ __global__ void __launch_bounds__(SCHED == 2 ? NT + WS_BUILDERS : NT, 1) m4rm_ke
   };
 
   if constexpr (WS) {
-    constexpr int NB = NT + WS_BUILDERS;  // all threads take part in every FULL / EMPTY barrier
-    constexpr int NBT = WS_BUILDERS;
+    constexpr int NBT = ws_builders(SCHED);
+    constexpr int NB = NT + NBT;  // all threads take part in every FULL / EMPTY barrier
     auto FULL = [](int s) { return 1 + (s & 1); };
     auto EMPTY = [](int s) { return 3 + (s & 1); };
     if (tid >= NT) {
@@ -555,9 +556,9 @@ constexpr int smem_bytes_for() {
          NSLOT * NAP * RT * NT * 4;
 }
 
-#define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (P) == 2 ? (NT) + WS_BUILDERS : (NT), P, \
+#define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \
                                smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0}
-#define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (P) == 2 ? (NT) + WS_BUILDERS : (NT), P, \
+#define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (NT) + ws_builders(P), P, \
                                    smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A}
 // k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
 #define SG_KSET8(F)                                                                                 \

@@ -105,6 +105,10 @@ def build_table(B: BitslicedMatrix, s: int, k: int) -> torch.Tensor:
     return T
 
 
+SCHEDULES = {0: "serial", 1: "pipelined", 2: "warp-specialized (4 builder warps)",
+             3: "warp-specialized (1 builder warp)", 4: "warp-specialized (2 builder warps)"}
+
+
 def plan(field, m: int, l: int, n: int, k: int = 8) -> dict:
     """The launch the planner picks for this product (rows per CTA, k-splits, CTAs)."""
     from .fields import by_name
@@ -114,7 +118,7 @@ def plan(field, m: int, l: int, n: int, k: int = 8) -> dict:
     _lib.check(_lib.load().sg_plan(field.code, m, l, n, k, ctypes.byref(rows), ctypes.byref(splits),
                                    ctypes.byref(ctas), ctypes.byref(idx), ctypes.byref(pipe), ctypes.byref(thr)))
     return {"rows_per_cta": rows.value, "splits": splits.value, "ctas": ctas.value, "kernel": idx.value,
-            "schedule": ("serial", "pipelined", "warp-specialized")[pipe.value], "threads": thr.value}
+            "schedule": SCHEDULES.get(pipe.value, str(pipe.value)), "threads": thr.value}
 
 
 def set_plan_override(rows_per_thread: int = 0, splits: int = 0, pipe: int = -1, threads: int = 0):
