@@ -5,8 +5,6 @@
 namespace sg {
 
 static KernelInfo g_table[] = {
-    SG_K(F3, 8, 16, 3, 224),
-    SG_K(F3, 8, 18, 3, 224),
     SG_K(F3, 8, 16, 2, 256),
     SG_K(F3, 8, 8, 2, 256),
     SG_KSET8(F3),

@@ -5,8 +5,6 @@
 namespace sg {
 
 static KernelInfo g_table[] = {
-    SG_K(F5, 8, 8, 3, 224),
-    SG_K(F5, 8, 9, 3, 224),
     SG_K(F5, 8, 8, 2, 256),
     SG_K(F5, 8, 4, 2, 256),
     SG_KSET8(F5),

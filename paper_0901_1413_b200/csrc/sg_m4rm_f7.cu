@@ -5,8 +5,6 @@
 namespace sg {
 
 static KernelInfo g_table[] = {
-    SG_K(F7, 8, 8, 3, 224),
-    SG_K(F7, 8, 9, 3, 224),
     SG_K(F7, 8, 8, 2, 256),
     SG_K(F7, 8, 4, 2, 256),
     SG_KSET8(F7),

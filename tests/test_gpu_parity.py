@@ -122,9 +122,9 @@ def test_every_compiled_plan(fname):  # noqa: F811
     B = oracle.random_dense(fname, 1000, 777, 8)
     want = expect(fname, A, B)
     ran = 0
-    for rt in (1, 2, 4, 8, 9, 16, 18):
-        for pipe in (0, 1, 2, 3):
-            for nt in (224, 256, 512):
+    for rt in (1, 2, 4, 8, 16):
+        for pipe in (0, 1, 2):
+            for nt in (256, 512):
                 for splits in (1, 2, 5, 16):
                     m4rm_mod.set_plan_override(rt, splits, pipe, nt)
                     try:

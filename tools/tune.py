@@ -29,9 +29,9 @@ for ci in [int(x) for x in a.configs.split(",")]:
     M.set_plan_override(0, 0, -1, 0)
     auto = sg.plan(f, m, l, n, 8)
     best = None
-    for rt in (1, 2, 4, 8, 9, 16, 18):
-        for nt in (224, 256, 512):
-            for pipe in (0, 1, 2, 3):
+    for rt in (1, 2, 4, 8, 16):
+        for nt in (256, 512):
+            for pipe in (0, 1, 2):
                 for sp in [int(x) for x in a.splits.split(",")]:
                     M.set_plan_override(rt, sp, pipe, nt)
                     try:
