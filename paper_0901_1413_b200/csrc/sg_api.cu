@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -550,7 +551,10 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   const size_t a_bytes = (size_t)R * m * wa * 8, b_bytes = (size_t)R * l * wc * 8, c_bytes = (size_t)R * m * wc * 8;
   // Row-chunked pipeline: B goes up first, then chunk i's rows of A go up while chunk i-1 is
   // multiplied and chunk i-2's rows of C come down (three streams, events between them).
-  const int P = (int)std::max<int64_t>(1, std::min<int64_t>(4, m / 2048));
+  // measured on B200 (tools/e2e_chunks.py): 2 chunks from 4096 rows, 4 from 16384
+  int P = m >= 16384 ? 4 : (m >= 4096 ? 2 : 1);
+  if (const char* e = getenv("SG_HOST_CHUNKS")) P = std::max(1, std::min(4, atoi(e)));  // experiments
+  if (P > m) P = (int)std::max<int64_t>(1, m);
   struct Io {
     cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
     cudaEvent_t ev_in[4], ev_comp[4];
