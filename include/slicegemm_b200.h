@@ -18,6 +18,7 @@
  *   sg_m4rm                  m4rm_multiply(A, B, params) (__init__.py:16), and
  *                            for SG_GF4 ext_multiply over F4 (__init__.py:17)
  *   sg_m4rm_host             the same with host buffers (the call a CPU caller makes)
+ *   sg_classical             classical_multiply (__init__.py:16)
  *
  * Data layout (identical bits to the reference's BitslicedMatrix planes):
  *   a matrix of `rows` x `n` over a field with R planes is R contiguous planes, each `rows` x
@@ -127,6 +128,11 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
 /* Same with host buffers: copies in, multiplies on `device`, copies C back; synchronous. */
 int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
                  int64_t l, int64_t n, int k, int device);
+
+/* classical_multiply: the table-free row-accumulate product, a cross-check
+ * (O(m l n / 32) word operations); canonical output, same layout as sg_m4rm. */
+int sg_classical(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l,
+                 int64_t n, void* stream);
 
 /* Block-granularity plugin mirror.  Plane pointer arrays as in sg_plane_op.  T has the
  * reference table layout: per plane 2^kp rows x words 64-bit words, entry g = the sum of B rows

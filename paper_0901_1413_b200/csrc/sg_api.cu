@@ -647,6 +647,28 @@ int sg_m4rm_block(int field, uint64_t* const* C, int64_t c_words, const uint64_t
   return SG_OK;
 }
 
+int sg_classical(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
+                 void* stream) {
+  int rc = check_mul_args(field, A, B, C, m, l, n, 1);
+  if (rc != SG_OK) return rc;
+  if (m == 0 || n == 0) return SG_OK;
+  const int R = planes(field);
+  const int64_t wa = w64_of(l), wb = w64_of(n);
+  if (l == 0) {
+    SG_CUDA(cudaMemsetAsync(C, 0, (size_t)R * m * wb * 8, (cudaStream_t)stream), "sg_classical zero");
+    return SG_OK;
+  }
+  Planes a, b, c;
+  for (int d = 0; d < 3; ++d) {
+    a.p[d] = d < R ? const_cast<uint64_t*>(A) + d * m * wa : nullptr;
+    b.p[d] = d < R ? const_cast<uint64_t*>(B) + d * l * wb : nullptr;
+    c.p[d] = d < R ? C + d * m * wb : nullptr;
+  }
+  SG_CUDA(launch_classical(field, a, wa, b, wb, c, m, l, (cudaStream_t)stream), "sg_classical");
+  g_launches++;
+  return SG_OK;
+}
+
 int sg_probe_peaks(int device, double* lop3, double* lds, double* mhz) {
   if (!lop3 || !lds || !mhz) return fail(SG_EINVAL, "null pointer");
   if (probe_peaks(device, lop3, lds, mhz) != 0) return fail(SG_ECUDA, "peak probe failed");

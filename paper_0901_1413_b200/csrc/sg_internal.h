@@ -75,6 +75,8 @@ cudaError_t launch_block_driver(int field, Planes C, int64_t wc64, Planes A, int
                                 int kp, Planes T, int64_t row0, int64_t row1, cudaStream_t st);
 cudaError_t launch_build_table(int field, Planes B, int64_t b_rows, int64_t row_base, int kp, int64_t wc64,
                                Planes T, cudaStream_t st);
+cudaError_t launch_classical(int field, Planes A, int64_t wa64, Planes B, int64_t wb64, Planes C, int64_t m,
+                             int64_t l, cudaStream_t st);
 
 // sg_peaks.cu
 int probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_sm, double* sm_mhz);

@@ -355,6 +355,53 @@ __global__ void build_table_kernel(Planes B, int64_t b_rows, int64_t row_base, i
   }
 }
 
+// ------------------------------------------------------------------ classical product
+// C_i = sum_j a_ij B_j row by row (_core_py.py:289-366): no tables, one thread
+// per (row, 32-bit word of C), every coefficient expanded over the field's basis.  O(m l n / 32)
+// word operations: the independent mid-level cross-check of the M4RM kernel, not a fast path.
+template <int F>
+__global__ void classical_kernel(Planes A, int64_t wa64, Planes B, int64_t wb64, Planes C, int64_t m, int64_t l) {
+  constexpr int R = Traits<F>::R;
+  const int64_t wc32 = 2 * wb64;
+  const int64_t total = m * wc32;
+  const u32* Bp[3];
+  for (int d = 0; d < R; ++d) Bp[d] = reinterpret_cast<const u32*>(B.p[d]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / wc32, w = i % wc32;
+    V<F> acc;
+    for (int d = 0; d < R; ++d) acc.p[d] = 0u;
+    for (int64_t j = 0; j < l; ++j) {
+      unsigned pat = 0;
+      for (int d = 0; d < R; ++d) pat |= (unsigned)((A.p[d][row * wa64 + (j >> 6)] >> (j & 63)) & 1ull) << d;
+      if (!pat) continue;
+      V<F> b;
+      for (int d = 0; d < R; ++d) b.p[d] = Bp[d][j * wc32 + w];
+      if constexpr (F == F3) {  // pattern 01 = 1, 11 = -1
+        if (pat == 1) f3_add(acc.p[0], acc.p[1], b.p[0], b.p[1]);
+        else f3_sub(acc.p[0], acc.p[1], b.p[0], b.p[1]);
+      } else if constexpr (F == GF4 || F == GF8) {  // a = sum_d bit_d x^d
+        for (int d = 0; d < R; ++d) {
+          if ((pat >> d) & 1)
+            for (int e = 0; e < R; ++e) acc.p[e] ^= b.p[e];
+          if (F == GF4) { const u32 t = b.p[1]; b.p[1] ^= b.p[0]; b.p[0] = t; }
+          else gf8_mulx(b.p[0], b.p[1], b.p[2]);
+        }
+      } else {  // binary digits with doubling: F2, F5, F7, Z4, Z8
+        for (int d = 0; d < R; ++d) {
+          if ((pat >> d) & 1) vadd<F>(acc, b);
+          if constexpr (F == F5) f5_double(b.p[0], b.p[1], b.p[2]);
+          if constexpr (F == F7) f7_double(b.p[0], b.p[1], b.p[2]);
+          if constexpr (F == Z4) { b.p[1] = b.p[0]; b.p[0] = 0u; }
+          if constexpr (F == Z8) { b.p[2] = b.p[1]; b.p[1] = b.p[0]; b.p[0] = 0u; }
+        }
+      }
+    }
+    vcanon<F>(acc);
+    for (int d = 0; d < R; ++d) reinterpret_cast<u32*>(C.p[d])[row * wc32 + w] = acc.p[d];
+  }
+}
+
 static unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -426,4 +473,15 @@ cudaError_t launch_build_table(int field, Planes B, int64_t b_rows, int64_t row_
   return cudaGetLastError();
 }
 
+}  // namespace sg
+
+namespace sg {
+cudaError_t launch_classical(int field, Planes A, int64_t wa64, Planes B, int64_t wb64, Planes C, int64_t m,
+                             int64_t l, cudaStream_t st) {
+  const int64_t work = m * 2 * wb64;
+  if (work <= 0) return cudaSuccess;
+  const unsigned g = grid_for(work, 256);
+  SG_FIELD_SWITCH(field, classical_kernel, A, wa64, B, wb64, C, m, l);
+  return cudaGetLastError();
+}
 }  // namespace sg
