@@ -9,7 +9,7 @@ C ABI in include/slicegemm_b200.h.  There is no CPU fallback.
 
 from .fields import F2, F3, F5, F7, GF4, GF8, Z4, Z8, FIELDS, FieldSpec, by_name
 from .matrix import BitslicedMatrix
-from .m4rm import M4rmParams, build_table, choose_k, m4rm_multiply, plan
+from .m4rm import M4rmParams, build_table, choose_k, classical_multiply, m4rm_multiply, plan
 from .extension import EXT_FIELDS, F4, F8, F9, F25, F27, ExtFieldSpec, ExtMatrix, ext_multiply, poly_reduce
 from . import _core_cuda
 
@@ -24,5 +24,5 @@ def backend_name() -> str:
 __all__ = [
     "BitslicedMatrix", "ExtFieldSpec", "ExtMatrix", "M4rmParams", "FieldSpec",
     "F2", "F3", "F4", "F5", "F7", "F8", "F9", "F25", "F27", "GF4", "GF8", "Z4", "Z8", "FIELDS", "EXT_FIELDS",
-    "backend_name", "build_table", "by_name", "choose_k", "ext_multiply", "m4rm_multiply", "plan", "poly_reduce",
+    "backend_name", "build_table", "by_name", "choose_k", "classical_multiply", "ext_multiply", "m4rm_multiply", "plan", "poly_reduce",
 ]

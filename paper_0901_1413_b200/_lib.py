@@ -33,7 +33,7 @@ EXPORTS = (
     "sg_abi_version", "sg_last_error", "sg_field_planes", "sg_pack", "sg_unpack",
     "sg_reduce_canonical", "sg_plane_op", "sg_m4rm_workspace_bytes", "sg_m4rm", "sg_m4rm_host",
     "sg_build_table", "sg_m4rm_block", "sg_plan", "sg_set_plan_override", "sg_set_timing",
-    "sg_last_timing", "sg_launch_count", "sg_probe_peaks", "sg_debug_ablation",
+    "sg_last_timing", "sg_launch_count", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
 )
 
 _lib = None
@@ -77,6 +77,7 @@ def load():
         "sg_launch_count": ([], i64),
         "sg_probe_peaks": ([i32, dp, dp, dp], i32),
         "sg_debug_ablation": ([i32], i32),
+        "sg_classical": ([i32, vp, vp, vp, i64, i64, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -82,6 +82,24 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
     return C
 
 
+def classical_multiply(A: BitslicedMatrix, B: BitslicedMatrix) -> BitslicedMatrix:
+    """C = A B by row accumulation without tables: the reference's mid-level
+    cross-check, on the GPU (O(m l n / 32) word operations)."""
+    _check(A, B)
+    m, l, n = A.nrows, A.ncols, B.ncols
+    dev = A.device if A.device.type == "cuda" else B.device
+    if dev.type != "cuda":
+        dev = torch.device("cuda", torch.cuda.current_device())
+    _require_cuda(dev)
+    a, b = A.planes.to(dev).contiguous(), B.planes.to(dev).contiguous()
+    C = BitslicedMatrix(A.field, m, n, torch.empty((A.field.bits, m, (n + 63) // 64), dtype=torch.int64, device=dev))
+    if m and n:
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().sg_classical(A.field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n,
+                                                _lib.current_stream_handle(dev)))
+    return C
+
+
 def build_table(B: BitslicedMatrix, s: int, k: int) -> torch.Tensor:
     """Table of block s (rows s*k .. s*k+kp-1 of B): int64 tensor (R, 2^kp, words).
 

@@ -387,3 +387,16 @@ def test_no_writes_outside_c():
                 (fname, rt, sched, splits)
             got = g[guard:guard + words].reshape(f.bits, m, -1)
             assert np.array_equal(got, want), (fname, rt, sched, splits)
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
+def test_classical_multiply_cross_check(fname):
+    """classical_multiply (no tables) agrees with m4rm_multiply and the oracle."""
+    f = FIELDS[fname]
+    for (m, l, n) in ((1, 1, 1), (33, 65, 70), (100, 130, 257)):
+        A = oracle.random_dense(fname, m, l, m + l)
+        B = oracle.random_dense(fname, l, n, n)
+        Ag, Bg = sg.BitslicedMatrix.from_dense(f, A), sg.BitslicedMatrix.from_dense(f, B)
+        Cc = sg.classical_multiply(Ag, Bg)
+        assert np.array_equal(Cc.planes_numpy(), expect(fname, A, B)), (fname, m, l, n)
+        assert np.array_equal(Cc.planes_numpy(), sg.m4rm_multiply(Ag, Bg).planes_numpy())
