@@ -1,6 +1,6 @@
 """Extract per-launch DRAM traffic of the M4RM kernel from ncu reports into profiles/<tag>_traffic.json.
 
-python tools/traffic_from_ncu.py TAG "CONFIG NAME=report.ncu-rep" ..."""
+python tools/traffic_from_ncu.py TAG "CONFIG NAME::report.ncu-rep" ..."""
 import csv
 import io
 import json
@@ -10,7 +10,7 @@ import sys
 tag = sys.argv[1]
 out = {"_source": f"profiles/{tag}_traffic.json from ncu --set full captures of the M4RM kernel"}
 for arg in sys.argv[2:]:
-    name, rep = arg.split("=", 1)
+    name, rep = arg.split("::", 1)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
