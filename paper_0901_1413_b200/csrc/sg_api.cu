@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <utility>
 
 #include "../../include/slicegemm_b200.h"
@@ -209,7 +210,29 @@ void field_costs(int f, double* lane_alu, double* lane_smem, double* entry_alu) 
   }
 }
 
+int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int device, Plan* out);
+
+// Plans are pure functions of the shape, the device and the overrides: cache them so repeated
+// products (the common case) skip the search (callers hold g_mu).
 int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Plan* out) {
+  typedef std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int, int, int, int> Key;
+  static std::map<Key, Plan> cache;
+  const Key key{field, m, l, n, std::min(k, 8), device, g_override_rt, g_override_splits, g_override_pipe,
+                g_override_threads, g_ablation};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return SG_OK;
+  }
+  const int rc = make_plan_uncached(field, m, l, n, k, device, out);
+  if (rc == SG_OK) {
+    if (cache.size() > 4096) cache.clear();
+    cache[key] = *out;
+  }
+  return rc;
+}
+
+int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int device, Plan* out) {
   DevState& ds = dev_state(device);
   const int K = std::min(k, 8);
   const int64_t wc32 = 2 * w64_of(n), wa32 = 2 * w64_of(l);
