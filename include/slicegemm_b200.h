@@ -149,8 +149,10 @@ int sg_m4rm_block(int field, uint64_t* const* C, int64_t c_words, const uint64_t
 /* Introspection and measurement. */
 int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta, int* splits,
             int* ctas, int* kernel_index, int* pipelined, int* threads);
-/* force rows per thread / k-splits / threads per CTA (0 = automatic) and the pipelined
- * schedule (-1 = automatic) */
+/* force rows per thread / k-splits / threads per CTA (0 = automatic) and the schedule
+ * (-1 = automatic; 0 serial, 1 pipelined, 2 warp-specialized).  splits = -1 forces the
+ * stream-K launch (one wave of CTAs over tile x k-block units + a compact reduction; k = 8
+ * only); sg_plan reports splits = -1 for a stream-K plan. */
 int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads);
 int sg_set_timing(int enable);                              /* event-time each internal launch */
 /* performance experiments only: select kernel variants with parts of the work removed

@@ -110,6 +110,9 @@ struct Plan {
   int64_t mpad = 0;
   int wa32 = 0, wc32 = 0;
   int at_words = 0, at_planes = 0;  // staged index array: k=8 packed words (1 plane), else A^T planes
+  bool streamk = false;              // one wave of CTAs over tiles x k-blocks (see m4rm_kernel)
+  int64_t units = 0, tiles = 0;
+  int slabs = 0, rows = 0;
   dim3 grid;
   double est_clk = 0;
 };
@@ -264,6 +267,36 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
     const Calib* cal = calib_for(ki);
     const int occ = std::max(1, ki->occupancy);
     const int max_splits = std::max(1, std::min(nblocks, 64));
+    const int64_t tiles = slabs * rgroups;
+    const int64_t units = tiles * nblocks;
+    {
+      // stream-K candidate: one wave of SMs x occupancy CTAs, each owning U / G consecutive
+      // (tile, k-block) units (<= SK_SEGS tile segments), then a compact reduction
+      const int64_t G = (int64_t)ds.sms * occ;
+      const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 &&
+                      (units + G - 1) / G <= 2 * (int64_t)nblocks - 1 && units >= G && tiles < G;
+      if (ok) {
+        const double per = (double)(units + G - 1) / G;
+        const double t_cta = cal ? per * cal->blk + 2.0 * cal->cta : 1.25 * (per * t_block + 6000.0);
+        const double bytes = (double)G * 2.0 * R * rows * 16.0 + (double)R * m * wc32 * 4.0;
+        // occ co-resident CTAs share the SM, as in the split-K estimate below
+        const double est = occ * t_cta + bytes / 3000.0 + 8000.0;
+        if (est < best.est_clk) {
+          best.est_clk = est;
+          best.ki = ki;
+          best.kernel_index = i;
+          best.splits = 1;
+          best.bps = nblocks;
+          best.mpad = rgroups * rows;
+          best.streamk = true;
+          best.units = units;
+          best.tiles = tiles;
+          best.slabs = (int)slabs;
+          best.rows = rows;
+          best.grid = dim3((unsigned)G, 1, 1);
+        }
+      }
+    }
     for (int sp = 1; sp <= max_splits; ++sp) {
       if (g_override_splits && sp != g_override_splits) continue;
       const int bps = (nblocks + sp - 1) / sp;
@@ -286,6 +319,7 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
         best.splits = splits;
         best.bps = bps;
         best.mpad = rgroups * rows;
+        best.streamk = false;
         best.grid = dim3((unsigned)slabs, (unsigned)rgroups, (unsigned)splits);
       }
     }
@@ -312,7 +346,8 @@ int64_t workspace_bytes_for(const Plan& p, int field) {
   const int R = planes(field);
   int64_t b = (int64_t)p.at_planes * p.at_words * p.mpad * 4;
   b = (b + 255) / 256 * 256;
-  if (p.splits > 1) b += (int64_t)p.splits * R * p.mpad * p.wc32 * 4;
+  if (p.streamk) b += (int64_t)p.grid.x * SK_SEGS * R * p.rows * SLAB_WORDS * 4;
+  else if (p.splits > 1) b += (int64_t)p.splits * R * p.mpad * p.wc32 * 4;
   return std::max<int64_t>(b, 256);
 }
 
@@ -482,7 +517,7 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
   rc = make_plan(field, m, l, n, k, dev, &p);
   if (rc != SG_OK) return rc;
   if (rows_per_cta) *rows_per_cta = p.ki->rt * p.ki->threads;
-  if (splits) *splits = p.splits;
+  if (splits) *splits = p.streamk ? -1 : p.splits;
   if (ctas) *ctas = (int)(p.grid.x * p.grid.y * p.grid.z);
   if (kernel_index) *kernel_index = p.kernel_index;
   if (pipelined) *pipelined = p.ki->sched;
@@ -518,7 +553,7 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   }
   uint32_t* AT = (uint32_t*)ws;
   int64_t at_bytes = ((int64_t)p.at_planes * p.at_words * p.mpad * 4 + 255) / 256 * 256;
-  uint32_t* partial = p.splits > 1 ? (uint32_t*)(ws + at_bytes) : nullptr;
+  uint32_t* partial = (p.splits > 1 || p.streamk) ? (uint32_t*)(ws + at_bytes) : nullptr;
 
   cudaEvent_t ev[4];
   if (g_timing)
@@ -540,10 +575,20 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   a.nblocks = p.nblocks;
   a.bps = p.bps;
   a.partial = p.splits > 1;
+  a.streamk = p.streamk;
+  a.units = p.units;
+  a.slabs = p.slabs;
+  a.P2 = p.streamk ? partial : nullptr;
+  if (p.streamk) a.C = (uint32_t*)C;
   SG_CUDA(launch_m4rm(*p.ki, a, p.grid, st), "sg_m4rm kernel");
   g_launches++;
   if (g_timing) cudaEventRecord(ev[2], st);
-  if (p.splits > 1) {
+  if (p.streamk) {
+    SG_CUDA(launch_reduce_streamk(field, partial, (uint32_t*)C, m, p.wc32, p.rows, p.slabs, p.tiles, p.nblocks,
+                                  p.units, (int)p.grid.x, st),
+            "sg_m4rm stream-K reduce");
+    g_launches++;
+  } else if (p.splits > 1) {
     SG_CUDA(launch_reduce_splits(field, partial, (uint32_t*)C, m, p.mpad, p.wc32, p.splits, st),
             "sg_m4rm reduce");
     g_launches++;
@@ -576,11 +621,11 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   // multiplied and chunk i-2's rows of C come down (three streams, events between them).
   // measured on B200 (tools/e2e_chunks.py): 2 chunks from 4096 rows, 4 from 16384
   int P = m >= 16384 ? 4 : (m >= 4096 ? 2 : 1);
-  if (const char* e = getenv("SG_HOST_CHUNKS")) P = std::max(1, std::min(4, atoi(e)));  // experiments
+  if (const char* e = getenv("SG_HOST_CHUNKS")) P = std::max(1, std::min(8, atoi(e)));  // experiments
   if (P > m) P = (int)std::max<int64_t>(1, m);
   struct Io {
     cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
-    cudaEvent_t ev_in[4], ev_comp[4];
+    cudaEvent_t ev_in[8], ev_comp[8];
     Buf buf;
   };
   static std::map<int, Io> io;
@@ -593,7 +638,7 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
       SG_CUDA(cudaStreamCreateWithFlags(&d->in, cudaStreamNonBlocking), "sg_m4rm_host stream");
       SG_CUDA(cudaStreamCreateWithFlags(&d->comp, cudaStreamNonBlocking), "sg_m4rm_host stream");
       SG_CUDA(cudaStreamCreateWithFlags(&d->out, cudaStreamNonBlocking), "sg_m4rm_host stream");
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 8; ++i) {
         SG_CUDA(cudaEventCreateWithFlags(&d->ev_in[i], cudaEventDisableTiming), "sg_m4rm_host event");
         SG_CUDA(cudaEventCreateWithFlags(&d->ev_comp[i], cudaEventDisableTiming), "sg_m4rm_host event");
       }

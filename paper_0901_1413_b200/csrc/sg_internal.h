@@ -35,7 +35,13 @@ struct M4rmArgs {
   int wa32, wc32;      // 32-bit words per row of A and of B/C
   int nblocks, bps;    // k-blocks in total, k-blocks per split
   int partial;         // 1: write raw partial sums (split-K), 0: canonical C
+  // stream-K (partial = 0): CTA c covers work units [c U / G, (c+1) U / G) of U = tiles x nblocks
+  int streamk;
+  int64_t units;
+  int slabs;           // tiles = slabs x row groups, tile t -> slab t % slabs, row group t / slabs
+  uint32_t* P2;        // compact stream-K partials [G * SK_SEGS][R][ROWS][4]
 };
+constexpr int SK_SEGS = 3;  // tile segments per stream-K CTA (the planner keeps U / G <= 2 nblocks)
 
 struct KernelInfo {
   void (*fn)(M4rmArgs);
@@ -58,6 +64,8 @@ cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st);
 cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int64_t m, int64_t mpad,
                                  int wc32, int splits, cudaStream_t st);
+cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,
+                                  int slabs, int64_t tiles, int nblocks, int64_t units, int ctas, cudaStream_t st);
 
 // sg_pack.cu
 cudaError_t launch_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld,

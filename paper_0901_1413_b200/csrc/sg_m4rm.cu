@@ -110,6 +110,60 @@ __global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict_
   }
 }
 
+// ------------------------------------------------------------------ stream-K reduction
+// C(tile t) = sum of the compact slots of the CTAs whose unit ranges intersect tile t's
+// [t nb, (t+1) nb), canonicalized.  One thread per (tile row, word); slots are summed in CTA
+// order (the field sums are exact, so any order gives the same bits).
+template <int F>
+__global__ void reduce_streamk_kernel(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m, int wc32,
+                                      int rows_cta, int slabs, int64_t tiles, int nb, int64_t U, int G) {
+  constexpr int R = Traits<F>::R;
+  const int64_t per_tile = (int64_t)rows_cta * SLAB_WORDS;
+  const int64_t total = tiles * per_tile;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / per_tile;
+    const int lr = (int)((i % per_tile) / SLAB_WORDS), w = (int)(i % SLAB_WORDS);
+    const int64_t row = (t / slabs) * rows_cta + lr;
+    const int word = (int)(t % slabs) * SLAB_WORDS + w;
+    if (row >= m || word >= wc32) continue;
+    const int64_t lo = t * nb, hi = lo + nb;
+    int64_t c = lo * G / U;
+    while (c > 0 && c * U / G > lo) --c;
+    while ((c + 1) * U / G <= lo) ++c;
+    V<F> acc;
+#pragma unroll
+    for (int d = 0; d < R; ++d) acc.p[d] = 0u;
+    for (; c < G && c * U / G < hi; ++c) {
+      const int64_t u0 = c * U / G;
+      if ((c + 1) * U / G == u0) continue;  // an empty range owns no slot
+      const int seg = (int)(t - u0 / nb);
+      const int64_t slot = c * SK_SEGS + seg;
+      V<F> x;
+#pragma unroll
+      for (int d = 0; d < R; ++d) x.p[d] = P2[((slot * R + d) * rows_cta + lr) * SLAB_WORDS + w];
+      vadd<F>(acc, x);
+    }
+    vcanon<F>(acc);
+#pragma unroll
+    for (int d = 0; d < R; ++d) C[(d * m + row) * (int64_t)wc32 + word] = acc.p[d];
+  }
+}
+
+cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,
+                                  int slabs, int64_t tiles, int nblocks, int64_t units, int ctas, cudaStream_t st) {
+  const int64_t total = tiles * rows_cta * SLAB_WORDS;
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+#define SG_RK(FF) reduce_streamk_kernel<FF><<<(unsigned)blocks, threads, 0, st>>>(P2, C, m, wc32, rows_cta, slabs, \
+                                                                                tiles, nblocks, units, ctas)
+  SG_FOR_EACH_FIELD_CASE(field, SG_RK)
+#undef SG_RK
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ registry
 int kernels_f2(KernelInfo** out);
 int kernels_f3(KernelInfo** out);

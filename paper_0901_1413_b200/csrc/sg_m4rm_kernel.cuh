@@ -167,8 +167,12 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 // builder threads of the warp-specialized schedules: SCHED 2 -> 4 warps, 3 -> 1 warp, 4 -> 2 warps
 __host__ __device__ constexpr int ws_builders(int sched) { return sched == 2 ? 128 : sched == 3 ? 32 : sched == 4 ? 64 : 0; }
 
-template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
-__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a) {
+// One segment: the CTA's slab (word0) x row group (row0) x k-blocks [s_begin, s_end), written to
+// C (mode 0), to split-K partial plane `slot` (mode 1) or to compact stream-K slot `slot` (mode 2).
+template <int F, int K, int RT, int SCHED, int NT, int ABL>
+__device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* smem, const int word0,
+                                             const int64_t row0, const int s_begin, const int s_end,
+                                             const int mode, const int slot) {
   constexpr bool PIPE = SCHED == 1;
   constexpr bool WS = SCHED >= 2;
   static_assert(!WS || K == 8, "the warp-specialized schedules are k = 8 only");
@@ -196,17 +200,12 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const 
   constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
   constexpr int CPT = COPIES / TPE;        // replicas written per thread
 
-  extern __shared__ __align__(128) unsigned char smem[];
   uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][R][E][COPIES] uint4
   u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][16][R][4]
   u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
 
   const int tid = threadIdx.x;
-  const int word0 = blockIdx.x * SLAB_WORDS;
-  const int64_t row0 = (int64_t)blockIdx.y * ROWS;
-  const int s_begin = blockIdx.z * a.bps;
-  const int s_end = min(a.nblocks, s_begin + a.bps);
   if (s_begin >= s_end) return;
 
   int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
@@ -523,10 +522,24 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const 
   }
 
   // ---- epilogue
+  if (mode == 2) {  // stream-K: compact slot [R][ROWS][4 words], canonical (summed by the reduce)
+    u32* out = a.P2 + (int64_t)slot * R * ROWS * 4;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int lr = t * NT + tid;
+      u32 o[4][R];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], true);
+#pragma unroll
+      for (int d = 0; d < R; ++d)
+        *reinterpret_cast<uint4*>(out + ((int64_t)d * ROWS + lr) * 4) = make_uint4(o[0][d], o[1][d], o[2][d], o[3][d]);
+    }
+    return;
+  }
   u32* out = a.C;
   int64_t rows_out = a.m;
-  if (a.partial) {
-    out += (int64_t)blockIdx.z * R * a.mpad * a.wc32;
+  if (mode == 1) {
+    out += (int64_t)slot * R * a.mpad * a.wc32;
     rows_out = a.mpad;
   }
 #pragma unroll
@@ -535,7 +548,7 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const 
     if (row < a.m) {
       u32 o[4][R];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], !a.partial);
+      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], mode == 0);
 #pragma unroll
       for (int d = 0; d < R; ++d) {
         u32* dst = out + ((int64_t)d * rows_out + row) * a.wc32 + word0;
@@ -543,6 +556,35 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const 
         if (word0 + 2 < a.wc32) *reinterpret_cast<uint2*>(dst + 2) = make_uint2(o[2][d], o[3][d]);
       }
     }
+  }
+}
+
+// Stream-K: CTA c owns work units [c U / G, (c+1) U / G) of U = tiles x k-blocks, i.e. at most
+// SK_SEGS tile segments; each lands in compact slot c * SK_SEGS + segment and reduce_streamk sums
+// the slots of every tile.  Otherwise one segment per CTA: (slab, row group, k-split) = blockIdx.
+template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
+__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int ROWS = RT * NT;
+  if (!a.streamk) {
+    const int s_begin = blockIdx.z * a.bps;
+    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS, s_begin,
+                                           min(a.nblocks, s_begin + a.bps), a.partial ? 1 : 0, blockIdx.z);
+    return;
+  }
+  const int64_t U = a.units, G = gridDim.x;
+  int64_t u = blockIdx.x * U / G;
+  const int64_t u1 = (blockIdx.x + 1) * U / G;
+  for (int seg = 0; u < u1 && seg < SK_SEGS; ++seg) {
+    const int64_t tile = u / a.nblocks;
+    const int s0 = (int)(u - tile * a.nblocks);
+    const int64_t room = u1 - u;
+    const int s1 = (int)(s0 + room < a.nblocks ? s0 + room : (int64_t)a.nblocks);
+    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, smem, (int)(tile % a.slabs) * SLAB_WORDS, (tile / a.slabs) * ROWS, s0,
+                                           s1, 2, blockIdx.x * SK_SEGS + seg);
+    u += s1 - s0;
+    cp_async_wait<0>();
+    __syncthreads();  // shared memory is reused by the next segment
   }
 }
 

@@ -138,6 +138,31 @@ def test_every_compiled_plan(fname):  # noqa: F811
 
 
 @pytest.mark.parametrize("fname", list(FIELDS))
+def test_streamk_forced(fname):
+    """Stream-K (splits = -1): CTA ranges that start and end mid-tile and span up to three tiles,
+    every schedule and CTA shape, ragged m / l / n; bit-identical to the oracle."""
+    ran = 0
+    for (m, l, n) in [(700, 1000, 777), (3000, 64, 1000), (1111, 333, 200), (257, 2500, 129)]:
+        A = oracle.random_dense(fname, m, l, m + l)
+        B = oracle.random_dense(fname, l, n, n + 3)
+        want = expect(fname, A, B)
+        for rt in (1, 2, 4, 8, 16):
+            for pipe in (0, 1, 2):
+                for nt in (256, 512):
+                    m4rm_mod.set_plan_override(rt, -1, pipe, nt)
+                    try:
+                        C = gpu_multiply(fname, A, B)
+                    except RuntimeError as e:
+                        assert "no compiled" in str(e)
+                        continue
+                    assert m4rm_mod.plan(fname, m, l, n)["splits"] == -1
+                    ran += 1
+                    assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, rt, pipe, nt)
+    m4rm_mod.set_plan_override()
+    assert ran >= 12
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
 def test_general_k_pipelined_straddle(fname):
     """k = 5 (blocks straddle 32-bit words) through the pipelined schedule."""
     A = oracle.random_dense(fname, 300, 333, 17)
