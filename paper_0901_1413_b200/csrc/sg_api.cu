@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -617,33 +618,47 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   const int R = planes(field);
   const int64_t wa = w64_of(l), wc = w64_of(n);
   const size_t a_bytes = (size_t)R * m * wa * 8, b_bytes = (size_t)R * l * wc * 8, c_bytes = (size_t)R * m * wc * 8;
-  // Row-chunked pipeline: B goes up first, then chunk i's rows of A go up while chunk i-1 is
-  // multiplied and chunk i-2's rows of C come down (three streams, events between them).
-  // measured on B200 (tools/e2e_chunks.py): 2 chunks from 4096 rows, 4 from 16384
-  int P = m >= 16384 ? 4 : (m >= 4096 ? 2 : 1);
-  if (const char* e = getenv("SG_HOST_CHUNKS")) P = std::max(1, std::min(8, atoi(e)));  // experiments
-  if (P > m) P = (int)std::max<int64_t>(1, m);
+  // Pipeline over three streams (H2D, compute, D2H), measured on B200 (tools/e2e_chunks.py):
+  //  * the inner dimension is cut into Pk word-aligned chunks: the multiply of chunk j (A's
+  //    columns and B's rows of that chunk) starts as soon as that chunk is up, instead of after
+  //    all of B;
+  //  * the last chunk's product is cut into Pr row pieces: once piece r is done, the chunk
+  //    partials of those rows are summed (canonical) and piece r goes down while r+1 computes.
+  // Field sums are exact and F5 / F7 results canonical, so any chunking gives the same bits.
+  const size_t io = a_bytes + b_bytes;
+  // (B200, profiles/r01c_e2e_chunks.txt: F5 4096 best 1x2, GF(4) 8192 4x2, F7 16384x8192 4x4;
+  // every product carries ~30 us of fixed cost, so small ones are not cut on k)
+  int Pk = io >= ((size_t)24 << 20) ? 4 : 1;
+  int Pr = c_bytes >= ((size_t)64 << 20) ? 4 : (c_bytes >= ((size_t)1 << 20) ? 2 : 1);
+  if (const char* e = getenv("SG_HOST_KCHUNKS")) Pk = std::max(1, std::min(4, atoi(e)));  // experiments
+  if (const char* e = getenv("SG_HOST_CHUNKS")) Pr = std::max(1, std::min(4, atoi(e)));
+  Pk = (int)std::max<int64_t>(1, std::min<int64_t>(Pk, wa));  // chunks of whole 64-column words
+  Pr = (int)std::max<int64_t>(1, std::min<int64_t>(Pr, m));
+  if (l == 0) Pk = 1;
   struct Io {
     cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
-    cudaEvent_t ev_in[8], ev_comp[8];
+    cudaEvent_t ev_in[8], ev_comp[4];
     Buf buf;
   };
-  static std::map<int, Io> io;
+  static std::map<int, Io> io_state;
   Io* d;
   char* dbuf = nullptr;
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  // device layout: B chunks | A chunks (last one as row pieces) | chunk partials | last-chunk
+  // pieces | C
+  const size_t need = b_bytes + a_bytes + (size_t)(Pk - 1) * c_bytes + (Pk > 1 ? c_bytes : 0) + c_bytes + 32 * 256;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    d = &io[device];
+    d = &io_state[device];
     if (!d->in) {
       SG_CUDA(cudaStreamCreateWithFlags(&d->in, cudaStreamNonBlocking), "sg_m4rm_host stream");
       SG_CUDA(cudaStreamCreateWithFlags(&d->comp, cudaStreamNonBlocking), "sg_m4rm_host stream");
       SG_CUDA(cudaStreamCreateWithFlags(&d->out, cudaStreamNonBlocking), "sg_m4rm_host stream");
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 8; ++i)
         SG_CUDA(cudaEventCreateWithFlags(&d->ev_in[i], cudaEventDisableTiming), "sg_m4rm_host event");
+      for (int i = 0; i < 4; ++i)
         SG_CUDA(cudaEventCreateWithFlags(&d->ev_comp[i], cudaEventDisableTiming), "sg_m4rm_host event");
-      }
     }
-    const size_t need = a_bytes + b_bytes + c_bytes + 16 * 256;
     if (d->buf.bytes < need) {
       if (d->buf.p) {
         cudaDeviceSynchronize();
@@ -656,34 +671,132 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
     }
     dbuf = (char*)d->buf.p;
   }
-  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  uint64_t* dB = (uint64_t*)dbuf;
-  char* cur = dbuf + up(b_bytes);
-  if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, d->in), "sg_m4rm_host H2D B");
-  for (int i = 0; i < P; ++i) {
-    const int64_t r0 = m * i / P, r1 = m * (i + 1) / P, rows = r1 - r0;
-    uint64_t* dA = (uint64_t*)cur;
-    cur += up((size_t)R * rows * wa * 8);
-    uint64_t* dC = (uint64_t*)cur;
-    cur += up((size_t)R * rows * wc * 8);
-    if (rows == 0) continue;
-    // this chunk's rows of every plane of A: R rows of rows*wa words, pitch m*wa
-    if (wa)
-      SG_CUDA(cudaMemcpy2DAsync(dA, rows * wa * 8, A + r0 * wa, m * wa * 8, rows * wa * 8, R, cudaMemcpyHostToDevice,
-                                d->in),
+  // SG_HOST_TRACE=1 (experiments): event timestamps of every pipeline step on stderr
+  static const bool trace = getenv("SG_HOST_TRACE") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  cudaEvent_t t0 = nullptr;
+  if (trace) {
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, d->in);
+  }
+  auto mark = [&](const char* what, cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.push_back({what, e});
+  };
+  char* cur = dbuf;
+  auto take = [&](size_t bytes) {
+    char* p = cur;
+    cur += up(bytes);
+    return (uint64_t*)p;
+  };
+  auto wcut = [&](int j) { return wa * j / Pk; };  // chunk j = words [wcut(j), wcut(j+1)) of A's rows
+  auto rcut = [&](int r) { return m * r / Pr; };
+  // ---- uploads: B rows and A columns of chunk j (j < Pk-1), then the last chunk by row pieces
+  uint64_t* dB[4];
+  uint64_t* dA[4];
+  uint64_t* dAp[4];
+  for (int j = 0; j < Pk; ++j) {
+    const int64_t w0 = wcut(j), w1 = wcut(j + 1);
+    const int64_t r0 = std::min(l, w0 * 64), r1 = j == Pk - 1 ? l : std::min(l, w1 * 64);  // B rows
+    dB[j] = take((size_t)R * (r1 - r0) * wc * 8);
+    if (r1 > r0)
+      SG_CUDA(cudaMemcpy2DAsync(dB[j], (r1 - r0) * wc * 8, B + r0 * wc, l * wc * 8, (r1 - r0) * wc * 8, R,
+                                cudaMemcpyHostToDevice, d->in),
+              "sg_m4rm_host H2D B");
+    if (j < Pk - 1) {
+      dA[j] = take((size_t)R * m * (w1 - w0) * 8);
+      // all R*m rows share the pitch wa: one 2D copy of the column range
+      SG_CUDA(cudaMemcpy2DAsync(dA[j], (w1 - w0) * 8, A + w0, wa * 8, (w1 - w0) * 8, (size_t)R * m,
+                                cudaMemcpyHostToDevice, d->in),
               "sg_m4rm_host H2D A");
-    SG_CUDA(cudaEventRecord(d->ev_in[i], d->in), "sg_m4rm_host event");
-    SG_CUDA(cudaStreamWaitEvent(d->comp, d->ev_in[i], 0), "sg_m4rm_host wait");
-    rc = sg_m4rm(field, dA, dB, dC, rows, l, n, k, nullptr, 0, d->comp);
+      mark("in: chunk up", d->in);
+      SG_CUDA(cudaEventRecord(d->ev_in[j], d->in), "sg_m4rm_host event");
+    } else {
+      for (int r = 0; r < Pr; ++r) {
+        const int64_t q0 = rcut(r), q1 = rcut(r + 1);
+        dAp[r] = take((size_t)R * (q1 - q0) * (w1 - w0) * 8);
+        if (q1 > q0 && w1 > w0)
+          for (int p = 0; p < R; ++p)
+            SG_CUDA(cudaMemcpy2DAsync(dAp[r] + (int64_t)p * (q1 - q0) * (w1 - w0), (w1 - w0) * 8,
+                                      A + ((int64_t)p * m + q0) * wa + w0, wa * 8, (w1 - w0) * 8, q1 - q0,
+                                      cudaMemcpyHostToDevice, d->in),
+                    "sg_m4rm_host H2D A");
+        mark("in: last-chunk piece up", d->in);
+        SG_CUDA(cudaEventRecord(d->ev_in[Pk - 1 + r], d->in), "sg_m4rm_host event");
+      }
+    }
+  }
+  // ---- products: chunk partials S_j over all rows, then the last chunk piece by piece
+  uint64_t* S[4];
+  for (int j = 0; j + 1 < Pk; ++j) S[j] = take(c_bytes);
+  uint64_t* L = Pk > 1 ? take(c_bytes) : nullptr;  // last-chunk pieces, each [R][rows][wc]
+  uint64_t* dC = take(c_bytes);                     // final C, [R][m][wc]
+  for (int j = 0; j + 1 < Pk; ++j) {
+    const int64_t w0 = wcut(j), w1 = wcut(j + 1);
+    SG_CUDA(cudaStreamWaitEvent(d->comp, d->ev_in[j], 0), "sg_m4rm_host wait");
+    rc = sg_m4rm(field, dA[j], dB[j], S[j], m, std::min(l, w1 * 64) - w0 * 64, n, k, nullptr, 0, d->comp);
     if (rc != SG_OK) return rc;
-    SG_CUDA(cudaEventRecord(d->ev_comp[i], d->comp), "sg_m4rm_host event");
-    SG_CUDA(cudaStreamWaitEvent(d->out, d->ev_comp[i], 0), "sg_m4rm_host wait");
-    SG_CUDA(cudaMemcpy2DAsync(C + r0 * wc, m * wc * 8, dC, rows * wc * 8, rows * wc * 8, R, cudaMemcpyDeviceToHost,
-                              d->out),
-            "sg_m4rm_host D2H C");
+    mark("comp: chunk product", d->comp);
+  }
+  const int64_t lw0 = wcut(Pk - 1) * 64, l_last = l - std::min(l, lw0);
+  uint64_t* Lcur = L;
+  for (int r = 0; r < Pr; ++r) {
+    const int64_t q0 = rcut(r), q1 = rcut(r + 1), rows = q1 - q0;
+    SG_CUDA(cudaStreamWaitEvent(d->comp, d->ev_in[Pk - 1 + r], 0), "sg_m4rm_host wait");
+    if (rows > 0) {
+      if (Pk == 1) {
+        // no chunk partials: the piece lands in C directly (rows q0.. of every plane)
+        uint64_t* piece = dC + (int64_t)R * q0 * wc;  // pieces packed back to back, each [R][rows][wc]
+        rc = sg_m4rm(field, dAp[r], dB[0], piece, rows, l, n, k, nullptr, 0, d->comp);
+        if (rc != SG_OK) return rc;
+        mark("comp: piece product", d->comp);
+        SG_CUDA(cudaEventRecord(d->ev_comp[r], d->comp), "sg_m4rm_host event");
+        SG_CUDA(cudaStreamWaitEvent(d->out, d->ev_comp[r], 0), "sg_m4rm_host wait");
+        SG_CUDA(cudaMemcpy2DAsync(C + q0 * wc, m * wc * 8, piece, rows * wc * 8, rows * wc * 8, R,
+                                  cudaMemcpyDeviceToHost, d->out),
+                "sg_m4rm_host D2H C");
+        mark("out: piece down", d->out);
+        continue;
+      }
+      rc = sg_m4rm(field, dAp[r], dB[Pk - 1], Lcur, rows, l_last, n, k, nullptr, 0, d->comp);
+      if (rc != SG_OK) return rc;
+      SliceSet ss;
+      ss.n = Pk;
+      for (int j = 0; j + 1 < Pk; ++j) {
+        ss.base[j] = (const uint32_t*)(S[j] + q0 * wc);
+        ss.pstride[j] = 2 * m * wc;
+      }
+      ss.base[Pk - 1] = (const uint32_t*)Lcur;
+      ss.pstride[Pk - 1] = 2 * rows * wc;
+      SG_CUDA(launch_sum_slices(field, ss, (uint32_t*)(dC + q0 * wc), 2 * m * wc, rows, (int)(2 * wc), d->comp),
+              "sg_m4rm_host chunk sum");
+      g_launches++;
+      mark("comp: piece product + sum", d->comp);
+      SG_CUDA(cudaEventRecord(d->ev_comp[r], d->comp), "sg_m4rm_host event");
+      SG_CUDA(cudaStreamWaitEvent(d->out, d->ev_comp[r], 0), "sg_m4rm_host wait");
+      SG_CUDA(cudaMemcpy2DAsync(C + q0 * wc, m * wc * 8, dC + q0 * wc, m * wc * 8, rows * wc * 8, R,
+                                cudaMemcpyDeviceToHost, d->out),
+              "sg_m4rm_host D2H C");
+      mark("out: piece down", d->out);
+      Lcur += (int64_t)R * rows * wc;
+    }
   }
   SG_CUDA(cudaStreamSynchronize(d->out), "sg_m4rm_host sync");
   SG_CUDA(cudaStreamSynchronize(d->comp), "sg_m4rm_host sync");
+  SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host sync");
+  if (trace) {
+    fprintf(stderr, "sg_m4rm_host trace Pk=%d Pr=%d\n", Pk, Pr);
+    for (auto& mk : marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t0, mk.second);
+      fprintf(stderr, "  %8.3f ms  %s\n", ms, mk.first);
+      cudaEventDestroy(mk.second);
+    }
+    cudaEventDestroy(t0);
+  }
   return SG_OK;
 }
 

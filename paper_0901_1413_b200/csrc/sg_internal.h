@@ -62,6 +62,15 @@ KernelInfo* m4rm_kernel_at(int i);
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
                                int wa32, int nwords, cudaStream_t st);
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st);
+// up to SLICES_MAX equally shaped R-plane row slices with their own plane strides (u32 words)
+constexpr int SLICES_MAX = 8;
+struct SliceSet {
+  const uint32_t* base[SLICES_MAX];
+  int64_t pstride[SLICES_MAX];
+  int n;
+};
+cudaError_t launch_sum_slices(int field, const SliceSet& s, uint32_t* out, int64_t out_pstride, int64_t rows,
+                              int wc32, cudaStream_t st);
 cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int64_t m, int64_t mpad,
                                  int wc32, int splits, cudaStream_t st);
 cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,

@@ -110,6 +110,44 @@ __global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict_
   }
 }
 
+// ------------------------------------------------------------------ slice sums (host pipeline)
+// out rows = sum over the n slices (each canonical or raw field values, R planes of `rows` x wc32
+// words at base[i] with plane stride pstride[i] words), canonicalized.
+template <int F>
+__global__ void sum_slices_kernel(const SliceSet s, u32* __restrict__ out, int64_t out_pstride, int64_t rows,
+                                  int wc32) {
+  constexpr int R = Traits<F>::R;
+  const int64_t total = rows * wc32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    V<F> acc;
+#pragma unroll
+    for (int d = 0; d < R; ++d) acc.p[d] = s.base[0][d * s.pstride[0] + i];
+    for (int j = 1; j < s.n; ++j) {
+      V<F> x;
+#pragma unroll
+      for (int d = 0; d < R; ++d) x.p[d] = s.base[j][d * s.pstride[j] + i];
+      vadd<F>(acc, x);
+    }
+    vcanon<F>(acc);
+#pragma unroll
+    for (int d = 0; d < R; ++d) out[d * out_pstride + i] = acc.p[d];
+  }
+}
+
+cudaError_t launch_sum_slices(int field, const SliceSet& s, uint32_t* out, int64_t out_pstride, int64_t rows,
+                              int wc32, cudaStream_t st) {
+  const int64_t total = rows * wc32;
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+#define SG_SS(FF) sum_slices_kernel<FF><<<(unsigned)blocks, threads, 0, st>>>(s, out, out_pstride, rows, wc32)
+  SG_FOR_EACH_FIELD_CASE(field, SG_SS)
+#undef SG_SS
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ stream-K reduction
 // C(tile t) = sum of the compact slots of the CTAs whose unit ranges intersect tile t's
 // [t nb, (t+1) nb), canonicalized.  One thread per (tile row, word); slots are summed in CTA

@@ -2,6 +2,8 @@
 golden outputs.  Bar: bit-exact planes (F5/F7 outputs are canonical, compared against the
 canonicalized reference)."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -223,7 +225,8 @@ def test_host_buffers_e2e_path():
 
 
 def test_host_buffers_pipelined_chunks():
-    """m >= 4096 runs sg_m4rm_host's row-chunked copy/compute pipeline (2..4 chunks)."""
+    """sg_m4rm_host's pipeline: the default chunking at m >= 4096, and every (k-chunks, row
+    pieces) pair forced through SG_HOST_KCHUNKS / SG_HOST_CHUNKS on ragged shapes."""
     for fname, m in (("f7", 5000), ("f3", 9001)):
         A = oracle.random_dense(fname, m, 300, 5)
         B = oracle.random_dense(fname, 300, 200, 6)
@@ -231,6 +234,22 @@ def test_host_buffers_pipelined_chunks():
         Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), 200, device="cpu")
         C = sg.m4rm_multiply(Ah, Bh)
         assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
+    try:
+        for fname in FIELDS:
+            for (m, l, n) in ((600, 1000, 200), (7, 129, 65), (300, 64, 100), (333, 65, 7)):
+                A = oracle.random_dense(fname, m, l, m + n)
+                B = oracle.random_dense(fname, l, n, l + 1)
+                want = expect(fname, A, B)
+                Ah = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, A), l, device="cpu")
+                Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), n, device="cpu")
+                for pk in (1, 2, 3, 4):
+                    for pr in (1, 3, 4):
+                        os.environ["SG_HOST_KCHUNKS"], os.environ["SG_HOST_CHUNKS"] = str(pk), str(pr)
+                        C = sg.m4rm_multiply(Ah, Bh)
+                        assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, pk, pr)
+    finally:
+        os.environ.pop("SG_HOST_KCHUNKS", None)
+        os.environ.pop("SG_HOST_CHUNKS", None)
 
 
 def test_elementwise_ops_match_dense():

@@ -1,6 +1,6 @@
 """e2e experiments for sg_m4rm_host: chunk count sweep, copy-only bandwidth, per-chunk compute.
 
-python tools/e2e_chunks.py [--configs 1,2,3] [--chunks 1,2,3,4,6,8]"""
+python tools/e2e_chunks.py [--configs 1,2,3] [--chunks 1:1,2:2,4:4]   (k-chunks:row pieces)"""
 import argparse
 import os
 import subprocess
@@ -9,12 +9,14 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="1,2,3")
-ap.add_argument("--chunks", default="1,2,3,4,6,8")
+ap.add_argument("--chunks", default="1:1,1:2,1:4,2:2,2:4,4:2,4:4,3:4")
 a = ap.parse_args()
 for P in a.chunks.split(","):
+    PK, PR = P.split(":")
     out = subprocess.run([sys.executable, "-c", f"""
 import os, sys, time, ctypes, torch
-os.environ['SG_HOST_CHUNKS'] = '{P}'
+os.environ['SG_HOST_KCHUNKS'] = '{PK}'
+os.environ['SG_HOST_CHUNKS'] = '{PR}'
 sys.path.insert(0, '.')
 import bench
 import paper_0901_1413_b200 as sg
@@ -32,7 +34,7 @@ for ci in ({a.configs},):
     for _ in range(5):
         t0 = time.perf_counter(); L.sg_m4rm_host(f.code, vp(Ah), vp(Bh), vp(Ch), m, l, n, 8, 0); ts.append(time.perf_counter() - t0)
     extra = ''
-    if {P} == 1:
+    if '{P}' == '1:1':
         d = torch.empty_like(Ah, device=dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
