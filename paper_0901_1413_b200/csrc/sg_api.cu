@@ -576,6 +576,7 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   a.nblocks = p.nblocks;
   a.bps = p.bps;
   a.partial = p.splits > 1;
+  a.early_trigger = pdl_mode() == 2;
   a.streamk = p.streamk;
   a.units = p.units;
   a.slabs = p.slabs;

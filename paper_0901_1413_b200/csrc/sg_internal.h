@@ -1,9 +1,33 @@
 // sg_internal.h -- launch-level interfaces shared by the .cu translation units.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace sg {
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may start (prologue, smem
+// carve-out, launch latency) while its predecessor on the stream drains; it must call pdl_wait()
+// before touching memory the predecessor writes.  Predecessors call pdl_trigger() to let it in.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// SG_PDL (experiments): 0 plain launches, 1 PDL (default)
+int pdl_mode();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_mode() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // X(F) for every supported field (F2, F3, F5, F7, GF4, GF8, Z4, Z8), used to dispatch runtime
 // field codes to template instantiations.
@@ -40,6 +64,7 @@ struct M4rmArgs {
   int64_t units;
   int slabs;           // tiles = slabs x row groups, tile t -> slab t % slabs, row group t / slabs
   uint32_t* P2;        // compact stream-K partials [G * SK_SEGS][R][ROWS][4]
+  int early_trigger;   // experiments (SG_PDL=2): release the dependent reduction at kernel start
 };
 constexpr int SK_SEGS = 3;  // tile segments per stream-K CTA (the planner keeps U / G <= 2 nblocks)
 

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // sg_m4rm.cu -- pre-pass, split-K reduction and launch glue around the M4RM kernel
 // (kernel template: sg_m4rm_kernel.cuh; per-field instantiations: sg_m4rm_<field>.cu).
 #include <vector>
@@ -12,6 +13,7 @@ namespace sg {
 __global__ void transpose_a_kernel(const u32* __restrict__ A, u32* __restrict__ AT, int64_t m,
                                    int64_t mpad, int wa32, int f3) {
   __shared__ u32 tile[32][33];
+  pdl_trigger();
   const int d = blockIdx.z;
   const int64_t rbase = (int64_t)blockIdx.y * 32;
   const int wbase = blockIdx.x * 32;
@@ -47,6 +49,7 @@ __global__ void index_words_kernel(const u32* __restrict__ A, u32* __restrict__ 
   constexpr int R = Traits<F>::R, NI = Traits<F>::NI;
   constexpr int NIP = NI == 3 ? 4 : NI, RPW = 4 / NIP;
   __shared__ u32 tile[R][32][33];
+  pdl_trigger();  // the product kernel may launch now; it waits for this grid before reading IW
   const int64_t rbase = (int64_t)blockIdx.y * 32;
   const int wbase = blockIdx.x * 32;  // A words wbase.. (= k-blocks 4*wbase ..)
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -89,6 +92,7 @@ template <int F>
 __global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict__ C, int64_t m,
                                      int64_t mpad, int wc32, int splits) {
   constexpr int R = Traits<F>::R;
+  pdl_wait();  // launched with PDL behind the product kernel
   const int64_t total = m * wc32;
   const int64_t plane = mpad * (int64_t)wc32;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -156,6 +160,7 @@ template <int F>
 __global__ void reduce_streamk_kernel(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m, int wc32,
                                       int rows_cta, int slabs, int64_t tiles, int nb, int64_t U, int G) {
   constexpr int R = Traits<F>::R;
+  pdl_wait();  // launched with PDL behind the product kernel
   const int64_t per_tile = (int64_t)rows_cta * SLAB_WORDS;
   const int64_t total = tiles * per_tile;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -195,8 +200,8 @@ cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, in
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-#define SG_RK(FF) reduce_streamk_kernel<FF><<<(unsigned)blocks, threads, 0, st>>>(P2, C, m, wc32, rows_cta, slabs, \
-                                                                                tiles, nblocks, units, ctas)
+#define SG_RK(FF) return launch_pdl(reduce_streamk_kernel<FF>, dim3((unsigned)blocks), dim3(threads), 0, st, P2, C, m, \
+                                 wc32, rows_cta, slabs, tiles, nblocks, units, ctas)
   SG_FOR_EACH_FIELD_CASE(field, SG_RK)
 #undef SG_RK
   return cudaGetLastError();
@@ -225,11 +230,18 @@ static std::vector<KernelInfo*>& registry() {
   return all;
 }
 
+int pdl_mode() {
+  static const int mode = [] {
+    const char* e = getenv("SG_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return mode;
+}
+
 int m4rm_kernel_count() { return (int)registry().size(); }
 KernelInfo* m4rm_kernel_at(int i) { return registry()[i]; }
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st) {
-  ki.fn<<<grid, ki.launch_threads, ki.smem_bytes, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(ki.fn, grid, dim3(ki.launch_threads), ki.smem_bytes, st, a);
 }
 
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
@@ -254,7 +266,8 @@ cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int6
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-#define SG_RS(FF) reduce_splits_kernel<FF><<<(unsigned)blocks, threads, 0, st>>>(P, C, m, mpad, wc32, splits)
+#define SG_RS(FF) return launch_pdl(reduce_splits_kernel<FF>, dim3((unsigned)blocks), dim3(threads), 0, st, P, C, m, mpad, \
+                                 wc32, splits)
   SG_FOR_EACH_FIELD_CASE(field, SG_RS)
 #undef SG_RS
   return cudaGetLastError();

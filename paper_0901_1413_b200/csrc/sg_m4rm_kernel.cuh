@@ -566,6 +566,8 @@ template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
 __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ROWS = RT * NT;
+  if (a.early_trigger) pdl_trigger();
+  pdl_wait();  // launched with PDL behind the index pre-pass: wait for its writes
   if (!a.streamk) {
     const int s_begin = blockIdx.z * a.bps;
     m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS, s_begin,
