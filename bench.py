@@ -156,10 +156,14 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     params = sg.M4rmParams(8)
 
+    from paper_0901_1413_b200 import dist as sgdist
+    chunks = sgdist.default_chunks(f, l, n)
+
     def step():
-        if world > 1:
-            dist.broadcast(B.planes, src=0)
-        sg.m4rm_multiply(A, B, params, out=C)
+        if world > 1:  # B broadcast from rank 0 in row blocks, overlapped with the chunk products
+            sgdist.sharded_multiply(A, B if rank == 0 else None, f, l, n, src=0, chunks=chunks, return_b=False)
+        else:
+            sg.m4rm_multiply(A, B, params, out=C)
 
     for _ in range(args.warmup):
         step()
@@ -275,11 +279,14 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
         if world == 1:
             _lib.check(L.sg_m4rm_host(f.code, vp(Ah), vp(Bh), vp(Ch), m, l, n, 8, dev))
             return
+        from paper_0901_1413_b200 import dist as sgdist
+        Bm = None
         if rank == 0:
             Bd.copy_(Bh, non_blocking=True)
-        dist.broadcast(Bd, src=0)
+            Bm = sg.BitslicedMatrix(f, l, n, Bd)
         Ad = Ah.to(device, non_blocking=True)
-        C = sg.m4rm_multiply(sg.BitslicedMatrix(f, m, l, Ad), sg.BitslicedMatrix(f, l, n, Bd), sg.M4rmParams(8))
+        C, _ = sgdist.sharded_multiply(sg.BitslicedMatrix(f, m, l, Ad), Bm, f, l, n, src=0,
+                                       chunks=sgdist.default_chunks(f, l, n), return_b=False)
         Ch.copy_(C.planes, non_blocking=True)
         torch.cuda.synchronize()
 
@@ -300,8 +307,8 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8),
             "path": ("sg_m4rm_host (C ABI; pinned host planes; H2D, multiply, D2H pipelined in row chunks)"
-                     if world == 1 else "rank-0 H2D of B + NCCL broadcast, per-rank H2D of A rows, "
-                     "m4rm_multiply, D2H of C rows (wall clock, max over ranks)")}
+                     if world == 1 else "rank-0 H2D of B + broadcast in row blocks overlapped with the chunk products "
+                     "(dist.sharded_multiply), per-rank H2D of A rows, D2H of C rows (wall clock, max over ranks)")}
 
 
 # ----------------------------------------------------------------------------- CPU (oracle port)
@@ -399,11 +406,19 @@ def main():
     if args.warmup < 3:
         log("warning: the contract needs >= 3 warm-up steps; using 3")
         args.warmup = 3
+    # SG_BENCH_BACKEND=gloo: functional check of the N > 1 code path on a one-GPU box (ranks share
+    # cuda:0, collectives through gloo); its numbers are not measurements.
+    backend = os.environ.get("SG_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     pk = M.probe_peaks(local)
     peaks = {"lop3_per_clk_per_sm": pk["lop3_per_clk_per_sm"], "lds_bytes_per_clk_per_sm": pk["lds_bytes_per_clk_per_sm"],
@@ -436,11 +451,14 @@ def main():
         name, field, m, l, n = head
         line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bitsliced boolean words)",
+                "scaling": res["scaling"] if world > 1 else "weak", "vs_baseline": None,
+                "dtype": "u32 (bitsliced boolean words)",
                 "data": "synthetic (seeded uniform residues, torch.randint on device)",
-                "config": {"workload": name, "field": field, "m_per_gpu": m, "l": l, "n": n, "k": 8,
-                           "parallelism": (f"rows of A/C sharded over {world} GPUs, B broadcast from rank 0 by NCCL "
-                                           "inside every step" if world > 1 else "1 GPU"),
+                "config": {"workload": name, "field": field, "m_per_gpu": res["m_per_gpu"], "m_total":
+                           m * world if res["scaling"] == "weak" else m, "l": l, "n": n, "k": 8,
+                           "parallelism": (f"rows of A/C sharded over {world} GPUs, B broadcast from rank 0 by "
+                                           f"{backend.upper()} inside every step (row blocks overlapped with the "
+                                           "chunk products)" if world > 1 else "1 GPU"),
                            "l2": "flushed (256 MiB write) before every timed step"},
                 "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
                 "roofline": res["roofline"], "plan": res["plan"], "cpu_baseline": cpu,

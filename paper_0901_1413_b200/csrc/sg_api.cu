@@ -275,7 +275,7 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       // (tile, k-block) units (<= SK_SEGS tile segments), then a compact reduction
       const int64_t G = (int64_t)ds.sms * occ;
       const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 &&
-                      (units + G - 1) / G <= 2 * (int64_t)nblocks - 1 && units >= G && tiles < G;
+                      (units + G - 1) / G <= 2 * (int64_t)nblocks - 1 && units >= G;
       if (ok) {
         const double per = (double)(units + G - 1) / G;
         const double t_cta = cal ? per * cal->blk + 2.0 * cal->cta : 1.25 * (per * t_block + 6000.0);

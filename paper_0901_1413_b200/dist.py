@@ -45,15 +45,63 @@ def broadcast_matrix(B: BitslicedMatrix, field, nrows: int, ncols: int, src: int
     return BitslicedMatrix(field, nrows, ncols, t)
 
 
+def b_chunks(l: int, chunks: int) -> list:
+    """Word-aligned row ranges [(r0, r1)] of B (= k-chunks of the inner dimension)."""
+    w = (l + 63) // 64
+    chunks = max(1, min(chunks, w)) if l else 1
+    cuts = [min(l, 64 * (w * j // chunks)) for j in range(chunks)] + [l]
+    return [(cuts[j], cuts[j + 1]) for j in range(chunks)]
+
+
+def default_chunks(field, l: int, n: int) -> int:
+    """Overlap the broadcast with the products when B is big enough for it to matter."""
+    return 4 if field.bits * l * ((n + 63) // 64) * 8 >= (16 << 20) else 1
+
+
 def sharded_multiply(A_shard: BitslicedMatrix, B: BitslicedMatrix, field, l: int, n: int, src: int = 0,
-                     group=None, multiply=None, device=None):
-    """C_shard = A_shard * B with B broadcast from `src`.  Returns (C_shard, B_local)."""
+                     group=None, multiply=None, device=None, chunks: int = 1, add=None, return_b: bool = True):
+    """C_shard = A_shard * B with B broadcast from `src`.  Returns (C_shard, B_local).
+
+    chunks > 1 overlaps the broadcast with the products (SURVEY.md 8e "optional fusion"): B goes
+    out as `chunks` word-aligned row blocks, all queued at once (async collectives), and the
+    product of chunk j -- A's matching columns times B's rows -- starts as soon as chunk j has
+    arrived, while chunk j+1 is still on the wire.  The chunk products are summed in the field
+    (exact, then canonical), so the result is bit-identical to the single-broadcast path.
+    B_local is None when return_b is False (saves re-assembling B from its chunks)."""
     if multiply is None:
         from .m4rm import m4rm_multiply as multiply
     if A_shard.ncols != l:
         raise ValueError(f"inner dimensions {A_shard.ncols} != {l}")
-    B_local = broadcast_matrix(B, field, l, n, src=src, group=group, device=device)
-    return multiply(A_shard, B_local), B_local
+    parts = b_chunks(l, chunks)
+    if len(parts) == 1:
+        B_local = broadcast_matrix(B, field, l, n, src=src, group=group, device=device)
+        return multiply(A_shard, B_local), B_local
+    canonical = add is None and field.name in ("f5", "f7")  # redundant encodings: canonical at the end
+    if add is None:
+        def add(X, Y):
+            return X.add(Y)
+    rank = dist.get_rank(group)
+    W = (n + 63) // 64
+    dev = device if device is not None else A_shard.device
+    if rank == src:
+        if B is None or (B.nrows, B.ncols) != (l, n) or B.field is not field:
+            raise ValueError("source rank must pass B with the announced field and shape")
+        src_planes = B.planes.to(dev)
+        bufs = [src_planes[:, r0:r1].contiguous() for r0, r1 in parts]
+    else:
+        bufs = [torch.empty((field.bits, r1 - r0, W), dtype=torch.int64, device=dev) for r0, r1 in parts]
+    works = [dist.broadcast(t, src=src, group=group, async_op=True) for t in bufs]
+    C = None
+    for (r0, r1), t, work in zip(parts, bufs, works):
+        w0, w1 = r0 // 64, (r1 + 63) // 64
+        A_j = BitslicedMatrix(field, A_shard.nrows, r1 - r0, A_shard.planes[:, :, w0:w1].contiguous())
+        work.wait()  # NCCL: the current stream waits for this chunk (the host does not block)
+        P = multiply(A_j, BitslicedMatrix(field, r1 - r0, n, t))
+        C = P if C is None else add(C, P)
+    if canonical:
+        C = C.reduce_canonical()
+    B_local = BitslicedMatrix(field, l, n, torch.cat(bufs, dim=1)) if return_b else None
+    return C, B_local
 
 
 def gather_rows(C_shard: BitslicedMatrix, m: int, group=None) -> BitslicedMatrix:

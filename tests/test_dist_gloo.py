@@ -30,7 +30,17 @@ def _oracle_multiply(A, B):
     return sg.BitslicedMatrix.from_planes(A.field, C, B.ncols, device="cpu")
 
 
-def _worker(rank, world, port, field_name, m, l, n, out_q):
+def _oracle_add(X, Y):
+    import oracle
+    import paper_0901_1413_b200 as sg
+    name = X.field.name
+    q = oracle.ORDER[name]
+    x, y = oracle.unpack(name, X.planes_numpy(), X.ncols), oracle.unpack(name, Y.planes_numpy(), Y.ncols)
+    s = (x ^ y) if name in ("gf4", "gf8", "f2") else (x.astype(int) + y) % q
+    return sg.BitslicedMatrix.from_planes(X.field, oracle.pack(name, s.astype(np.uint8)), X.ncols, device="cpu")
+
+
+def _worker(rank, world, port, field_name, m, l, n, out_q, chunks=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -47,7 +57,11 @@ def _worker(rank, world, port, field_name, m, l, n, out_q):
         if rank == 0:
             B = sg.BitslicedMatrix.from_planes(field, oracle.pack(oname, oracle.random_dense(oname, l, n, 1)), n,
                                                device="cpu")
-        C_shard, B_local = sgdist.sharded_multiply(A_shard, B, field, l, n, src=0, multiply=_oracle_multiply)
+        C_shard, B_local = sgdist.sharded_multiply(A_shard, B, field, l, n, src=0, multiply=_oracle_multiply,
+                                                   chunks=chunks, add=_oracle_add if chunks > 1 else None)
+        if rank == 1:
+            want_b = oracle.pack(oname, oracle.random_dense(oname, l, n, 1))
+            assert np.array_equal(B_local.planes_numpy(), want_b)
         C = sgdist.gather_rows(C_shard, m)
         if rank == 0:
             want = oracle.dense_multiply(oname, A_full, oracle.random_dense(oname, l, n, 1))
@@ -57,12 +71,15 @@ def _worker(rank, world, port, field_name, m, l, n, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("field_name,m,l,n", [("f3", 67, 90, 130), ("f7", 10, 33, 65), ("gf4", 5, 17, 64)])
-def test_world2_sharded_multiply_matches_oracle(field_name, m, l, n):
+@pytest.mark.parametrize("field_name,m,l,n,chunks", [("f3", 67, 90, 130, 1), ("f7", 10, 33, 65, 1),
+                                                     ("gf4", 5, 17, 64, 1), ("f5", 9, 300, 70, 4),
+                                                     ("f3", 33, 129, 65, 2), ("f7", 6, 200, 20, 3)])
+def test_world2_sharded_multiply_matches_oracle(field_name, m, l, n, chunks):
+    """chunks > 1: the broadcast of B in row blocks overlapped with the per-chunk products."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, field_name, m, l, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, field_name, m, l, n, q, chunks)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

@@ -444,3 +444,29 @@ def test_classical_multiply_cross_check(fname):
         Cc = sg.classical_multiply(Ag, Bg)
         assert np.array_equal(Cc.planes_numpy(), expect(fname, A, B)), (fname, m, l, n)
         assert np.array_equal(Cc.planes_numpy(), sg.m4rm_multiply(Ag, Bg).planes_numpy())
+
+
+def test_sharded_multiply_chunked_on_device():
+    """dist.sharded_multiply's overlapped path (B in row blocks, per-chunk products summed on the
+    GPU) in a one-rank gloo group: bit-identical to the oracle for every field and chunk count."""
+    import tempfile
+
+    import torch.distributed as dist
+
+    from paper_0901_1413_b200 import dist as sgdist
+    store = tempfile.NamedTemporaryFile(delete=False)
+    dist.init_process_group("gloo", init_method=f"file://{store.name}", rank=0, world_size=1)
+    try:
+        for fname in FIELDS:
+            m, l, n = 70, 333, 150
+            A = oracle.random_dense(fname, m, l, 5)
+            B = oracle.random_dense(fname, l, n, 6)
+            want = expect(fname, A, B)
+            Am = sg.BitslicedMatrix.from_dense(FIELDS[fname], A)
+            Bm = sg.BitslicedMatrix.from_dense(FIELDS[fname], B)
+            for chunks in (1, 2, 3, 4, 6):
+                C, Bl = sgdist.sharded_multiply(Am, Bm, FIELDS[fname], l, n, chunks=chunks)
+                assert np.array_equal(C.planes_numpy(), want), (fname, chunks)
+                assert np.array_equal(Bl.planes_numpy(), Bm.planes_numpy())
+    finally:
+        dist.destroy_process_group()

@@ -16,20 +16,26 @@ from paper_0901_1413_b200 import _lib, m4rm as M  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="0,1,2,3,4")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--shapes", default="", help="extra field:m:l:n shapes")
+ap.add_argument("--rts", default="1,2,4,8,16")
 ap.add_argument("--splits", default="-1,1,2,4,8,16")  # -1 = stream-K
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 L = _lib.load()
 variants = set()
 import ctypes  # noqa: E402
-for ci in [int(x) for x in a.configs.split(",")]:
-    name, field, m, l, n = bench.CONFIGS[ci]
+jobs = [bench.CONFIGS[int(x)] for x in a.configs.split(",") if x]
+for sh in a.shapes.split(","):  # field:m:l:n, e.g. the per-rank shapes of a sharded run
+    if sh:
+        fld, m, l, n = sh.split(":")
+        jobs.append((f"{fld.upper()} {m}x{l}x{n} k=8", fld, int(m), int(l), int(n)))
+for name, field, m, l, n in jobs:
     f, A, B = bench.make_inputs(field, m, l, n, 0, dev, True)
     C = sg.BitslicedMatrix.zero(f, m, n, device=dev)
     M.set_plan_override(0, 0, -1, 0)
     auto = sg.plan(f, m, l, n, 8)
     best = None
-    for rt in (1, 2, 4, 8, 16):
+    for rt in [int(x) for x in a.rts.split(",")]:
         for nt in (256, 512):
             for pipe in (0, 1, 2):
                 for sp in [int(x) for x in a.splits.split(",")]:
