@@ -306,7 +306,7 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
     h2d = Ah.numel() * 8 + (Bh.numel() * 8 if rank == 0 else 0)
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8),
-            "path": ("sg_m4rm_host (C ABI; pinned host planes; H2D, multiply, D2H pipelined in row chunks)"
+            "path": ("sg_m4rm_host (C ABI; pinned host planes; H2D, multiply, D2H pipelined over k-chunks and row pieces)"
                      if world == 1 else "rank-0 H2D of B + broadcast in row blocks overlapped with the chunk products "
                      "(dist.sharded_multiply), per-rank H2D of A rows, D2H of C rows (wall clock, max over ranks)")}
 
