@@ -640,17 +640,22 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
     cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
     cudaEvent_t ev_in[8], ev_comp[4];
     Buf buf;
+    std::mutex busy;  // one host-buffer product per device at a time (the staging buffers are shared)
   };
   static std::map<int, Io> io_state;
   Io* d;
   char* dbuf = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    d = &io_state[device];  // std::map nodes are stable: d stays valid
+  }
+  std::lock_guard<std::mutex> busy(d->busy);  // held to the end of the call (after the final syncs)
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   // device layout: B chunks | A chunks (last one as row pieces) | chunk partials | last-chunk
   // pieces | C
   const size_t need = b_bytes + a_bytes + (size_t)(Pk - 1) * c_bytes + (Pk > 1 ? c_bytes : 0) + c_bytes + 32 * 256;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    d = &io_state[device];
     if (!d->in) {
       SG_CUDA(cudaStreamCreateWithFlags(&d->in, cudaStreamNonBlocking), "sg_m4rm_host stream");
       SG_CUDA(cudaStreamCreateWithFlags(&d->comp, cudaStreamNonBlocking), "sg_m4rm_host stream");

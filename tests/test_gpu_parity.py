@@ -470,3 +470,35 @@ def test_sharded_multiply_chunked_on_device():
                 assert np.array_equal(Bl.planes_numpy(), Bm.planes_numpy())
     finally:
         dist.destroy_process_group()
+
+
+def test_host_path_thread_safety():
+    """Pure functions, safe from any thread: concurrent host-buffer products on
+    one device (ctypes drops the GIL) each get their own correct result."""
+    import threading
+    jobs = []
+    for i, fname in enumerate(("f3", "f5", "f7", "gf4", "f2", "z8")):
+        m, l, n = 300 + 37 * i, 500 + 11 * i, 200 + 5 * i
+        A = oracle.random_dense(fname, m, l, 40 + i)
+        B = oracle.random_dense(fname, l, n, 50 + i)
+        Ah = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, A), l, device="cpu")
+        Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), n, device="cpu")
+        jobs.append((fname, Ah, Bh, expect(fname, A, B)))
+    errors = []
+
+    def run(job):
+        fname, Ah, Bh, want = job
+        try:
+            for _ in range(5):
+                C = sg.m4rm_multiply(Ah, Bh)
+                if not np.array_equal(C.planes_numpy(), want):
+                    errors.append(fname)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=run, args=(j,)) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
