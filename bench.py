@@ -51,6 +51,13 @@ for _f in sorted(os.listdir(os.path.join(ROOT, "profiles"))) if os.path.isdir(os
     if _f.endswith("_traffic.json"):
         with open(os.path.join(ROOT, "profiles", _f)) as _fh:
             TRAFFIC.update(json.load(_fh))
+# ALU-pipe and shared-memory-wavefront utilization of the M4RM kernel from the same captures
+# (profiles/*_pipes.json, tools/pipes_from_ncu.py): what the kernel is actually bound by
+PIPES = {}
+for _f in sorted(os.listdir(os.path.join(ROOT, "profiles"))) if os.path.isdir(os.path.join(ROOT, "profiles")) else []:
+    if _f.endswith("_pipes.json"):
+        with open(os.path.join(ROOT, "profiles", _f)) as _fh:
+            PIPES.update(json.load(_fh))
 METRIC = "field mul-adds/sec (m*l*n/t) for C=A*B over F3/F5/F7/GF(4), % of roofline"
 UNIT = "mul-adds/s"
 
@@ -234,6 +241,8 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
                        "definition": "same, with this kernel's own LOP3 networks (fewer ops than the reference's)"}
     roof["traffic"] = TRAFFIC.get(name)
     roof["traffic_source"] = TRAFFIC.get("_source") if name in TRAFFIC else None
+    roof["measured_pipes"] = PIPES.get(name)
+    roof["measured_pipes_source"] = PIPES.get("_source") if name in PIPES else None
     roof["kernel_ms"] = k_ms
     roof["kernel_share_of_step"] = k_ms / ms_per_step if world == 1 else None
     roof["achieved_muladds_per_s"] = work / (k_ms * 1e-3)
