@@ -502,3 +502,14 @@ def test_host_path_thread_safety():
     for t in threads:
         t.join(timeout=300)
     assert not errors, errors
+
+
+@pytest.mark.parametrize("fname", ["f3", "f5", "f7", "gf4", "f2"])
+def test_extreme_aspect_ratios(fname):
+    """Matrix-vector and long-inner-dimension shapes: one tile over 12500 k-blocks (every CTA of
+    a stream-K wave on the same tile), one row, one column, a single wide row of C."""
+    for (m, l, n) in [(3, 100000, 70), (1, 4096, 4096), (4096, 4096, 1), (1, 1, 20000), (2, 9, 130000)]:
+        A = oracle.random_dense(fname, m, l, m + 1)
+        B = oracle.random_dense(fname, l, n, n + 2)
+        C = gpu_multiply(fname, A, B)
+        assert np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, m, l, n)
