@@ -260,7 +260,6 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
     const double E = (double)(1 << K);
     const double alu_l = rows * lane_alu / 64.0, alu_t = E * entry_alu / 64.0;
     const double smem_l = (rows * lane_smem + rows * R * 4.0) / 128.0, smem_t = E * R * ENTRY_BYTES / 128.0;
-    // serialized schedule: table build, then lookups; pipelined: both share the pipes
     // serial: table build then lookups; pipelined / warp-specialized: both share the pipes
     const double t_block = ki->sched == 2   ? std::max(alu_l + alu_t, smem_l + smem_t) + 100.0
                            : ki->sched == 1 ? std::max(alu_l + alu_t, smem_l + smem_t) + 250.0
