@@ -13,6 +13,8 @@
 #include <tuple>
 #include <utility>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/slicegemm_b200.h"
 #include "sg_field.cuh"
 #include "sg_internal.h"
@@ -342,6 +344,28 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
   return SG_OK;
 }
 
+// B's planes as a 3-D u32 tensor {words, rows, planes} with a {4, 8, R} box: one TMA copy stages
+// one k-block of a 128-column slab (rows past l and words past wc32 arrive as zeros).
+bool encode_b_map(CUtensorMap* map, const void* B, int field, int64_t l, int wc32) {
+  static PFN_cuTensorMapEncodeTiled encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }();
+  if (!encode || l <= 0) return false;
+  const cuuint32_t R = (cuuint32_t)planes(field);
+  const cuuint64_t dims[3] = {(cuuint64_t)wc32, (cuuint64_t)l, R};
+  const cuuint64_t strides[2] = {(cuuint64_t)wc32 * 4, (cuuint64_t)l * wc32 * 4};
+  const cuuint32_t box[3] = {4, 8, R};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(B), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int64_t workspace_bytes_for(const Plan& p, int field) {
   const int R = planes(field);
   int64_t b = (int64_t)p.at_planes * p.at_words * p.mpad * 4;
@@ -564,6 +588,8 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   g_launches++;
   if (g_timing) cudaEventRecord(ev[1], st);
   M4rmArgs a;
+  CUtensorMap tmB;
+  memset(&tmB, 0, sizeof(tmB));
   a.B = (const uint32_t*)B;
   a.AT = AT;
   a.C = p.splits > 1 ? partial : (uint32_t*)C;
@@ -576,12 +602,23 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   a.bps = p.bps;
   a.partial = p.splits > 1;
   a.early_trigger = pdl_mode() == 2;
+  {
+    // B staging: one TMA tensor copy per k-block for the warp-specialized schedule (its builder
+    // warps wait on an mbarrier), cp.async for the others (measured equal or better there).
+    // Experiments: SG_TMA=0 stages with cp.async everywhere.
+    static const int tma_env = [] {
+      const char* e = getenv("SG_TMA");
+      return e ? atoi(e) : -1;
+    }();
+    a.tma_b = tma_env != 0 && p.ki->sched == 2 && p.K == 8 && p.wc32 % 4 == 0 && ((uintptr_t)B % 16) == 0 &&
+              encode_b_map(&tmB, B, field, l, p.wc32);
+  }
   a.streamk = p.streamk;
   a.units = p.units;
   a.slabs = p.slabs;
   a.P2 = p.streamk ? partial : nullptr;
   if (p.streamk) a.C = (uint32_t*)C;
-  SG_CUDA(launch_m4rm(*p.ki, a, p.grid, st), "sg_m4rm kernel");
+  SG_CUDA(launch_m4rm(*p.ki, a, tmB, p.grid, st), "sg_m4rm kernel");
   g_launches++;
   if (g_timing) cudaEventRecord(ev[2], st);
   if (p.streamk) {

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <utility>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sg {
@@ -65,11 +66,13 @@ struct M4rmArgs {
   int slabs;           // tiles = slabs x row groups, tile t -> slab t % slabs, row group t / slabs
   uint32_t* P2;        // compact stream-K partials [G * SK_SEGS][R][ROWS][4]
   int early_trigger;   // experiments (SG_PDL=2): release the dependent reduction at kernel start
+  int tma_b;           // stage B's k-blocks with one TMA tensor copy each (k = 8, wc32 % 4 == 0,
+                       // B 16-B aligned)
 };
 constexpr int SK_SEGS = 3;  // tile segments per stream-K CTA (the planner keeps U / G <= 2 nblocks)
 
 struct KernelInfo {
-  void (*fn)(M4rmArgs);
+  void (*fn)(M4rmArgs, CUtensorMap);  // (args, B as a 3-D u32 tensor map for TMA staging)
   int field, k, rt, threads;  // threads = lookup threads (rows = rt * threads)
   int launch_threads;  // threads + 32 for the warp-specialized schedule
   int sched;           // 0 serial, 1 pipelined (double-buffered table), 2 warp-specialized
@@ -86,7 +89,8 @@ KernelInfo* m4rm_kernel_at(int i);
 // k = 8: packed index words [nwords][mpad]; k < 8: A^T bit planes [R][wa32][mpad]
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
                                int wa32, int nwords, cudaStream_t st);
-cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st);
+cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorMap& tmB, dim3 grid,
+                        cudaStream_t st);
 // up to SLICES_MAX equally shaped R-plane row slices with their own plane strides (u32 words)
 constexpr int SLICES_MAX = 8;
 struct SliceSet {

@@ -240,8 +240,9 @@ int pdl_mode() {
 
 int m4rm_kernel_count() { return (int)registry().size(); }
 KernelInfo* m4rm_kernel_at(int i) { return registry()[i]; }
-cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, dim3 grid, cudaStream_t st) {
-  return launch_pdl(ki.fn, grid, dim3(ki.launch_threads), ki.smem_bytes, st, a);
+cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorMap& tmB, dim3 grid,
+                        cudaStream_t st) {
+  return launch_pdl(ki.fn, grid, dim3(ki.launch_threads), ki.smem_bytes, st, a, tmB);
 }
 
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,

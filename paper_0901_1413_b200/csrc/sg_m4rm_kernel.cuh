@@ -41,6 +41,40 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// ---- TMA bulk copies (cp.async.bulk) completing on shared-memory mbarriers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
 template <int F> __device__ __forceinline__ V<F> vzero() {
   V<F> v;
 #pragma unroll
@@ -170,7 +204,8 @@ __host__ __device__ constexpr int ws_builders(int sched) { return sched == 2 ? 1
 // One segment: the CTA's slab (word0) x row group (row0) x k-blocks [s_begin, s_end), written to
 // C (mode 0), to split-K partial plane `slot` (mode 1) or to compact stream-K slot `slot` (mode 2).
 template <int F, int K, int RT, int SCHED, int NT, int ABL>
-__device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* smem, const int word0,
+__device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMap* tmB, unsigned char* smem,
+                                             const int word0,
                                              const int64_t row0, const int s_begin, const int s_end,
                                              const int mode, const int slot) {
   constexpr bool PIPE = SCHED == 1;
@@ -204,14 +239,30 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* s
   u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][16][R][4]
   u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
+  uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ROWS);  // [3] B-slot barriers
 
   const int tid = threadIdx.x;
   if (s_begin >= s_end) return;
+  // TMA staging of B is compiled into the warp-specialized schedule only (measured: no gain for
+  // the others); there it is used when the host found B aligned for it (a.tma_b).
+  constexpr bool TMA_OK = WS && K == 8;
+  const bool tma_b = TMA_OK && a.tma_b;
 
   int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
   // Stage block s's B rows (K x R x 16 B) into bst[s % 3].
   auto issue_b = [&](int s, int t0 = -1, int nthr = NT) {
     if (t0 < 0) t0 = tid;
+    if (TMA_OK && tma_b) {
+      // TMA: one thread sends the block's [R planes][K rows][4 words] box of B as ONE tensor
+      // copy (rows past l arrive zero-filled) completing on mbar_b[s % 3]
+      if constexpr (K == 8) {
+        if (s < s_end && t0 == 0) {
+          mbar_expect_tx(&mbar_b[s % 3], (unsigned)(K * R * 16));
+          tma_load_3d(bst + (s % 3) * K * R * 4, tmB, word0, s * K, 0, &mbar_b[s % 3]);
+        }
+      }
+      return;
+    }
     if (s < s_end) {
       u32* bdst = bst + (s % 3) * K * R * 4;
       for (int q = t0; q < K * R * 2; q += nthr) {
@@ -241,11 +292,20 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* s
     }
   };
 
+  // staged B piece (row i of the block, plane d): TMA boxes land plane-major [d][i], cp.async
+  // writes row-major [i][d] (consecutive threads -> consecutive 8-byte halves, no bank conflicts)
+  auto bpos = [&](int i, int d) { return (TMA_OK && tma_b) ? d * K + i : i * R + d; };
+  // TMA path: block s's B rows have landed (slot s % 3 is used once per 3 blocks of the segment)
+  auto wait_b = [&](int s) {
+    if (TMA_OK && tma_b) mbar_wait(&mbar_b[s % 3], (unsigned)(((s - s_begin) / 3) & 1));
+  };
+
   // phase 1: the two 16-entry half tables of block s (rows 0..KLO-1 and KLO..K-1)
   auto phase1 = [&](int s) {
     const u32* bs = bst + (s % 3) * K * R * 4;
     u32* th = thalf + (s & 1) * 2 * HALF;
     if (tid < 128) {
+      wait_b(s);
       const int h = tid >> 6, e = (tid >> 2) & 15, w = tid & 3;
       const int nrows = h ? KHI : KLO;
       if (e < (1 << nrows)) {
@@ -255,7 +315,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* s
           if (i < nrows && ((e >> i) & 1)) {
             V<F> b;
 #pragma unroll
-            for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
+            for (int d = 0; d < R; ++d) b.p[d] = bs[bpos(h * KLO + i, d) * 4 + w];
             vadd<F>(acc, b);
           }
         }
@@ -397,6 +457,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* s
         issue_a(s + 1, bt, NBT);
         cp_async_commit();
         cp_async_wait<1>();  // B rows of s and A words of s have landed (this thread's copies)
+        wait_b(s);           // TMA path: the block's B rows
         bsync();
         // phase 1: 2 halves x 16 entries x 4 words = 128 items
         {
@@ -411,7 +472,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* s
                 if (i < nrows && ((e >> i) & 1)) {
                   V<F> b;
 #pragma unroll
-                  for (int d = 0; d < R; ++d) b.p[d] = bs[((h * KLO + i) * R + d) * 4 + w];
+                  for (int d = 0; d < R; ++d) b.p[d] = bs[bpos(h * KLO + i, d) * 4 + w];
                   vadd<F>(acc, b);
                 }
               }
@@ -563,14 +624,27 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, unsigned char* s
 // SK_SEGS tile segments; each lands in compact slot c * SK_SEGS + segment and reduce_streamk sums
 // the slots of every tile.  Otherwise one segment per CTA: (slab, row group, k-split) = blockIdx.
 template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
-__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a) {
+__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ROWS = RT * NT;
   if (a.early_trigger) pdl_trigger();
   pdl_wait();  // launched with PDL behind the index pre-pass: wait for its writes
+  constexpr int R = Traits<F>::R;
+  constexpr int NSLOT = K == 8 ? 3 : 2;
+  constexpr int NAP = K == 8 ? 1 : R;
+  uint64_t* mbar_b = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES +
+                                                 (2 * 2 * 16 * R * 4 + 3 * K * R * 4 + NSLOT * NAP * ROWS) * 4);
+  constexpr bool TMA_OK = SCHED == 2 && K == 8;
+  if (TMA_OK && a.tma_b) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(&mbar_b[i], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   if (!a.streamk) {
     const int s_begin = blockIdx.z * a.bps;
-    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS, s_begin,
+    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, &tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS, s_begin,
                                            min(a.nblocks, s_begin + a.bps), a.partial ? 1 : 0, blockIdx.z);
     return;
   }
@@ -582,11 +656,20 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const 
     const int s0 = (int)(u - tile * a.nblocks);
     const int64_t room = u1 - u;
     const int s1 = (int)(s0 + room < a.nblocks ? s0 + room : (int64_t)a.nblocks);
-    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, smem, (int)(tile % a.slabs) * SLAB_WORDS, (tile / a.slabs) * ROWS, s0,
+    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, &tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS, (tile / a.slabs) * ROWS, s0,
                                            s1, 2, blockIdx.x * SK_SEGS + seg);
     u += s1 - s0;
     cp_async_wait<0>();
     __syncthreads();  // shared memory is reused by the next segment
+    if (TMA_OK && a.tma_b) {  // fresh barriers: the next segment counts its phases from zero
+      if (threadIdx.x == 0)
+        for (int i = 0; i < 3; ++i) {
+          mbar_inval(&mbar_b[i]);
+          mbar_init(&mbar_b[i], 1);
+        }
+      if (threadIdx.x == 0) fence_mbar_init();
+      __syncthreads();
+    }
   }
 }
 
@@ -597,7 +680,7 @@ constexpr int smem_bytes_for() {
   constexpr int NSLOT = K == 8 ? 3 : 2;
   constexpr int NAP = K == 8 ? 1 : R;
   return (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
-         NSLOT * NAP * RT * NT * 4;
+         NSLOT * NAP * RT * NT * 4 + 3 * 8;  // + the B-slot mbarriers
 }
 
 #define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \

@@ -119,24 +119,27 @@ def test_k_invariance(fname):
 
 @pytest.mark.parametrize("fname", list(FIELDS))
 def test_every_compiled_plan(fname):  # noqa: F811
-    """Force every rows-per-thread variant, both schedules and several k-splits."""
-    A = oracle.random_dense(fname, 700, 1000, 7)
-    B = oracle.random_dense(fname, 1000, 777, 8)
-    want = expect(fname, A, B)
+    """Force every rows-per-thread variant, every schedule and several k-splits, with B staged by
+    cp.async (n = 777: odd 64-bit word count) and by TMA bulk copies (n = 768), l = 1001 leaving
+    a partial last k-block (zero-filled B rows)."""
     ran = 0
-    for rt in (1, 2, 4, 8, 16):
-        for pipe in (0, 1, 2):
-            for nt in (256, 512):
-                for splits in (1, 2, 5, 16):
-                    m4rm_mod.set_plan_override(rt, splits, pipe, nt)
-                    try:
-                        C = gpu_multiply(fname, A, B)
-                    except RuntimeError as e:
-                        assert "no compiled" in str(e)
-                        continue
-                    ran += 1
-                    assert np.array_equal(C.planes_numpy(), want), (fname, rt, pipe, nt, splits)
-    assert ran >= 40
+    for n in (777, 768):
+        A = oracle.random_dense(fname, 700, 1001, 7)
+        B = oracle.random_dense(fname, 1001, n, 8)
+        want = expect(fname, A, B)
+        for rt in (1, 2, 4, 8, 16):
+            for pipe in (0, 1, 2):
+                for nt in (256, 512):
+                    for splits in (1, 2, 5, 16):
+                        m4rm_mod.set_plan_override(rt, splits, pipe, nt)
+                        try:
+                            C = gpu_multiply(fname, A, B)
+                        except RuntimeError as e:
+                            assert "no compiled" in str(e)
+                            continue
+                        ran += 1
+                        assert np.array_equal(C.planes_numpy(), want), (fname, n, rt, pipe, nt, splits)
+    assert ran >= 80
 
 
 @pytest.mark.parametrize("fname", list(FIELDS))
