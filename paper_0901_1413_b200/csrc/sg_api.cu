@@ -612,6 +612,9 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
     }();
     a.tma_b = tma_env != 0 && p.ki->sched == 2 && p.K == 8 && p.wc32 % 4 == 0 && ((uintptr_t)B % 16) == 0 &&
               encode_b_map(&tmB, B, field, l, p.wc32);
+    // A's index words by TMA too, except under stream-K (measured: F3 32768^3 -1 %, F7 -1.4 %,
+    // GF(4) 8192^3 stream-K +2.6 %; SG_TMA=2 forces it, for experiments)
+    a.tma_a = a.tma_b && (tma_env == 2 || !p.streamk);
   }
   a.streamk = p.streamk;
   a.units = p.units;

@@ -68,6 +68,7 @@ struct M4rmArgs {
   int early_trigger;   // experiments (SG_PDL=2): release the dependent reduction at kernel start
   int tma_b;           // stage B's k-blocks with one TMA tensor copy each (k = 8, wc32 % 4 == 0,
                        // B 16-B aligned)
+  int tma_a;           // ... and A's index words with 1-D bulk copies (with tma_b only)
 };
 constexpr int SK_SEGS = 3;  // tile segments per stream-K CTA (the planner keeps U / G <= 2 nblocks)
 

@@ -203,7 +203,10 @@ __host__ __device__ constexpr int ws_builders(int sched) { return sched == 2 ? 1
 
 // One segment: the CTA's slab (word0) x row group (row0) x k-blocks [s_begin, s_end), written to
 // C (mode 0), to split-K partial plane `slot` (mode 1) or to compact stream-K slot `slot` (mode 2).
-template <int F, int K, int RT, int SCHED, int NT, int ABL>
+// ROLE (warp-specialized schedule only): 1 = the builder warps' part, 2 = the lookup warps' part;
+// 0 = everything (the other schedules).  The two roles run separately compiled code so that each
+// can live with its own register budget (setmaxnreg in m4rm_kernel).
+template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE>
 __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMap* tmB, unsigned char* smem,
                                              const int word0,
                                              const int64_t row0, const int s_begin, const int s_end,
@@ -240,6 +243,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
   u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
   uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ROWS);  // [3] B-slot barriers
+  uint64_t* mbar_a = mbar_b + 3;                                               // [3] A-slot barriers
 
   const int tid = threadIdx.x;
   if (s_begin >= s_end) return;
@@ -247,6 +251,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
   // the others); there it is used when the host found B aligned for it (a.tma_b).
   constexpr bool TMA_OK = WS && K == 8;
   const bool tma_b = TMA_OK && a.tma_b;
+  const bool tma_a = tma_b && a.tma_a;
 
   int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
   // Stage block s's B rows (K x R x 16 B) into bst[s % 3].
@@ -278,6 +283,21 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
   // Stage the index words block s needs that are not yet staged.
   auto issue_a = [&](int s, int t0 = -1, int nthr = NT) {
     if (t0 < 0) t0 = tid;
+    if constexpr (TMA_OK) {
+      if (tma_a) {
+        // TMA: the CTA's ROWS index records of each new word as ONE 1-D bulk copy
+        if (s < s_end) {
+          for (const int whi = s / RPW; next_word <= whi; ++next_word) {
+            if (t0 == 0) {
+              const int sl = next_word % NSLOT;
+              mbar_expect_tx(&mbar_a[sl], ROWS * 4);
+              tma_load_1d(ast + sl * ROWS, a.AT + (int64_t)next_word * a.mpad + row0, ROWS * 4, &mbar_a[sl]);
+            }
+          }
+        }
+        return;
+      }
+    }
     if (s < s_end) {
       const int whi = IW ? s / RPW : (s * K + K - 1) >> 5;
       for (; next_word <= whi; ++next_word) {
@@ -298,6 +318,13 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
   // TMA path: block s's B rows have landed (slot s % 3 is used once per 3 blocks of the segment)
   auto wait_b = [&](int s) {
     if (TMA_OK && tma_b) mbar_wait(&mbar_b[s % 3], (unsigned)(((s - s_begin) / 3) & 1));
+  };
+  // ... and block s's index word (slot w % NSLOT, used once per NSLOT words of the segment)
+  auto wait_a = [&](int s) {
+    if (TMA_OK && tma_a) {
+      const int w = s / RPW, w0 = s_begin / RPW;
+      mbar_wait(&mbar_a[w % NSLOT], (unsigned)(((w - w0) / NSLOT) & 1));
+    }
   };
 
   // phase 1: the two 16-entry half tables of block s (rows 0..KLO-1 and KLO..K-1)
@@ -442,7 +469,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
     constexpr int NB = NT + NBT;  // all threads take part in every FULL / EMPTY barrier
     auto FULL = [](int s) { return 1 + (s & 1); };
     auto EMPTY = [](int s) { return 3 + (s & 1); };
-    if (tid >= NT) {
+    if constexpr (ROLE == 1) {
       // ------------------------------------------------ builder warps
       const int bt = tid - NT;
       auto bsync = [] { nbar_sync(5, NBT); };
@@ -457,7 +484,8 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
         issue_a(s + 1, bt, NBT);
         cp_async_commit();
         cp_async_wait<1>();  // B rows of s and A words of s have landed (this thread's copies)
-        wait_b(s);           // TMA path: the block's B rows
+        wait_b(s);           // TMA path: the block's B rows ...
+        wait_a(s);           // ... and index word (published to the lookup warps by FULL)
         bsync();
         // phase 1: 2 halves x 16 entries x 4 words = 128 items
         {
@@ -513,7 +541,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
       cp_async_wait<0>();
       return;
     }
-    // ------------------------------------------------ lookup warps
+    // ------------------------------------------------ lookup warps (ROLE 2)
     for (int s = s_begin; s < s_end; ++s) {
       nbar_sync(FULL(s), NB);
       lookups(s, s & 1, [](int) {});
@@ -620,32 +648,20 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
   }
 }
 
-// Stream-K: CTA c owns work units [c U / G, (c+1) U / G) of U = tiles x k-blocks, i.e. at most
-// SK_SEGS tile segments; each lands in compact slot c * SK_SEGS + segment and reduce_streamk sums
-// the slots of every tile.  Otherwise one segment per CTA: (slab, row group, k-split) = blockIdx.
-template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
-__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const M4rmArgs a, const __grid_constant__ CUtensorMap tmB) {
-  extern __shared__ __align__(128) unsigned char smem[];
+// All of this CTA's segments.  Stream-K: CTA c owns work units [c U / G, (c+1) U / G) of
+// U = tiles x k-blocks, i.e. at most SK_SEGS tile segments; each lands in compact slot
+// c * SK_SEGS + segment and reduce_streamk sums the slots of every tile.  Otherwise one segment
+// per CTA: (slab, row group, k-split) = blockIdx.
+template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE>
+__device__ __forceinline__ void run_segments(const M4rmArgs& a, const CUtensorMap* tmB, unsigned char* smem,
+                                             uint64_t* mbar) {
   constexpr int ROWS = RT * NT;
-  if (a.early_trigger) pdl_trigger();
-  pdl_wait();  // launched with PDL behind the index pre-pass: wait for its writes
-  constexpr int R = Traits<F>::R;
-  constexpr int NSLOT = K == 8 ? 3 : 2;
-  constexpr int NAP = K == 8 ? 1 : R;
-  uint64_t* mbar_b = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES +
-                                                 (2 * 2 * 16 * R * 4 + 3 * K * R * 4 + NSLOT * NAP * ROWS) * 4);
   constexpr bool TMA_OK = SCHED == 2 && K == 8;
-  if (TMA_OK && a.tma_b) {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < 3; ++i) mbar_init(&mbar_b[i], 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
-  }
   if (!a.streamk) {
     const int s_begin = blockIdx.z * a.bps;
-    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, &tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS, s_begin,
-                                           min(a.nblocks, s_begin + a.bps), a.partial ? 1 : 0, blockIdx.z);
+    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE>(a, tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS,
+                                                 s_begin, min(a.nblocks, s_begin + a.bps), a.partial ? 1 : 0,
+                                                 blockIdx.z);
     return;
   }
   const int64_t U = a.units, G = gridDim.x;
@@ -656,20 +672,57 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1) m4rm_kernel(const 
     const int s0 = (int)(u - tile * a.nblocks);
     const int64_t room = u1 - u;
     const int s1 = (int)(s0 + room < a.nblocks ? s0 + room : (int64_t)a.nblocks);
-    m4rm_segment<F, K, RT, SCHED, NT, ABL>(a, &tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS, (tile / a.slabs) * ROWS, s0,
-                                           s1, 2, blockIdx.x * SK_SEGS + seg);
+    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE>(a, tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS,
+                                                 (tile / a.slabs) * ROWS, s0, s1, 2, blockIdx.x * SK_SEGS + seg);
     u += s1 - s0;
     cp_async_wait<0>();
     __syncthreads();  // shared memory is reused by the next segment
     if (TMA_OK && a.tma_b) {  // fresh barriers: the next segment counts its phases from zero
-      if (threadIdx.x == 0)
-        for (int i = 0; i < 3; ++i) {
-          mbar_inval(&mbar_b[i]);
-          mbar_init(&mbar_b[i], 1);
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < 6; ++i) {
+          mbar_inval(&mbar[i]);
+          mbar_init(&mbar[i], 1);
         }
-      if (threadIdx.x == 0) fence_mbar_init();
+        fence_mbar_init();
+      }
       __syncthreads();
     }
+  }
+}
+
+template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
+__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
+    m4rm_kernel(const M4rmArgs a, const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int ROWS = RT * NT;
+  if (a.early_trigger) pdl_trigger();
+  pdl_wait();  // launched with PDL behind the index pre-pass: wait for its writes
+  constexpr int R = Traits<F>::R;
+  constexpr int NSLOT = K == 8 ? 3 : 2;
+  constexpr int NAP = K == 8 ? 1 : R;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES +
+                                               (2 * 2 * 16 * R * 4 + 3 * K * R * 4 + NSLOT * NAP * ROWS) * 4);
+  constexpr bool TMA_OK = SCHED == 2 && K == 8;
+  if (TMA_OK && a.tma_b) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 6; ++i) mbar_init(&mbar[i], 1);  // 3 B slots, 3 A slots
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  if constexpr (SCHED == 2) {
+    // warp-specialized: the builder warpgroup hands registers to the two lookup warpgroups,
+    // whose row accumulators need them (384 x 168 = 128 x BREGS + 256 x LREGS)
+    constexpr int BREGS = 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
+    if (threadIdx.x >= NT) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(BREGS));
+      run_segments<F, K, RT, SCHED, NT, ABL, 1>(a, &tmB, smem, mbar);
+    } else {
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LREGS));
+      run_segments<F, K, RT, SCHED, NT, ABL, 2>(a, &tmB, smem, mbar);
+    }
+  } else {
+    run_segments<F, K, RT, SCHED, NT, ABL, 0>(a, &tmB, smem, mbar);
   }
 }
 
@@ -680,7 +733,7 @@ constexpr int smem_bytes_for() {
   constexpr int NSLOT = K == 8 ? 3 : 2;
   constexpr int NAP = K == 8 ? 1 : R;
   return (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
-         NSLOT * NAP * RT * NT * 4 + 3 * 8;  // + the B-slot mbarriers
+         NSLOT * NAP * RT * NT * 4 + 6 * 8;  // + the B- and A-slot mbarriers
 }
 
 #define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \
