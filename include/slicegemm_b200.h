@@ -161,6 +161,11 @@ int sg_set_timing(int enable);                              /* event-time each i
 int sg_debug_ablation(int mask);
 int sg_last_timing(double* transpose_ms, double* m4rm_ms, double* reduce_ms);
 int64_t sg_launch_count(void);                              /* kernels launched by this library */
+/* compiled M4RM instantiation `index` (0 .. count-1; returns the count, or -1 for a bad index):
+ * field, k, rows per thread, lookup threads, schedule, CTAs per SM on `device`, registers per
+ * thread, dynamic shared memory bytes (any pointer may be NULL) */
+int sg_kernel_info(int index, int device, int* field, int* k, int* rows_per_thread, int* threads,
+                   int* schedule, int* occupancy, int* regs, int* smem_bytes);
 int sg_probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_sm,
                    double* sm_mhz);
 

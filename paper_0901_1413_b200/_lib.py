@@ -33,7 +33,7 @@ EXPORTS = (
     "sg_abi_version", "sg_last_error", "sg_field_planes", "sg_pack", "sg_unpack",
     "sg_reduce_canonical", "sg_plane_op", "sg_m4rm_workspace_bytes", "sg_m4rm", "sg_m4rm_host",
     "sg_build_table", "sg_m4rm_block", "sg_plan", "sg_set_plan_override", "sg_set_timing",
-    "sg_last_timing", "sg_launch_count", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
+    "sg_last_timing", "sg_launch_count", "sg_kernel_info", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
 )
 
 _lib = None
@@ -76,6 +76,7 @@ def load():
         "sg_set_timing": ([i32], i32),
         "sg_last_timing": ([dp, dp, dp], i32),
         "sg_launch_count": ([], i64),
+        "sg_kernel_info": ([i32, i32, ip, ip, ip, ip, ip, ip, ip, ip], i32),
         "sg_probe_peaks": ([i32, dp, dp, dp], i32),
         "sg_debug_ablation": ([i32], i32),
         "sg_classical": ([i32, vp, vp, vp, i64, i64, i64, vp], i32),

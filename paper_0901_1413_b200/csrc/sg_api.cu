@@ -120,78 +120,79 @@ struct Plan {
   double est_clk = 0;
 };
 
-// Measured per-CTA cost of the k = 8 variants on B200 (tools/tune.py over BASELINE.json's
-// configs, least-squares fit of  time = waves * (blocks_per_cta * blk + cta), max error 2 %):
-// {field, rows per thread, lookup threads, schedule, clocks per k-block, clocks per CTA}.
+// Measured per-CTA cost of the k = 8 variants on B200 (tools/tune.py over BASELINE.json's configs
+// and the per-rank shapes of the sharded runs, fitted by tools/fit_calib.py to the model below;
+// profiles/r01d_tune_all.jsonl): {field, rows per thread, lookup threads, schedule, clocks per
+// k-block, clocks per CTA}.
 struct Calib {
   int field, rt, threads, sched;
   double blk, cta;
 };
 const Calib g_calib[] = {
-    {1, 1, 256, 0, 981, 2000},  // max err 0%
-    {1, 1, 256, 1, 1370, 2000},  // max err 1%
-    {1, 2, 256, 0, 1129, 3617},  // max err 0%
-    {1, 2, 256, 1, 1464, 2000},  // max err 1%
-    {1, 2, 512, 0, 1924, 10081},  // max err 0%
-    {1, 2, 512, 1, 1743, 9596},  // max err 0%
-    {1, 4, 256, 0, 1473, 7734},  // max err 0%
-    {1, 4, 256, 1, 1918, 13221},  // max err 0%
-    {1, 4, 512, 0, 2441, 16015},  // max err 0%
-    {1, 4, 512, 1, 2440, 19552},  // max err 0%
-    {1, 8, 256, 0, 2415, 16468},  // max err 0%
-    {1, 8, 256, 1, 2319, 18453},  // max err 0%
-    {1, 8, 256, 2, 2123, 18847},  // max err 0%
-    {1, 8, 512, 0, 3703, 19088},  // max err 1%
-    {1, 8, 512, 1, 3860, 35949},  // max err 0%
-    {1, 16, 256, 0, 3592, 26712},  // max err 0%
-    {1, 16, 256, 1, 3613, 29265},  // max err 0%
-    {1, 16, 256, 2, 3299, 32254},  // max err 0%
-    {2, 1, 256, 0, 1826, 2174},  // max err 1%
-    {2, 1, 256, 1, 2333, 5903},  // max err 1%
-    {2, 2, 256, 0, 2224, 4963},  // max err 1%
-    {2, 2, 256, 1, 2569, 10700},  // max err 0%
-    {2, 2, 512, 0, 3859, 16994},  // max err 1%
-    {2, 2, 512, 1, 3687, 19251},  // max err 1%
-    {2, 4, 256, 0, 3552, 16921},  // max err 0%
-    {2, 4, 256, 1, 3204, 18621},  // max err 0%
-    {2, 4, 256, 2, 2895, 17950},  // max err 0%
-    {2, 4, 512, 0, 5397, 35088},  // max err 2%
-    {2, 4, 512, 1, 5208, 39246},  // max err 2%
-    {2, 8, 256, 0, 5051, 35463},  // max err 2%
-    {2, 8, 256, 1, 4742, 38123},  // max err 2%
-    {2, 8, 256, 2, 5575, 39612},  // max err 2%
-    {3, 1, 256, 0, 1689, 4212},  // max err 0%
-    {3, 1, 256, 1, 2255, 6002},  // max err 0%
-    {3, 2, 256, 0, 2006, 7342},  // max err 0%
-    {3, 2, 256, 1, 2507, 9571},  // max err 0%
-    {3, 2, 512, 0, 3547, 14538},  // max err 0%
-    {3, 2, 512, 1, 3320, 17115},  // max err 0%
-    {3, 4, 256, 0, 3311, 15066},  // max err 0%
-    {3, 4, 256, 1, 3167, 17247},  // max err 0%
-    {3, 4, 256, 2, 2779, 16263},  // max err 0%
-    {3, 4, 512, 0, 4885, 27384},  // max err 1%
-    {3, 4, 512, 1, 4916, 32669},  // max err 0%
-    {3, 8, 256, 0, 4587, 29211},  // max err 0%
-    {3, 8, 256, 1, 4506, 32100},  // max err 0%
-    {3, 8, 256, 2, 4042, 32361},  // max err 0%
-    {4, 1, 256, 0, 986, 2000},  // max err 0%
-    {4, 1, 256, 1, 1301, 4015},  // max err 0%
-    {4, 2, 256, 0, 1138, 2693},  // max err 1%
-    {4, 2, 256, 1, 1414, 6175},  // max err 0%
-    {4, 2, 512, 0, 1765, 9289},  // max err 0%
-    {4, 2, 512, 1, 1746, 10665},  // max err 0%
-    {4, 4, 256, 0, 1494, 6096},  // max err 0%
-    {4, 4, 256, 1, 1717, 9997},  // max err 0%
-    {4, 4, 512, 0, 2471, 17760},  // max err 0%
-    {4, 4, 512, 1, 2415, 19116},  // max err 0%
-    {4, 8, 256, 0, 2338, 18147},  // max err 0%
-    {4, 8, 256, 1, 2291, 18981},  // max err 0%
-    {4, 8, 256, 2, 2186, 18743},  // max err 0%
-    {4, 8, 512, 0, 3663, 35513},  // max err 0%
-    {4, 8, 512, 1, 3651, 35671},  // max err 1%
-    {4, 16, 256, 0, 3558, 35759},  // max err 0%
-    {4, 16, 256, 1, 3542, 36911},  // max err 0%
-    {4, 16, 256, 2, 3314, 37255},  // max err 0%
+    {1, 1, 256, 0, 1008, 4776},  // max err 32%, 16 runs
+    {1, 1, 256, 1, 1358, 9249},  // max err 8%, 16 runs
+    {1, 2, 256, 0, 1246, 13806},  // max err 23%, 16 runs
+    {1, 2, 256, 1, 1461, 15548},  // max err 5%, 16 runs
+    {1, 2, 512, 0, 1937, 20379},  // max err 3%, 16 runs
+    {1, 2, 512, 1, 1757, 23095},  // max err 5%, 16 runs
+    {1, 4, 256, 0, 1498, 20872},  // max err 19%, 16 runs
+    {1, 4, 256, 1, 1778, 22034},  // max err 4%, 16 runs
+    {1, 4, 512, 0, 2531, 22821},  // max err 3%, 16 runs
+    {1, 4, 512, 1, 2520, 23839},  // max err 1%, 16 runs
+    {1, 8, 256, 0, 2435, 22269},  // max err 3%, 16 runs
+    {1, 8, 256, 1, 2311, 23809},  // max err 2%, 16 runs
+    {1, 8, 256, 2, 2332, 23947},  // max err 2%, 16 runs
+    {1, 8, 512, 0, 3731, 22100},  // max err 2%, 17 runs
+    {1, 8, 512, 1, 3909, 23979},  // max err 9%, 17 runs
+    {1, 16, 256, 0, 3620, 21271},  // max err 2%, 17 runs
+    {1, 16, 256, 1, 3690, 21923},  // max err 1%, 17 runs
+    {1, 16, 256, 2, 3085, 22701},  // max err 3%, 17 runs
+    {2, 1, 256, 0, 1751, 2566},  // max err 12%, 12 runs
+    {2, 1, 256, 1, 2323, 4983},  // max err 2%, 11 runs
+    {2, 2, 256, 0, 2224, 0},  // max err 20%, 12 runs
+    {2, 2, 256, 1, 2597, 8949},  // max err 1%, 12 runs
+    {2, 2, 512, 0, 3905, 13200},  // max err 1%, 12 runs
+    {2, 2, 512, 1, 3491, 16819},  // max err 3%, 12 runs
+    {2, 4, 256, 0, 3611, 11742},  // max err 2%, 12 runs
+    {2, 4, 256, 1, 3230, 14751},  // max err 2%, 12 runs
+    {2, 4, 256, 2, 3052, 14398},  // max err 3%, 12 runs
+    {2, 4, 512, 0, 5787, 23269},  // max err 3%, 12 runs
+    {2, 4, 512, 1, 5496, 29464},  // max err 6%, 12 runs
+    {2, 8, 256, 0, 5078, 24707},  // max err 1%, 12 runs
+    {2, 8, 256, 1, 4624, 27467},  // max err 3%, 12 runs
+    {2, 8, 256, 2, 4280, 27483},  // max err 2%, 12 runs
+    {3, 1, 256, 0, 1661, 6451},  // max err 8%, 10 runs
+    {3, 1, 256, 1, 2286, 4824},  // max err 0%, 10 runs
+    {3, 2, 256, 0, 2009, 6708},  // max err 11%, 11 runs
+    {3, 2, 256, 1, 2522, 8210},  // max err 0%, 10 runs
+    {3, 2, 512, 0, 3601, 12463},  // max err 1%, 11 runs
+    {3, 2, 512, 1, 3372, 15226},  // max err 1%, 11 runs
+    {3, 4, 256, 0, 3385, 11532},  // max err 2%, 11 runs
+    {3, 4, 256, 1, 3121, 14450},  // max err 1%, 11 runs
+    {3, 4, 256, 2, 2877, 12478},  // max err 5%, 11 runs
+    {3, 4, 512, 0, 5032, 24646},  // max err 1%, 11 runs
+    {3, 4, 512, 1, 4885, 29181},  // max err 2%, 11 runs
+    {3, 8, 256, 0, 4661, 24285},  // max err 1%, 11 runs
+    {3, 8, 256, 1, 4440, 27624},  // max err 1%, 11 runs
+    {3, 8, 256, 2, 3870, 27697},  // max err 1%, 11 runs
+    {4, 1, 256, 0, 891, 9118},  // max err 13%, 10 runs
+    {4, 1, 256, 1, 1296, 3985},  // max err 0%, 10 runs
+    {4, 2, 256, 0, 1154, 5752},  // max err 9%, 11 runs
+    {4, 2, 256, 1, 1419, 5412},  // max err 0%, 10 runs
+    {4, 2, 512, 0, 1844, 7143},  // max err 1%, 11 runs
+    {4, 2, 512, 1, 1750, 7672},  // max err 6%, 11 runs
+    {4, 4, 256, 0, 1817, 7237},  // max err 1%, 11 runs
+    {4, 4, 256, 1, 1738, 7639},  // max err 3%, 11 runs
+    {4, 4, 512, 0, 2540, 14624},  // max err 0%, 12 runs
+    {4, 4, 512, 1, 2446, 15162},  // max err 1%, 12 runs
+    {4, 8, 256, 0, 2398, 13635},  // max err 1%, 12 runs
+    {4, 8, 256, 1, 2302, 14121},  // max err 2%, 12 runs
+    {4, 8, 256, 2, 2324, 10497},  // max err 7%, 12 runs
+    {4, 8, 512, 0, 3690, 26807},  // max err 2%, 12 runs
+    {4, 8, 512, 1, 3643, 27070},  // max err 1%, 12 runs
+    {4, 16, 256, 0, 3598, 26686},  // max err 1%, 12 runs
+    {4, 16, 256, 1, 3547, 27403},  // max err 2%, 12 runs
+    {4, 16, 256, 2, 3107, 27836},  // max err 3%, 12 runs
 };
 
 const Calib* calib_for(const KernelInfo* ki) {
@@ -394,6 +395,28 @@ int sg_abi_version(void) { return SG_ABI_VERSION; }
 const char* sg_last_error(void) { return g_err.c_str(); }
 int sg_field_planes(int field) { return valid_field(field) ? planes(field) : -1; }
 int64_t sg_launch_count(void) { return g_launches.load(); }
+
+int sg_kernel_info(int index, int device, int* field, int* k, int* rows_per_thread, int* threads, int* schedule,
+                   int* occupancy, int* regs, int* smem_bytes) {
+  const int count = m4rm_kernel_count();
+  if (index < 0 || index >= count) return -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cudaSetDevice(device) != cudaSuccess) return -1;
+  std::lock_guard<std::mutex> lk(g_mu);
+  dev_state(device);  // fills registers and occupancy
+  const KernelInfo* ki = m4rm_kernel_at(index);
+  if (field) *field = ki->field;
+  if (k) *k = ki->k;
+  if (rows_per_thread) *rows_per_thread = ki->rt;
+  if (threads) *threads = ki->threads;
+  if (schedule) *schedule = ki->sched;
+  if (occupancy) *occupancy = ki->occupancy;
+  if (regs) *regs = ki->regs;
+  if (smem_bytes) *smem_bytes = ki->smem_bytes;
+  cudaSetDevice(cur);
+  return count;
+}
 
 int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads) {
   std::lock_guard<std::mutex> lk(g_mu);

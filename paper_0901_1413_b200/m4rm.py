@@ -153,6 +153,21 @@ def set_timing(enable: bool):
     _lib.check(_lib.load().sg_set_timing(1 if enable else 0))
 
 
+def kernel_info(device: int = 0) -> list:
+    """Every compiled M4RM instantiation: field code, k, rows per thread, lookup threads,
+    schedule, CTAs per SM, registers per thread, dynamic shared memory bytes."""
+    L = _lib.load()
+    out, i = [], 0
+    while True:
+        v = [ctypes.c_int() for _ in range(8)]
+        n = L.sg_kernel_info(i, device, *(ctypes.byref(x) for x in v))
+        if n < 0:
+            return out
+        out.append(dict(zip(("field", "k", "rt", "threads", "schedule", "occupancy", "regs", "smem_bytes"),
+                            (x.value for x in v)), index=i))
+        i += 1
+
+
 def launch_count() -> int:
     return int(_lib.load().sg_launch_count())
 

@@ -50,6 +50,7 @@ def test_invalid_arguments_are_rejected_before_cuda():
     rc = L.sg_m4rm(1, vp(1), vp(1), vp(1), -1, 4, 4, 8, None, 0, None)
     assert rc == _lib.SG_EINVAL
     assert L.sg_plane_op(99, None, None, 1, 1, 0, 0, None) == _lib.SG_EINVAL
+    assert L.sg_kernel_info(-1, 0, None, None, None, None, None, None, None, None) == -1
     assert L.sg_pack(1, None, 2, 5, 3, None, None) == _lib.SG_EINVAL  # ld < n
     with pytest.raises(ValueError):
         _lib.check(_lib.SG_EINVAL)

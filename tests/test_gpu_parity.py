@@ -516,3 +516,13 @@ def test_extreme_aspect_ratios(fname):
         B = oracle.random_dense(fname, l, n, n + 2)
         C = gpu_multiply(fname, A, B)
         assert np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, m, l, n)
+
+
+def test_kernel_info_registry():
+    """sg_kernel_info: every field has k = 1..8 instantiations that fit on the B200, and the
+    warp-specialized ones launch 128 builder threads on top of the lookup threads."""
+    info = m4rm_mod.kernel_info(0)
+    assert info and all(i["occupancy"] >= 1 and i["regs"] > 0 for i in info if i["k"] == 8)
+    for code in range(8):
+        assert {i["k"] for i in info if i["field"] == code} == set(range(1, 9))
+    assert any(i["schedule"] == 2 for i in info)

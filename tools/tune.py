@@ -21,6 +21,7 @@ ap.add_argument("--rts", default="1,2,4,8,16")
 ap.add_argument("--splits", default="-1,1,2,4,8,16")  # -1 = stream-K
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
+KINFO = M.kernel_info(0)
 L = _lib.load()
 variants = set()
 import ctypes  # noqa: E402
@@ -57,8 +58,10 @@ for name, field, m, l, n in jobs:
                         torch.cuda.synchronize()
                         ts.append(e0.elapsed_time(e1))
                     ms = min(ts)
-                    rec = {"config": name, "rt": rt, "threads": nt, "pipe": pipe, "splits": sp, "ms": ms,
-                           "muladds_per_s": m * l * n / ms * 1e3, "ctas": p["ctas"]}
+                    ki = KINFO[p["kernel"]]
+                    rec = {"config": name, "field": field, "m": m, "l": l, "n": n, "rt": rt, "threads": nt,
+                           "pipe": pipe, "splits": sp, "ms": ms, "muladds_per_s": m * l * n / ms * 1e3,
+                           "ctas": p["ctas"], "occ": ki["occupancy"], "regs": ki["regs"]}
                     print(json.dumps(rec), flush=True)
                     if best is None or ms < best["ms"]:
                         best = rec
