@@ -58,6 +58,10 @@ for _f in sorted(os.listdir(os.path.join(ROOT, "profiles"))) if os.path.isdir(os
     if _f.endswith("_pipes.json"):
         with open(os.path.join(ROOT, "profiles", _f)) as _fh:
             PIPES.update(json.load(_fh))
+MEASURED = {}
+if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as _fh:
+        MEASURED = json.load(_fh)
 METRIC = "field mul-adds/sec (m*l*n/t) for C=A*B over F3/F5/F7/GF(4), % of roofline"
 UNIT = "mul-adds/s"
 
@@ -260,6 +264,51 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
     return out
 
 
+def run_pack_unpack(device, field="f3", m=16384, n=32768, reps=5):
+    """HBM roofline of the pack / unpack kernels (dense uint8 residues <-> bit planes) on a matrix
+    larger than L2: algorithmic bytes = m n (1 + R/8) per call, against MEASURED_PEAKS.json."""
+    import ctypes
+
+    import torch
+    import paper_0901_1413_b200 as sg
+    from paper_0901_1413_b200 import _lib
+
+    L = _lib.load()
+    f = sg.by_name(field)
+    dense = torch.randint(0, ORDER[field], (m, n), dtype=torch.uint8, device=device)
+    planes = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64, device=device)
+    out = torch.empty_like(dense)
+    st = _lib.current_stream_handle(device)
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    pack = lambda: _lib.check(L.sg_pack(f.code, vp(dense), m, n, n, vp(planes), st))  # noqa: E731
+    unpack = lambda: _lib.check(L.sg_unpack(f.code, vp(planes), m, n, vp(out), n, st))  # noqa: E731
+    res = {}
+    for name, fn in (("pack", pack), ("unpack", unpack)):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[name + "_ms"] = min(ts)
+    assert torch.equal(out, dense), "pack/unpack round trip"
+    nbytes = m * n * (1 + f.bits / 8.0)
+    peak = MEASURED.get("hbm_gbs")
+    for name in ("pack", "unpack"):
+        res[name + "_gbps"] = nbytes / (res[name + "_ms"] * 1e-3) / 1e9
+        res[name + "_frac"] = res[name + "_gbps"] / peak if peak else None
+    res.update({"workload": f"{field.upper()} {m}x{n} dense uint8 <-> {f.bits} planes",
+                "bytes_per_call": nbytes, "peak_gbps": peak,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+                "note": "each call includes the range-check flag read-back (a few us)"})
+    del dense, planes, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_e2e(f, A, B, m, l, n, args, world, device):
     """Same metric end to end through the public API with host buffers (pinned memory).
 
@@ -449,6 +498,7 @@ def main():
                                   "kernel_ms": r["roofline"]["kernel_ms"],
                                   "achieved_muladds_per_s": r["roofline"]["achieved_muladds_per_s"],
                                   "plan": r["plan"], "clocks": r["clocks"]}
+    pack_unpack = run_pack_unpack(device) if not args.no_per_config else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         name, field, m, l, n = head
@@ -471,7 +521,7 @@ def main():
                            "l2": "flushed (256 MiB write) before every timed step"},
                 "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
                 "roofline": res["roofline"], "plan": res["plan"], "cpu_baseline": cpu,
-                "peaks_probe": peaks, "per_config": per_config}
+                "peaks_probe": peaks, "per_config": per_config, "pack_unpack": pack_unpack}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -8,6 +8,8 @@
 //                        and build_table for callers of the _core API.
 // Layout everywhere: planes [R][rows][W64] uint64, column c -> word c>>6, bit c&63;
 // viewed as 32-bit words, column c -> word c>>5, bit c&31 (little endian).
+#include <algorithm>
+
 #include "sg_field.cuh"
 #include "sg_internal.h"
 
@@ -34,95 +36,120 @@ __device__ __forceinline__ u32 gather_bit(u32 x, int d) {
 // nibble -> one 0/1 byte per bit (bit i -> byte i)
 __device__ __forceinline__ u32 spread_nibble(u32 nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
-// One thread per (row, 32-bit plane word): 32 consecutive dense bytes -> R plane words.
-__global__ void pack_kernel(int field, const uint8_t* __restrict__ dense, int64_t m, int64_t n,
-                            int64_t ld, u32* __restrict__ planes, int wc32, int* err) {
-  const int R = planes_of(field);
-  const int order = order_of(field);
-  const int64_t total = m * wc32;
-  const u32 lim = 0x01010101u * (u32)order;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / wc32;
-    const int w = (int)(i % wc32);
-    const int64_t c0 = (int64_t)w * 32;
-    const uint8_t* src = dense + row * ld + c0;
-    u32 x[8];
-    const bool full = c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-    if (full) {
-      const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
-      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        u32 v = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int64_t c = c0 + 4 * q + b;
-          if (c < n) v |= (u32)src[4 * q + b] << (8 * b);
-        }
-        x[q] = v;
-      }
-    }
-    bool bad = false;
-    u32 p0 = 0, p1 = 0, p2 = 0;
+// Pack / unpack: thread (blockIdx.x * 256 + threadIdx.x) owns 32-bit plane word w of every
+// row blockIdx.y, blockIdx.y + gridDim.y, ... (2-D grid: no 64-bit index division), two rows per
+// iteration with both rows' loads issued first.  Field-templated (constant plane count).
+template <int F>
+__device__ __forceinline__ void pack_word(const uint8_t* __restrict__ src, bool full, int64_t c0, int64_t n,
+                                          u32 (&p)[3], bool& bad) {
+  constexpr int R = F == F2 ? 1 : (F == F5 || F == F7 || F == GF8 || F == Z8) ? 3 : 2;
+  constexpr u32 order = F == F2 ? 2 : F == F3 ? 3 : F == F5 ? 5 : F == F7 ? 7 : (F == GF4 || F == Z4) ? 4 : 8;
+  u32 x[8];
+  if (full) {
+    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(src)), b = __ldcs(reinterpret_cast<const uint4*>(src) + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      u32 v = x[q];
-      bad |= __vcmpgeu4(v, lim) != 0u;
-      if (field == F3) v = ((v | (v >> 1)) & 0x01010101u) | (v & 0x02020202u);  // 1->01, 2->11
-      p0 |= gather_bit(v, 0) << (4 * q);
-      if (R > 1) p1 |= gather_bit(v, 1) << (4 * q);
-      if (R > 2) p2 |= gather_bit(v, 2) << (4 * q);
-    }
-    if (bad) atomicOr(err, 1);
-    planes[row * wc32 + w] = p0;
-    if (R > 1) planes[(m + row) * wc32 + w] = p1;
-    if (R > 2) planes[(2 * m + row) * wc32 + w] = p2;
-  }
-}
-
-// One thread per (row, 32-bit plane word): R plane words -> 32 dense residues.
-__global__ void unpack_kernel(int field, const u32* __restrict__ planes, int64_t m, int64_t n,
-                              uint8_t* __restrict__ dense, int64_t ld, int wc32, int* err) {
-  const int R = planes_of(field);
-  const int64_t total = m * wc32;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / wc32;
-    const int w = (int)(i % wc32);
-    const int64_t c0 = (int64_t)w * 32;
-    if (c0 >= n) continue;
-    const u32 p0 = planes[row * wc32 + w];
-    const u32 p1 = R > 1 ? planes[(m + row) * wc32 + w] : 0u;
-    const u32 p2 = R > 2 ? planes[(2 * m + row) * wc32 + w] : 0u;
-    u32 x[8];
-    bool bad = false;
+      u32 v = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const u32 b0 = spread_nibble((p0 >> (4 * q)) & 0xFu);
-      const u32 b1 = spread_nibble((p1 >> (4 * q)) & 0xFu);
-      const u32 b2 = spread_nibble((p2 >> (4 * q)) & 0xFu);
-      u32 v;
-      if (field == F3) {
-        bad |= (b1 & ~b0) != 0u;  // sign without unit: illegal (fields.py:88-101)
-        v = b0 + b1;
-      } else {
-        v = b0 | (b1 << 1) | (b2 << 2);
-        if (field == F5) v = __vsub4(v, __vcmpgeu4(v, 0x05050505u) & 0x05050505u);
-        if (field == F7) v = __vsub4(v, __vcmpeq4(v, 0x07070707u) & 0x07070707u);
+      for (int b = 0; b < 4; ++b) {
+        const int64_t c = c0 + 4 * q + b;
+        if (c < n) v |= (u32)src[4 * q + b] << (8 * b);
       }
       x[q] = v;
     }
-    if (bad) atomicOr(err, 2);
-    uint8_t* dst = dense + row * ld + c0;
-    if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-      reinterpret_cast<uint4*>(dst)[0] = make_uint4(x[0], x[1], x[2], x[3]);
-      reinterpret_cast<uint4*>(dst)[1] = make_uint4(x[4], x[5], x[6], x[7]);
-    } else {
-      for (int c = 0; c < 32 && c0 + c < n; ++c) dst[c] = (uint8_t)(x[c >> 2] >> (8 * (c & 3)));
+  }
+  p[0] = p[1] = p[2] = 0u;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    u32 v = x[q];
+    bad |= __vcmpgeu4(v, 0x01010101u * order) != 0u;
+    if constexpr (F == F3) v = ((v | (v >> 1)) & 0x01010101u) | (v & 0x02020202u);  // 1->01, 2->11
+    p[0] |= gather_bit(v, 0) << (4 * q);
+    if constexpr (R > 1) p[1] |= gather_bit(v, 1) << (4 * q);
+    if constexpr (R > 2) p[2] |= gather_bit(v, 2) << (4 * q);
+  }
+}
+
+template <int F>
+__global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ dense, int64_t m, int64_t n,
+                                                   int64_t ld, u32* __restrict__ planes, int wc32, int* err) {
+  constexpr int R = F == F2 ? 1 : (F == F5 || F == F7 || F == GF8 || F == Z8) ? 3 : 2;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= wc32) return;
+  const int64_t c0 = (int64_t)w * 32;
+  bool bad = false;
+  const int64_t step = gridDim.y;
+  for (int64_t row = blockIdx.y; row < m; row += 2 * step) {
+    const int64_t row2 = row + step;
+    const uint8_t* s1 = dense + row * ld + c0;
+    const uint8_t* s2 = dense + row2 * ld + c0;
+    const bool al = c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(s1) & 15) == 0) && (ld & 15) == 0;
+    u32 p1[3], p2[3];
+    pack_word<F>(s1, al, c0, n, p1, bad);
+    if (row2 < m) pack_word<F>(s2, al, c0, n, p2, bad);
+#pragma unroll
+    for (int d = 0; d < R; ++d) {
+      __stcs(planes + ((int64_t)d * m + row) * wc32 + w, p1[d]);
+      if (row2 < m) __stcs(planes + ((int64_t)d * m + row2) * wc32 + w, p2[d]);
     }
   }
+  if (bad) atomicOr(err, 1);
+}
+
+template <int F>
+__device__ __forceinline__ void unpack_word(const u32 (&p)[3], u32 (&x)[8], bool& bad) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const u32 b0 = spread_nibble((p[0] >> (4 * q)) & 0xFu);
+    const u32 b1 = spread_nibble((p[1] >> (4 * q)) & 0xFu);
+    const u32 b2 = spread_nibble((p[2] >> (4 * q)) & 0xFu);
+    u32 v;
+    if constexpr (F == F3) {
+      bad |= (b1 & ~b0) != 0u;  // sign without unit: illegal (fields.py:88-101)
+      v = b0 + b1;
+    } else {
+      v = b0 | (b1 << 1) | (b2 << 2);
+      if constexpr (F == F5) v = __vsub4(v, __vcmpgeu4(v, 0x05050505u) & 0x05050505u);
+      if constexpr (F == F7) v = __vsub4(v, __vcmpeq4(v, 0x07070707u) & 0x07070707u);
+    }
+    x[q] = v;
+  }
+}
+
+template <int F>
+__global__ void __launch_bounds__(256) unpack_kernel(const u32* __restrict__ planes, int64_t m, int64_t n,
+                                                     uint8_t* __restrict__ dense, int64_t ld, int wc32, int* err) {
+  constexpr int R = F == F2 ? 1 : (F == F5 || F == F7 || F == GF8 || F == Z8) ? 3 : 2;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c0 = (int64_t)w * 32;
+  if (w >= wc32 || c0 >= n) return;
+  bool bad = false;
+  const int64_t step = gridDim.y;
+  for (int64_t row = blockIdx.y; row < m; row += 2 * step) {
+    const int64_t row2 = row + step;
+    u32 p1[3] = {0u, 0u, 0u}, p2[3] = {0u, 0u, 0u};
+#pragma unroll
+    for (int d = 0; d < R; ++d) {
+      p1[d] = __ldcs(planes + ((int64_t)d * m + row) * wc32 + w);
+      if (row2 < m) p2[d] = __ldcs(planes + ((int64_t)d * m + row2) * wc32 + w);
+    }
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = h ? row2 : row;
+      if (r >= m) break;
+      u32 x[8];
+      unpack_word<F>(h ? p2 : p1, x, bad);
+      uint8_t* dst = dense + r * ld + c0;
+      if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        __stcs(reinterpret_cast<uint4*>(dst), make_uint4(x[0], x[1], x[2], x[3]));
+        __stcs(reinterpret_cast<uint4*>(dst) + 1, make_uint4(x[4], x[5], x[6], x[7]));
+      } else {
+        for (int c = 0; c < 32 && c0 + c < n; ++c) dst[c] = (uint8_t)(x[c >> 2] >> (8 * (c & 3)));
+      }
+    }
+  }
+  if (bad) atomicOr(err, 2);
 }
 
 __global__ void canonicalize_kernel(int field, uint64_t* __restrict__ p, int64_t n_words) {
@@ -408,12 +435,22 @@ static unsigned grid_for(int64_t work, int threads) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
+// 2-D grid for pack / unpack: x covers the words of a row, y strides over rows (~16 CTAs per SM)
+static dim3 grid_2d(int64_t m, int wc32) {
+  const unsigned gx = (unsigned)((wc32 + 255) / 256);
+  int64_t gy = (148 * 16 + gx - 1) / gx;
+  gy = std::min<int64_t>(std::max<int64_t>(gy, 1), std::min<int64_t>(m, 65535));
+  return dim3(gx, (unsigned)std::max<int64_t>(gy, 1));
+}
+
 cudaError_t launch_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld,
                         uint64_t* planes, int* err, cudaStream_t st) {
   const int wc32 = (int)(2 * ((n + 63) / 64));
   if (m == 0 || wc32 == 0) return cudaSuccess;
-  pack_kernel<<<grid_for(m * wc32, 256), 256, 0, st>>>(field, dense, m, n, ld,
-                                                        reinterpret_cast<u32*>(planes), wc32, err);
+#define SG_PK(FF) pack_kernel<FF><<<grid_2d(m, wc32), 256, 0, st>>>(dense, m, n, ld, reinterpret_cast<u32*>(planes), \
+                                                                   wc32, err)
+  SG_FOR_EACH_FIELD_CASE(field, SG_PK)
+#undef SG_PK
   return cudaGetLastError();
 }
 
@@ -421,8 +458,10 @@ cudaError_t launch_unpack(int field, const uint64_t* planes, int64_t m, int64_t 
                           int64_t ld, int* err, cudaStream_t st) {
   const int wc32 = (int)(2 * ((n + 63) / 64));
   if (m == 0 || wc32 == 0) return cudaSuccess;
-  unpack_kernel<<<grid_for(m * wc32, 256), 256, 0, st>>>(field, reinterpret_cast<const u32*>(planes), m, n,
-                                                          dense, ld, wc32, err);
+#define SG_UPK(FF) unpack_kernel<FF><<<grid_2d(m, wc32), 256, 0, st>>>(reinterpret_cast<const u32*>(planes), m, n, \
+                                                                      dense, ld, wc32, err)
+  SG_FOR_EACH_FIELD_CASE(field, SG_UPK)
+#undef SG_UPK
   return cudaGetLastError();
 }
 
