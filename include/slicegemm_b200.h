@@ -18,6 +18,8 @@
  *   sg_m4rm                  m4rm_multiply(A, B, params) (__init__.py:16), and
  *                            for SG_GF4 ext_multiply over F4 (__init__.py:17)
  *   sg_m4rm_host             the same with host buffers (the call a CPU caller makes)
+ *   sg_m4rm_multi            the same over several GPUs of one process (rows sharded, B
+ *                            replicated; the reference's row0/row1 partition)
  *   sg_classical             classical_multiply (__init__.py:16)
  *
  * Data layout (identical bits to the reference's BitslicedMatrix planes):
@@ -128,6 +130,14 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
 /* Same with host buffers: copies in, multiplies on `device`, copies C back; synchronous. */
 int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
                  int64_t l, int64_t n, int k, int device);
+
+/* Multi-GPU from one process: rows of A and C are split into ngpus contiguous
+ * balanced slabs, B goes up once to devices[0] and is replicated to the other devices by peer
+ * copies (NVLink / NVSwitch), each device multiplies its slab, and the C slabs come back into
+ * the host buffer.  Host buffers as in sg_m4rm_host; synchronous.  The inner dimension is
+ * never split, so C is bit-identical for any device list (devices may repeat). */
+int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
+                  int64_t l, int64_t n, int k, int ngpus, const int* devices);
 
 /* classical_multiply: the table-free row-accumulate product, a cross-check
  * (O(m l n / 32) word operations); canonical output, same layout as sg_m4rm. */

@@ -868,6 +868,113 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   return SG_OK;
 }
 
+int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
+                  int k, int ngpus, const int* devices) {
+  int rc = check_mul_args(field, A, B, C, m, l, n, k);
+  if (rc != SG_OK) return rc;
+  if (ngpus < 1 || ngpus > 64 || !devices) return fail(SG_EINVAL, "need 1..64 devices");
+  int ndev = 0;
+  SG_CUDA(cudaGetDeviceCount(&ndev), "sg_m4rm_multi device count");
+  for (int g = 0; g < ngpus; ++g)
+    if (devices[g] < 0 || devices[g] >= ndev) return fail(SG_EINVAL, "device index out of range");
+  if (m == 0 || n == 0) return SG_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  const int R = planes(field);
+  const int64_t wa = w64_of(l), wc = w64_of(n);
+  const size_t b_bytes = (size_t)R * l * wc * 8;
+  struct Dev {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    Buf buf;
+  };
+  static std::map<int, Dev> state;
+  static std::mutex multi_mu;
+  std::lock_guard<std::mutex> busy(multi_mu);  // one multi-device product at a time
+  // per distinct device: B, then the A and C slabs of every shard it runs
+  std::map<int, size_t> need;
+  std::vector<int64_t> r0(ngpus), r1(ngpus);
+  for (int g = 0; g < ngpus; ++g) {
+    r0[g] = m * g / ngpus;
+    r1[g] = m * (g + 1) / ngpus;
+    need[devices[g]] += ((size_t)R * (r1[g] - r0[g]) * (wa + wc) * 8 + 2 * 256);
+  }
+  for (auto& kv : need) {
+    kv.second += b_bytes + 256;
+    Dev& d = state[kv.first];
+    SG_CUDA(cudaSetDevice(kv.first), "sg_m4rm_multi set device");
+    if (!d.st) {
+      SG_CUDA(cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking), "sg_m4rm_multi stream");
+      SG_CUDA(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming), "sg_m4rm_multi event");
+    }
+    if (d.buf.bytes < kv.second) {
+      if (d.buf.p) {
+        cudaDeviceSynchronize();
+        cudaFree(d.buf.p);
+      }
+      d.buf.p = nullptr;
+      d.buf.bytes = 0;
+      SG_CUDA(cudaMalloc(&d.buf.p, kv.second), "sg_m4rm_multi alloc");
+      d.buf.bytes = kv.second;
+    }
+  }
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  // B: host -> devices[0], then peer copies to every other device (one hop each over NVSwitch)
+  const int d0 = devices[0];
+  uint64_t* B0 = (uint64_t*)state[d0].buf.p;
+  SG_CUDA(cudaSetDevice(d0), "sg_m4rm_multi set device");
+  if (b_bytes) SG_CUDA(cudaMemcpyAsync(B0, B, b_bytes, cudaMemcpyHostToDevice, state[d0].st), "sg_m4rm_multi H2D B");
+  SG_CUDA(cudaEventRecord(state[d0].ev, state[d0].st), "sg_m4rm_multi event");
+  for (auto& kv : need) {
+    if (kv.first == d0 || !b_bytes) continue;
+    Dev& d = state[kv.first];
+    SG_CUDA(cudaSetDevice(kv.first), "sg_m4rm_multi set device");
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, kv.first, d0);
+    if (can) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(d0, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "sg_m4rm_multi peer access");
+      cudaGetLastError();
+    }
+    SG_CUDA(cudaStreamWaitEvent(d.st, state[d0].ev, 0), "sg_m4rm_multi wait");
+    SG_CUDA(cudaMemcpyPeerAsync(d.buf.p, kv.first, B0, d0, b_bytes, d.st), "sg_m4rm_multi peer copy B");
+  }
+  // shards: A rows up, multiply, C rows down (each device's stream; shards on one device in order)
+  std::map<int, size_t> offset;
+  for (auto& kv : need) offset[kv.first] = up(b_bytes);
+  for (int g = 0; g < ngpus; ++g) {
+    const int dv = devices[g];
+    Dev& d = state[dv];
+    const int64_t rows = r1[g] - r0[g];
+    if (rows == 0) continue;
+    SG_CUDA(cudaSetDevice(dv), "sg_m4rm_multi set device");
+    char* base = (char*)d.buf.p;
+    uint64_t* dB = (uint64_t*)base;
+    uint64_t* dA = (uint64_t*)(base + offset[dv]);
+    offset[dv] += up((size_t)R * rows * wa * 8);
+    uint64_t* dC = (uint64_t*)(base + offset[dv]);
+    offset[dv] += up((size_t)R * rows * wc * 8);
+    if (wa)
+      SG_CUDA(cudaMemcpy2DAsync(dA, rows * wa * 8, A + r0[g] * wa, m * wa * 8, rows * wa * 8, R,
+                                cudaMemcpyHostToDevice, d.st),
+              "sg_m4rm_multi H2D A");
+    rc = sg_m4rm(field, dA, dB, dC, rows, l, n, k, nullptr, 0, d.st);
+    if (rc != SG_OK) {
+      cudaSetDevice(cur);
+      return rc;
+    }
+    SG_CUDA(cudaMemcpy2DAsync(C + r0[g] * wc, m * wc * 8, dC, rows * wc * 8, rows * wc * 8, R,
+                              cudaMemcpyDeviceToHost, d.st),
+            "sg_m4rm_multi D2H C");
+  }
+  for (auto& kv : need) {
+    SG_CUDA(cudaSetDevice(kv.first), "sg_m4rm_multi set device");
+    SG_CUDA(cudaStreamSynchronize(state[kv.first].st), "sg_m4rm_multi sync");
+  }
+  cudaSetDevice(cur);
+  return SG_OK;
+}
+
 int sg_build_table(int field, const uint64_t* const* B, int64_t b_rows, int64_t row_base, int kp, int64_t words,
                    uint64_t* const* T, void* stream) {
   if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");

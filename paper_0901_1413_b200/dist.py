@@ -104,6 +104,33 @@ def sharded_multiply(A_shard: BitslicedMatrix, B: BitslicedMatrix, field, l: int
     return C, B_local
 
 
+def multi_device_multiply(A: BitslicedMatrix, B: BitslicedMatrix, devices, params=None) -> BitslicedMatrix:
+    """C = A B over several GPUs from ONE process (sg_m4rm_multi): rows of A / C sharded over
+    `devices` (indices may repeat), B replicated by peer copies.  A and B are host matrices;
+    C comes back on the host, bit-identical to the single-GPU product."""
+    import ctypes
+
+    from . import _lib
+    from .m4rm import choose_k
+    from .matrix import _vp
+    if A.field is not B.field:
+        raise ValueError("field mismatch")
+    if A.ncols != B.nrows:
+        raise ValueError(f"inner dimensions {A.ncols} != {B.nrows}")
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise ValueError("need at least one device")
+    m, l, n = A.nrows, A.ncols, B.ncols
+    k = (params.k if params is not None and params.k is not None else None) or choose_k(l)
+    a = A.planes.cpu().contiguous()
+    b = B.planes.cpu().contiguous()
+    C = BitslicedMatrix.zero(A.field, m, n, device="cpu")
+    devs = (ctypes.c_int * len(devices))(*devices)
+    _lib.check(_lib.load().sg_m4rm_multi(A.field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k, len(devices),
+                                         devs))
+    return C
+
+
 def gather_rows(C_shard: BitslicedMatrix, m: int, group=None) -> BitslicedMatrix:
     """All-gather row shards into the full C (verification only; not on the timed path)."""
     world = dist.get_world_size(group)

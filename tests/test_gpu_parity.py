@@ -526,3 +526,21 @@ def test_kernel_info_registry():
     for code in range(8):
         assert {i["k"] for i in info if i["field"] == code} == set(range(1, 9))
     assert any(i["schedule"] == 2 for i in info)
+
+
+def test_multi_device_entry_point():
+    """sg_m4rm_multi (one process, several devices; here device 0 listed 1-3 times, i.e. the
+    sharding, the B replication and the row reassembly on one GPU): bit-identical to the oracle."""
+    from paper_0901_1413_b200 import dist as sgdist
+    for fname in ("f3", "f5", "f7", "gf4"):
+        m, l, n = 1001, 777, 300
+        A = oracle.random_dense(fname, m, l, 11)
+        B = oracle.random_dense(fname, l, n, 12)
+        want = expect(fname, A, B)
+        Ah = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, A), l, device="cpu")
+        Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), n, device="cpu")
+        for devs in ([0], [0, 0], [0, 0, 0]):
+            C = sgdist.multi_device_multiply(Ah, Bh, devs)
+            assert np.array_equal(C.planes_numpy(), want), (fname, devs)
+    with pytest.raises(ValueError):
+        sgdist.multi_device_multiply(Ah, Bh, [99])
