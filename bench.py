@@ -521,6 +521,9 @@ def main():
                            "l2": "flushed (256 MiB write) before every timed step"},
                 "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
                 "roofline": res["roofline"], "plan": res["plan"], "cpu_baseline": cpu,
+                "step_breakdown_ms": {"index_prepass": res["transpose_ms"], "m4rm": res["roofline"]["kernel_ms"],
+                                      "reduce": res["reduce_ms"],
+                                      "note": "events around each launch (serialised, sg_set_timing)"},
                 "peaks_probe": peaks, "per_config": per_config, "pack_unpack": pack_unpack}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // sg_m4rm.cu -- pre-pass, split-K reduction and launch glue around the M4RM kernel
 // (kernel template: sg_m4rm_kernel.cuh; per-field instantiations: sg_m4rm_<field>.cu).
@@ -88,16 +89,21 @@ __global__ void index_words_kernel(const u32* __restrict__ A, u32* __restrict__ 
 }
 
 // ------------------------------------------------------------------ split-K reduction
+__device__ __forceinline__ u32 comp4(const uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
+__device__ __forceinline__ void set4(uint4& v, int w, u32 x) {
+  if (w == 0) v.x = x; else if (w == 1) v.y = x; else if (w == 2) v.z = x; else v.w = x;
+}
+
 template <int F>
-__global__ void reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict__ C, int64_t m,
-                                     int64_t mpad, int wc32, int splits) {
+__global__ void __launch_bounds__(256) reduce_splits_kernel(const u32* __restrict__ P, u32* __restrict__ C, int64_t m,
+                                                            int64_t mpad, int wc32, int splits) {
   constexpr int R = Traits<F>::R;
   pdl_wait();  // launched with PDL behind the product kernel
-  const int64_t total = m * wc32;
+  // thread x: word w of rows blockIdx.y, blockIdx.y + gridDim.y, ... (no index division)
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= wc32) return;
   const int64_t plane = mpad * (int64_t)wc32;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / wc32, w = i % wc32;
+  for (int64_t row = blockIdx.y; row < m; row += gridDim.y) {
     const int64_t off = row * wc32 + w;
     V<F> acc;
 #pragma unroll
@@ -157,51 +163,86 @@ cudaError_t launch_sum_slices(int field, const SliceSet& s, uint32_t* out, int64
 // [t nb, (t+1) nb), canonicalized.  One thread per (tile row, word); slots are summed in CTA
 // order (the field sums are exact, so any order gives the same bits).
 template <int F>
-__global__ void reduce_streamk_kernel(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m, int wc32,
-                                      int rows_cta, int slabs, int64_t tiles, int nb, int64_t U, int G) {
+__global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m,
+                                                             int wc32, int rows_cta, int slabs, int64_t tiles, int nb,
+                                                             int64_t U, int G) {
   constexpr int R = Traits<F>::R;
   pdl_wait();  // launched with PDL behind the product kernel
-  const int64_t per_tile = (int64_t)rows_cta * SLAB_WORDS;
-  const int64_t total = tiles * per_tile;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / per_tile;
-    const int lr = (int)((i % per_tile) / SLAB_WORDS), w = (int)(i % SLAB_WORDS);
-    const int64_t row = (t / slabs) * rows_cta + lr;
-    const int word = (int)(t % slabs) * SLAB_WORDS + w;
-    if (row >= m || word >= wc32) continue;
+  // blockIdx.x = tile; the CTAs whose unit ranges touch it are found once per block
+  const int64_t t = blockIdx.x;
+  __shared__ int c_range[2];
+  if (threadIdx.x == 0) {
     const int64_t lo = t * nb, hi = lo + nb;
     int64_t c = lo * G / U;
     while (c > 0 && c * U / G > lo) --c;
     while ((c + 1) * U / G <= lo) ++c;
-    V<F> acc;
+    int64_t c1 = c;
+    while (c1 + 1 < G && (c1 + 1) * U / G < hi) ++c1;
+    c_range[0] = (int)c;
+    c_range[1] = (int)c1;
+  }
+  __syncthreads();
+  const int c0 = c_range[0], c1 = c_range[1];
+  const int64_t row0 = (t / slabs) * rows_cta;
+  const int word0 = (int)(t % slabs) * SLAB_WORDS;
+  for (int lr = blockIdx.y * blockDim.x + threadIdx.x; lr < rows_cta; lr += gridDim.y * blockDim.x) {
+    const int64_t row = row0 + lr;
+    if (row >= m) break;
+    uint4 acc[R];
+    bool first = true;
+    for (int c = c0; c <= c1; ++c) {
+      const int64_t u0 = (int64_t)c * U / G;
+      if ((int64_t)(c + 1) * U / G == u0) continue;  // an empty range owns no slot
+      const int64_t slot = (int64_t)c * SK_SEGS + (t - u0 / nb);
+      uint4 x[R];
 #pragma unroll
-    for (int d = 0; d < R; ++d) acc.p[d] = 0u;
-    for (; c < G && c * U / G < hi; ++c) {
-      const int64_t u0 = c * U / G;
-      if ((c + 1) * U / G == u0) continue;  // an empty range owns no slot
-      const int seg = (int)(t - u0 / nb);
-      const int64_t slot = c * SK_SEGS + seg;
-      V<F> x;
+      for (int d = 0; d < R; ++d) x[d] = *reinterpret_cast<const uint4*>(P2 + ((slot * R + d) * rows_cta + lr) * 4);
+      if (first) {
 #pragma unroll
-      for (int d = 0; d < R; ++d) x.p[d] = P2[((slot * R + d) * rows_cta + lr) * SLAB_WORDS + w];
-      vadd<F>(acc, x);
+        for (int d = 0; d < R; ++d) acc[d] = x[d];
+        first = false;
+        continue;
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        V<F> a, b;
+#pragma unroll
+        for (int d = 0; d < R; ++d) {
+          a.p[d] = comp4(acc[d], w);
+          b.p[d] = comp4(x[d], w);
+        }
+        vadd<F>(a, b);
+#pragma unroll
+        for (int d = 0; d < R; ++d) set4(acc[d], w, a.p[d]);
+      }
     }
-    vcanon<F>(acc);
 #pragma unroll
-    for (int d = 0; d < R; ++d) C[(d * m + row) * (int64_t)wc32 + word] = acc.p[d];
+    for (int w = 0; w < 4; ++w) {
+      V<F> a;
+#pragma unroll
+      for (int d = 0; d < R; ++d) a.p[d] = comp4(acc[d], w);
+      vcanon<F>(a);
+#pragma unroll
+      for (int d = 0; d < R; ++d) set4(acc[d], w, a.p[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < R; ++d) {
+      u32* dst = C + ((int64_t)d * m + row) * wc32 + word0;
+      if (word0 + 4 <= wc32 && (wc32 & 3) == 0) {
+        *reinterpret_cast<uint4*>(dst) = acc[d];
+      } else {
+        for (int w = 0; w < 4 && word0 + w < wc32; ++w) dst[w] = comp4(acc[d], w);
+      }
+    }
   }
 }
 
 cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,
                                   int slabs, int64_t tiles, int nblocks, int64_t units, int ctas, cudaStream_t st) {
-  const int64_t total = tiles * rows_cta * SLAB_WORDS;
-  const int threads = 256;
-  int64_t blocks = (total + threads - 1) / threads;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-#define SG_RK(FF) return launch_pdl(reduce_streamk_kernel<FF>, dim3((unsigned)blocks), dim3(threads), 0, st, P2, C, m, \
-                                 wc32, rows_cta, slabs, tiles, nblocks, units, ctas)
+  if (tiles <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)tiles, (unsigned)((rows_cta + 255) / 256));
+#define SG_RK(FF) return launch_pdl(reduce_streamk_kernel<FF>, grid, dim3(256), 0, st, P2, C, m, wc32, rows_cta, \
+                                 slabs, tiles, nblocks, units, ctas)
   SG_FOR_EACH_FIELD_CASE(field, SG_RK)
 #undef SG_RK
   return cudaGetLastError();
@@ -262,13 +303,11 @@ cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT
 
 cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int64_t m, int64_t mpad,
                                  int wc32, int splits, cudaStream_t st) {
-  const int64_t total = m * wc32;
-  const int threads = 256;
-  int64_t blocks = (total + threads - 1) / threads;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-#define SG_RS(FF) return launch_pdl(reduce_splits_kernel<FF>, dim3((unsigned)blocks), dim3(threads), 0, st, P, C, m, mpad, \
-                                 wc32, splits)
+  if (m <= 0 || wc32 <= 0) return cudaSuccess;
+  const unsigned gx = (unsigned)((wc32 + 255) / 256);
+  const int64_t gy = std::min<int64_t>(std::min<int64_t>(m, 65535), std::max<int64_t>(1, (148 * 16 + gx - 1) / gx));
+  const dim3 grid(gx, (unsigned)gy);
+#define SG_RS(FF) return launch_pdl(reduce_splits_kernel<FF>, grid, dim3(256), 0, st, P, C, m, mpad, wc32, splits)
   SG_FOR_EACH_FIELD_CASE(field, SG_RS)
 #undef SG_RS
   return cudaGetLastError();
