@@ -73,7 +73,7 @@ OWN_LOP3_PER_MULADD = {"f2": 1 / 256, "f3": 6 / 256, "f5": 20 / 256, "f7": 18 / 
 SMEM_PER_MULADD = {"f2": 4 / 256, "f3": 16 / 256, "f5": 36 / 256, "f7": 36 / 256, "gf4": 16 / 256}
 TABLE_LOP3_PER_WORD = {"f2": 1, "f3": 5, "f5": 12, "f7": 10, "gf4": 2}  # one field add, 32-bit word
 PLANES = {"f2": 1, "f3": 2, "f5": 3, "f7": 3, "gf4": 2}
-ORDER = {"f2": 2, "f3": 3, "f5": 5, "f7": 7, "gf4": 4}
+ORDER = {"f2": 2, "f3": 3, "f5": 5, "f7": 7, "gf4": 4, "gf8": 8, "z4": 4, "z8": 8}
 
 
 def log(*a):
