@@ -274,13 +274,21 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
     const int64_t units = tiles * nblocks;
     {
       // stream-K candidate: one wave of SMs x occupancy CTAs, each owning U / G consecutive
-      // (tile, k-block) units (<= SK_SEGS tile segments), then a compact reduction
+      // (tile, k-block) units, then a compact reduction of the partially covered tiles
       const int64_t G = (int64_t)ds.sms * occ;
-      const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 &&
-                      (units + G - 1) / G <= 2 * (int64_t)nblocks - 1 && units >= G;
+      // a CTA's range: partial tail, whole tiles, partial head (one segment boundary each).  Ranges
+      // of more than ~2 tiles scatter the concurrent CTAs over row groups, so they are planned only
+      // when A's index words and B fit in L2 together (measured: F7 16384x8192x16384 -1.7 %,
+      // F3 32768^3 +1.7 % where they do not); forced plans (splits = -1) take any range.
+      const int rpw = field == SG_F2 ? 4 : planes(field) == 3 ? 1 : 2;
+      const double l2_set = (double)((nblocks + rpw - 1) / rpw) * rgroups * rows * 4.0 + (double)R * l * wc32 * 4.0;
+      const bool short_ranges = (units + G - 1) / G <= 2 * (int64_t)nblocks - 1;
+      const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 && units >= G &&
+                      (short_ranges || l2_set <= 120e6 || g_override_splits == -1);
       if (ok) {
         const double per = (double)(units + G - 1) / G;
-        const double t_cta = cal ? per * cal->blk + 2.0 * cal->cta : 1.25 * (per * t_block + 6000.0);
+        const double nseg = std::min(2.0, per) + std::floor(per / nblocks);  // segments per CTA
+        const double t_cta = cal ? per * cal->blk + nseg * cal->cta : 1.25 * (per * t_block + 3000.0 * nseg);
         const double bytes = (double)G * 2.0 * R * rows * 16.0 + (double)R * m * wc32 * 4.0;
         // occ co-resident CTAs share the SM, as in the split-K estimate below
         const double est = occ * t_cta + bytes / 3000.0 + 8000.0;
@@ -371,7 +379,7 @@ int64_t workspace_bytes_for(const Plan& p, int field) {
   const int R = planes(field);
   int64_t b = (int64_t)p.at_planes * p.at_words * p.mpad * 4;
   b = (b + 255) / 256 * 256;
-  if (p.streamk) b += (int64_t)p.grid.x * SK_SEGS * R * p.rows * SLAB_WORDS * 4;
+  if (p.streamk) b += (int64_t)p.grid.x * SK_SLOTS * R * p.rows * SLAB_WORDS * 4;
   else if (p.splits > 1) b += (int64_t)p.splits * R * p.mpad * p.wc32 * 4;
   return std::max<int64_t>(b, 256);
 }

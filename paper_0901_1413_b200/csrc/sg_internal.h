@@ -64,13 +64,13 @@ struct M4rmArgs {
   int streamk;
   int64_t units;
   int slabs;           // tiles = slabs x row groups, tile t -> slab t % slabs, row group t / slabs
-  uint32_t* P2;        // compact stream-K partials [G * SK_SEGS][R][ROWS][4]
+  uint32_t* P2;        // compact stream-K partials [G * SK_SLOTS][R][ROWS][4]
   int early_trigger;   // experiments (SG_PDL=2): release the dependent reduction at kernel start
   int tma_b;           // stage B's k-blocks with one TMA tensor copy each (k = 8, wc32 % 4 == 0,
                        // B 16-B aligned)
   int tma_a;           // ... and A's index words with 1-D bulk copies (with tma_b only)
 };
-constexpr int SK_SEGS = 3;  // tile segments per stream-K CTA (the planner keeps U / G <= 2 nblocks)
+constexpr int SK_SLOTS = 2;  // compact partial slots per stream-K CTA: its first and last segment
 
 struct KernelInfo {
   void (*fn)(M4rmArgs, CUtensorMap);  // (args, B as a 3-D u32 tensor map for TMA staging)

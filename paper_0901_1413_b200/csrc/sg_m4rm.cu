@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restri
   }
   __syncthreads();
   const int c0 = c_range[0], c1 = c_range[1];
+  // a tile inside one CTA's range was written to C by the product kernel itself
+  if ((int64_t)c0 * U / G <= t * nb && ((int64_t)c0 + 1) * U / G >= (t + 1) * nb) return;
   const int64_t row0 = (t / slabs) * rows_cta;
   const int word0 = (int)(t % slabs) * SLAB_WORDS;
   for (int lr = blockIdx.y * blockDim.x + threadIdx.x; lr < rows_cta; lr += gridDim.y * blockDim.x) {
@@ -193,7 +195,8 @@ __global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restri
     for (int c = c0; c <= c1; ++c) {
       const int64_t u0 = (int64_t)c * U / G;
       if ((int64_t)(c + 1) * U / G == u0) continue;  // an empty range owns no slot
-      const int64_t slot = (int64_t)c * SK_SEGS + (t - u0 / nb);
+      // the tile holds c's first segment (slot 2c) or its last (slot 2c + 1)
+      const int64_t slot = (int64_t)c * SK_SLOTS + (u0 / nb == t ? 0 : 1);
       uint4 x[R];
 #pragma unroll
       for (int d = 0; d < R; ++d) x[d] = *reinterpret_cast<const uint4*>(P2 + ((slot * R + d) * rows_cta + lr) * 4);

@@ -649,8 +649,8 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
 }
 
 // All of this CTA's segments.  Stream-K: CTA c owns work units [c U / G, (c+1) U / G) of
-// U = tiles x k-blocks, i.e. at most SK_SEGS tile segments; each lands in compact slot
-// c * SK_SEGS + segment and reduce_streamk sums the slots of every tile.  Otherwise one segment
+// U = tiles x k-blocks: a partial tail of one tile, whole tiles, a partial head of another; the
+// partial segments land in compact slots and reduce_streamk sums the slots of every tile.  Otherwise one segment
 // per CTA: (slab, row group, k-split) = blockIdx.
 template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE>
 __device__ __forceinline__ void run_segments(const M4rmArgs& a, const CUtensorMap* tmB, unsigned char* smem,
@@ -665,15 +665,19 @@ __device__ __forceinline__ void run_segments(const M4rmArgs& a, const CUtensorMa
     return;
   }
   const int64_t U = a.units, G = gridDim.x;
-  int64_t u = blockIdx.x * U / G;
+  const int64_t u0 = blockIdx.x * U / G;
   const int64_t u1 = (blockIdx.x + 1) * U / G;
-  for (int seg = 0; u < u1 && seg < SK_SEGS; ++seg) {
+  for (int64_t u = u0; u < u1;) {
     const int64_t tile = u / a.nblocks;
     const int s0 = (int)(u - tile * a.nblocks);
     const int64_t room = u1 - u;
     const int s1 = (int)(s0 + room < a.nblocks ? s0 + room : (int64_t)a.nblocks);
+    // a whole tile goes straight to C; a partial one (only the range's first or last segment can
+    // be partial) to compact slot 2c (first) or 2c + 1 (last), summed by reduce_streamk_kernel
+    const bool whole = s0 == 0 && s1 == a.nblocks;
     m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE>(a, tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS,
-                                                 (tile / a.slabs) * ROWS, s0, s1, 2, blockIdx.x * SK_SEGS + seg);
+                                                 (tile / a.slabs) * ROWS, s0, s1, whole ? 0 : 2,
+                                                 (int)(blockIdx.x * SK_SLOTS + (u == u0 ? 0 : 1)));
     u += s1 - s0;
     cp_async_wait<0>();
     __syncthreads();  // shared memory is reused by the next segment

@@ -144,10 +144,12 @@ def test_every_compiled_plan(fname):  # noqa: F811
 
 @pytest.mark.parametrize("fname", list(FIELDS))
 def test_streamk_forced(fname):
-    """Stream-K (splits = -1): CTA ranges that start and end mid-tile and span up to three tiles,
-    every schedule and CTA shape, ragged m / l / n; bit-identical to the oracle."""
+    """Stream-K (splits = -1): CTA ranges that start and end mid-tile, span several whole tiles
+    (written straight to C) or lie inside one tile, every schedule and CTA shape, ragged m / l / n;
+    bit-identical to the oracle."""
     ran = 0
-    for (m, l, n) in [(700, 1000, 777), (3000, 64, 1000), (1111, 333, 200), (257, 2500, 129)]:
+    for (m, l, n) in [(700, 1000, 777), (3000, 64, 1000), (1111, 333, 200), (257, 2500, 129), (9000, 40, 2000),
+                      (5000, 200, 768)]:
         A = oracle.random_dense(fname, m, l, m + l)
         B = oracle.random_dense(fname, l, n, n + 3)
         want = expect(fname, A, B)
