@@ -164,6 +164,9 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
  * stream-K launch (one wave of CTAs over tile x k-block units + a compact reduction; k = 8
  * only); sg_plan reports splits = -1 for a stream-K plan. */
 int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads);
+/* Plan for (SM count - sms) SMs, leaving `sms` SMs free for a kernel that must run concurrently
+ * (the NCCL broadcast of B's next row block in dist.sharded_multiply); 0 = all SMs. */
+int sg_set_sm_reserve(int sms);
 int sg_set_timing(int enable);                              /* event-time each internal launch */
 /* performance experiments only: select kernel variants with parts of the work removed
  * (bit 0: table-replica stores, bit 1: field arithmetic, bit 2: lookups); results are WRONG

@@ -32,7 +32,7 @@ OPS = {
 EXPORTS = (
     "sg_abi_version", "sg_last_error", "sg_field_planes", "sg_pack", "sg_unpack",
     "sg_reduce_canonical", "sg_plane_op", "sg_m4rm_workspace_bytes", "sg_m4rm", "sg_m4rm_host", "sg_m4rm_multi",
-    "sg_build_table", "sg_m4rm_block", "sg_plan", "sg_set_plan_override", "sg_set_timing",
+    "sg_build_table", "sg_m4rm_block", "sg_plan", "sg_set_plan_override", "sg_set_sm_reserve", "sg_set_timing",
     "sg_last_timing", "sg_launch_count", "sg_kernel_info", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
 )
 
@@ -74,6 +74,7 @@ def load():
         "sg_m4rm_block": ([i32, pp, i64, pp, i64, i64, i32, pp, i64, i64, vp], i32),
         "sg_plan": ([i32, i64, i64, i64, i32, ip, ip, ip, ip, ip, ip], i32),
         "sg_set_plan_override": ([i32, i32, i32, i32], i32),
+        "sg_set_sm_reserve": ([i32], i32),
         "sg_set_timing": ([i32], i32),
         "sg_last_timing": ([dp, dp, dp], i32),
         "sg_launch_count": ([], i64),

@@ -26,6 +26,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 int g_override_rt = 0, g_override_splits = 0, g_override_pipe = -1, g_override_threads = 0, g_ablation = 0;
+int g_sm_reserve = 0;  // SMs the planner leaves free (for a collective running concurrently)
 bool g_timing = false;
 double g_last_ms[3] = {0, 0, 0};
 std::mutex g_mu;
@@ -222,10 +223,10 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
 // Plans are pure functions of the shape, the device and the overrides: cache them so repeated
 // products (the common case) skip the search (callers hold g_mu).
 int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Plan* out) {
-  typedef std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int, int, int, int> Key;
+  typedef std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int, int, int, int, int> Key;
   static std::map<Key, Plan> cache;
   const Key key{field, m, l, n, std::min(k, 8), device, g_override_rt, g_override_splits, g_override_pipe,
-                g_override_threads, g_ablation};
+                g_override_threads, g_ablation, g_sm_reserve};
   auto it = cache.find(key);
   if (it != cache.end()) {
     *out = it->second;
@@ -240,7 +241,9 @@ int make_plan(int field, int64_t m, int64_t l, int64_t n, int k, int device, Pla
 }
 
 int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int device, Plan* out) {
-  DevState& ds = dev_state(device);
+  DevState& ds0 = dev_state(device);
+  DevState ds = ds0;
+  ds.sms = std::max(1, ds0.sms - g_sm_reserve);  // CTAs for sms - reserve SMs: the rest stay free
   const int K = std::min(k, 8);
   const int64_t wc32 = 2 * w64_of(n), wa32 = 2 * w64_of(l);
   const int nblocks = (int)((l + K - 1) / K);
@@ -432,6 +435,13 @@ int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads)
   g_override_rt = rows_per_thread;
   g_override_splits = splits;
   g_override_pipe = pipe < 0 ? -1 : pipe;
+  return SG_OK;
+}
+
+int sg_set_sm_reserve(int sms) {
+  if (sms < 0 || sms > 64) return fail(SG_EINVAL, "SM reserve must be in 0..64");
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_sm_reserve = sms;
   return SG_OK;
 }
 

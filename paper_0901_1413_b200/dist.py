@@ -45,6 +45,19 @@ def broadcast_matrix(B: BitslicedMatrix, field, nrows: int, ncols: int, src: int
     return BitslicedMatrix(field, nrows, ncols, t)
 
 
+SM_RESERVE = 8  # SMs left to the broadcast while later row blocks are in flight
+
+
+def _default_multiply():
+    from .m4rm import m4rm_multiply
+    return m4rm_multiply
+
+
+def _set_reserve(sms: int):
+    from .m4rm import set_sm_reserve
+    set_sm_reserve(sms)
+
+
 def b_chunks(l: int, chunks: int) -> list:
     """Word-aligned row ranges [(r0, r1)] of B (= k-chunks of the inner dimension)."""
     w = (l + 63) // 64
@@ -91,13 +104,22 @@ def sharded_multiply(A_shard: BitslicedMatrix, B: BitslicedMatrix, field, l: int
     else:
         bufs = [torch.empty((field.bits, r1 - r0, W), dtype=torch.int64, device=dev) for r0, r1 in parts]
     works = [dist.broadcast(t, src=src, group=group, async_op=True) for t in bufs]
+    # while a later block is still on the wire, plan the products on all but SM_RESERVE SMs so
+    # the collective's kernel always finds SMs (one product CTA fills an SM)
+    reserve = SM_RESERVE if (multiply is _default_multiply() and dev.type == "cuda") else 0
     C = None
-    for (r0, r1), t, work in zip(parts, bufs, works):
-        w0, w1 = r0 // 64, (r1 + 63) // 64
-        A_j = BitslicedMatrix(field, A_shard.nrows, r1 - r0, A_shard.planes[:, :, w0:w1].contiguous())
-        work.wait()  # NCCL: the current stream waits for this chunk (the host does not block)
-        P = multiply(A_j, BitslicedMatrix(field, r1 - r0, n, t))
-        C = P if C is None else add(C, P)
+    try:
+        for j, ((r0, r1), t, work) in enumerate(zip(parts, bufs, works)):
+            w0, w1 = r0 // 64, (r1 + 63) // 64
+            A_j = BitslicedMatrix(field, A_shard.nrows, r1 - r0, A_shard.planes[:, :, w0:w1].contiguous())
+            work.wait()  # NCCL: the current stream waits for this chunk (the host does not block)
+            if reserve:
+                _set_reserve(reserve if j + 1 < len(parts) else 0)
+            P = multiply(A_j, BitslicedMatrix(field, r1 - r0, n, t))
+            C = P if C is None else add(C, P)
+    finally:
+        if reserve:
+            _set_reserve(0)
     if canonical:
         C = C.reduce_canonical()
     B_local = BitslicedMatrix(field, l, n, torch.cat(bufs, dim=1)) if return_b else None

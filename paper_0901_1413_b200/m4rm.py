@@ -143,6 +143,11 @@ def set_plan_override(rows_per_thread: int = 0, splits: int = 0, pipe: int = -1,
     _lib.check(_lib.load().sg_set_plan_override(rows_per_thread, splits, pipe, threads))
 
 
+def set_sm_reserve(sms: int = 0):
+    """Leave `sms` SMs free in subsequent plans (for a concurrent collective); 0 = use all."""
+    _lib.check(_lib.load().sg_set_sm_reserve(sms))
+
+
 def last_timing() -> dict:
     t, mm, r = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     _lib.check(_lib.load().sg_last_timing(ctypes.byref(t), ctypes.byref(mm), ctypes.byref(r)))

@@ -546,3 +546,21 @@ def test_multi_device_entry_point():
             assert np.array_equal(C.planes_numpy(), want), (fname, devs)
     with pytest.raises(ValueError):
         sgdist.multi_device_multiply(Ah, Bh, [99])
+
+
+def test_sm_reserve_plans_fewer_ctas():
+    """sg_set_sm_reserve: a stream-K plan uses (SMs - reserve) x occupancy CTAs; results unchanged."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    A = oracle.random_dense("f5", 4096, 512, 1)
+    B = oracle.random_dense("f5", 512, 1024, 2)
+    want = expect("f5", A, B)
+    try:
+        m4rm_mod.set_plan_override(0, -1, 2, 256)
+        full = m4rm_mod.plan("f5", 4096, 512, 1024)
+        m4rm_mod.set_sm_reserve(8)
+        part = m4rm_mod.plan("f5", 4096, 512, 1024)
+        assert full["splits"] == part["splits"] == -1
+        assert part["ctas"] * sms == full["ctas"] * (sms - 8)
+        assert np.array_equal(gpu_multiply("f5", A, B).planes_numpy(), want)
+    finally:
+        m4rm_mod.set_sm_reserve(0)
