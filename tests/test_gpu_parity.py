@@ -564,3 +564,37 @@ def test_sm_reserve_plans_fewer_ctas():
         assert np.array_equal(gpu_multiply("f5", A, B).planes_numpy(), want)
     finally:
         m4rm_mod.set_sm_reserve(0)
+
+
+def test_fuzz_plans_shapes_fields():
+    """Seeded fuzz: random field, shape (incl. word-boundary and tiny / skinny ones), k, and a
+    random forced plan (rows per thread, schedule, split count or stream-K, CTA width, F3 SM
+    reserve); every product bit-identical to the oracle."""
+    rng = np.random.default_rng(2026)
+    names = list(FIELDS)
+    ran = 0
+    for it in range(120):
+        fname = names[it % len(names)]
+        m = int(rng.choice([1, 7, 63, 64, 65, 200, 513, 1500, 3000]))
+        l = int(rng.choice([1, 8, 31, 64, 100, 257, 1000, 2049]))
+        n = int(rng.choice([1, 32, 63, 64, 65, 128, 129, 700, 1024]))
+        k = int(rng.choice([8, 8, 8, 5, 3, 1, 12]))
+        rt = int(rng.choice([0, 1, 2, 4, 8, 16]))
+        pipe = int(rng.choice([-1, 0, 1, 2]))
+        nt = int(rng.choice([0, 256, 512]))
+        splits = int(rng.choice([0, 0, 1, 3, 7, -1]))
+        A = oracle.random_dense(fname, m, l, it)
+        B = oracle.random_dense(fname, l, n, it + 1000)
+        m4rm_mod.set_plan_override(rt, splits, pipe, nt)
+        if it % 7 == 0:
+            m4rm_mod.set_sm_reserve(8)
+        try:
+            C = gpu_multiply(fname, A, B, k=k)
+        except RuntimeError as e:
+            assert "no compiled" in str(e)
+            continue
+        finally:
+            m4rm_mod.set_sm_reserve(0)
+        ran += 1
+        assert np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, m, l, n, k, rt, pipe, nt, splits)
+    assert ran >= 40
