@@ -67,8 +67,8 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
         return C
     dev = A.device if A.device.type == "cuda" else B.device
     _require_cuda(dev)
-    a = A.planes.to(dev).contiguous()
-    b = B.planes.to(dev).contiguous()
+    a = A.planes if A.planes.device == dev else A.planes.to(dev).contiguous()
+    b = B.planes if B.planes.device == dev else B.planes.to(dev).contiguous()
     if out is None:
         C = BitslicedMatrix(field, m, n, torch.empty((field.bits, m, (n + 63) // 64), dtype=torch.int64, device=dev))
     else:
@@ -76,9 +76,13 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
             raise ValueError("out has the wrong field, shape or device")
         C = out
     if m and n:
-        with torch.cuda.device(dev):
+        if dev.index == torch.cuda.current_device():  # the common case: no device switch
             _lib.check(L.sg_m4rm(field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k, None, 0,
                                  _lib.current_stream_handle(dev)))
+        else:
+            with torch.cuda.device(dev):
+                _lib.check(L.sg_m4rm(field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k, None, 0,
+                                     _lib.current_stream_handle(dev)))
     return C
 
 
