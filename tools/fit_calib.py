@@ -6,7 +6,8 @@ Model (the planner's, make_plan_uncached): with slabs = ceil(wc32 / 4), rows = r
 row groups = ceil(m / rows), k-blocks nb = ceil(l / 8), and SMs = 148,
   split-K:  T = waves * occ' * (bps * blk + cta) + reduce,   waves = ceil(ctas / (SMs * occ)),
             occ' = occ if ctas > SMs else 1, reduce = (splits + 1) R m wc32 4 / 3000 + 8000 (splits > 1)
-  stream-K: T = occ * (ceil(U / G) * blk + 2 cta) + (G 2 R rows 16 + R m wc32 4) / 3000 + 8000,
+  stream-K: T = occ * (ceil(U / G) * blk + nseg cta) + (G 2 R rows 16 + R m wc32 4) / 3000 + 8000,
+            nseg = min(2, per) + floor(per / nb) segments per CTA,
             G = SMs * occ, U = slabs * row groups * nb
 plus FIX = 20000 clocks per product (pre-pass, launches; the same for every variant, so it does not
 steer the planner).  T in SM clocks at 1965 MHz; (blk, cta) by least squares on the relative error."""
@@ -45,7 +46,8 @@ for key in sorted(groups, key=lambda k: (CODE[k[0]], k[1], k[2], k[3])):
         if sp == -1:
             G = SMS * occ
             U = slabs * rg * nb
-            x, y = occ * math.ceil(U / G), occ * 2.0
+            per = math.ceil(U / G)
+            x, y = occ * per, occ * (min(2.0, per) + per // nb)  # segments per CTA, as the planner
             red = (G * 2 * R[field] * rows * 16 + R[field] * m * wc32 * 4) / 3000 + 8000
         else:
             bps = (nb + sp - 1) // sp
