@@ -74,6 +74,11 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
     else:
         if out.field is not field or (out.nrows, out.ncols) != (m, n) or out.device != dev:
             raise ValueError("out has the wrong field, shape or device")
+        for t in (a, b):  # the kernels read A and B while C is written
+            lo, hi = t.data_ptr(), t.data_ptr() + t.numel() * 8
+            if t.numel() and out.planes.numel() and lo < out.planes.data_ptr() + out.planes.numel() * 8 \
+                    and out.planes.data_ptr() < hi:
+                raise ValueError("out must not overlap the operands")
         C = out
     if m and n:
         if dev.index == torch.cuda.current_device():  # the common case: no device switch

@@ -598,3 +598,12 @@ def test_fuzz_plans_shapes_fields():
         ran += 1
         assert np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, m, l, n, k, rt, pipe, nt, splits)
     assert ran >= 40
+
+
+def test_out_must_not_alias_operands():
+    A = sg.BitslicedMatrix.random(sg.F3, 64, 64, seed=0)
+    B = sg.BitslicedMatrix.random(sg.F3, 64, 64, seed=1)
+    with pytest.raises(ValueError):
+        sg.m4rm_multiply(A, B, sg.M4rmParams(8), out=A)
+    with pytest.raises(ValueError):
+        sg.m4rm_multiply(A, B, sg.M4rmParams(8), out=B)
