@@ -394,6 +394,18 @@ int check_mul_args(int field, const void* A, const void* B, const void* C, int64
   if (k < 1 || k > 16) return fail(SG_EINVAL, "k must be in 1..16 (SPEC.md:306-311)");
   if (2 * w64_of(l) > 0x7fffffffLL || 2 * w64_of(n) > 0x7fffffffLL) return fail(SG_EINVAL, "dimension too large");
   if (m && n && (!C || (l && (!A || !B)))) return fail(SG_EINVAL, "null matrix pointer");
+  if (m && n && l && A != (const void*)1) {  // (const void*)1: shape-only queries
+    // the product reads A and B while it writes C
+    const int R = planes(field);
+    auto overlap = [](const void* p, int64_t pb, const void* q, int64_t qb) {
+      const char* a = (const char*)p;
+      const char* b = (const char*)q;
+      return a < b + qb && b < a + pb;
+    };
+    const int64_t ab = (int64_t)R * m * w64_of(l) * 8, bb = (int64_t)R * l * w64_of(n) * 8,
+                  cb = (int64_t)R * m * w64_of(n) * 8;
+    if (overlap(C, cb, A, ab) || overlap(C, cb, B, bb)) return fail(SG_EINVAL, "C overlaps an operand");
+  }
   return SG_OK;
 }
 

@@ -51,6 +51,9 @@ def test_invalid_arguments_are_rejected_before_cuda():
     assert rc == _lib.SG_EINVAL
     assert L.sg_plane_op(99, None, None, 1, 1, 0, 0, None) == _lib.SG_EINVAL
     assert L.sg_kernel_info(-1, 0, None, None, None, None, None, None, None, None) == -1
+    # C overlapping an operand is rejected before any device work
+    assert L.sg_m4rm(1, vp(4096), vp(1 << 20), vp(4096 + 64), 8, 8, 8, 8, None, 0, None) == _lib.SG_EINVAL
+    assert b"overlaps" in L.sg_last_error()
     assert L.sg_pack(1, None, 2, 5, 3, None, None) == _lib.SG_EINVAL  # ld < n
     with pytest.raises(ValueError):
         _lib.check(_lib.SG_EINVAL)
