@@ -124,7 +124,8 @@ class ExtMatrix:
         spec = {GF4: F4, GF8: F8}.get(M.field)
         if spec is None:
             raise ValueError("expected a GF4 or GF8 matrix")
-        return cls(spec, [BitslicedMatrix(F2, M.nrows, M.ncols, M.planes[d:d + 1].clone())
+        # plane d of the power-basis matrix is the F2 coefficient matrix of x^d (views, no copy)
+        return cls(spec, [BitslicedMatrix(F2, M.nrows, M.ncols, M.planes[d:d + 1])
                           for d in range(spec.degree)])
 
     from_gf4 = from_direct
