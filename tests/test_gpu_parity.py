@@ -252,9 +252,16 @@ def test_host_buffers_pipelined_chunks():
                         os.environ["SG_HOST_KCHUNKS"], os.environ["SG_HOST_CHUNKS"] = str(pk), str(pr)
                         C = sg.m4rm_multiply(Ah, Bh)
                         assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, pk, pr)
+                for pr in (1, 2, 3):  # row x column piece grid
+                    for pc in (2, 3, 4):
+                        os.environ["SG_HOST_CHUNKS"], os.environ["SG_HOST_CCHUNKS"] = str(pr), str(pc)
+                        C = sg.m4rm_multiply(Ah, Bh)
+                        assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, pr, pc)
+                os.environ.pop("SG_HOST_CCHUNKS", None)
     finally:
         os.environ.pop("SG_HOST_KCHUNKS", None)
         os.environ.pop("SG_HOST_CHUNKS", None)
+        os.environ.pop("SG_HOST_CCHUNKS", None)
 
 
 def test_elementwise_ops_match_dense():

@@ -1,6 +1,6 @@
 """e2e experiments for sg_m4rm_host: chunk count sweep, copy-only bandwidth, per-chunk compute.
 
-python tools/e2e_chunks.py [--configs 1,2,3] [--chunks 1:1,2:2,4:4]   (k-chunks:row pieces)"""
+python tools/e2e_chunks.py [--configs 1,2,3] [--chunks 1:1,2:2,4:4]   (k-chunks:row pieces[:column pieces])"""
 import argparse
 import os
 import subprocess
@@ -12,10 +12,13 @@ ap.add_argument("--configs", default="1,2,3")
 ap.add_argument("--chunks", default="1:1,1:2,1:4,2:2,2:4,4:2,4:4,3:4")
 a = ap.parse_args()
 for P in a.chunks.split(","):
-    PK, PR = P.split(":")
+    parts = P.split(":")
+    PK, PR = parts[0], parts[1]
+    PC = parts[2] if len(parts) > 2 else "1"
     out = subprocess.run([sys.executable, "-c", f"""
 import os, sys, time, ctypes, torch
 os.environ['SG_HOST_KCHUNKS'] = '{PK}'
+os.environ['SG_HOST_CCHUNKS'] = '{PC}'
 os.environ['SG_HOST_CHUNKS'] = '{PR}'
 sys.path.insert(0, '.')
 import bench
