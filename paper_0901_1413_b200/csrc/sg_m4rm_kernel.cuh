@@ -5,21 +5,29 @@
 // build_table then _core.active().m4rm_block_<f> (_core_py.py:205-281),
 // whose per-row loop does  C_i += sum_d alpha_d * T[phi_d(a_i, block s)].
 //
-// B200 design (DESIGN.md "Kernels"):
-//  * One CTA owns a 128-column slab of C (4 x 32-bit words per plane) and ROWS = RT*256 rows,
-//    and walks the k-blocks of its split of the inner dimension.  C lives in registers for
-//    the whole walk: lane (t, tid) holds rows t*256+tid, one uint4 per plane.
+// B200 design (DESIGN.md §3.1):
+//  * A tile is a 128-column slab of C (4 x 32-bit words per plane) x ROWS = RT*NT rows.  A CTA
+//    walks a range of k-blocks of a tile with C in registers: lane (t, tid) holds rows t*NT+tid,
+//    one uint4 per accumulator plane.  Work assignment (m4rm_kernel / run_segments): one tile
+//    and a split of k per CTA, or stream-K (one wave of CTAs over tiles x k-blocks; whole tiles
+//    straight to C, partial ones to compact slots for reduce_streamk_kernel).
 //  * Per k-block the CTA builds the 2^K-entry table of its slab in shared memory:
-//    phase 1: two half tables (rows 0..3 and 4..7 of the block, 16 entries each) from the B
-//    rows that cp.async staged two blocks ahead; phase 2: T[g] = Thi[g>>4] + Tlo[g&15],
-//    one bitsliced field add per word, written as 8 replicas (see COPIES).
+//    phase 1: two half tables (rows 0..3 and 4..7 of the block, 16 entries each) from B rows
+//    staged ahead of time; phase 2: T[g] = Thi[g>>4] + Tlo[g&15], one bitsliced field add per
+//    word, written as 8 replicas (see COPIES).
 //  * Lookups: the 8 lanes of each LDS.128 phase hold 8 different rows, i.e. 8 random table
 //    entries.  Replica j of every entry sits at bank offset 4j and lane (tid&7) reads replica
 //    tid&7, so each phase touches all 32 banks exactly once: conflict-free for any indices.
-//  * Index bytes come from A^T (A's planes transposed to [plane][word][row] by a pre-pass, F3's
-//    plane 0 pre-XORed to A0^A1), staged per 32-bit word into shared memory by cp.async: one
-//    conflict-free LDS.32 per (row, block, plane).
-//  * Epilogue: canonical reduce (F5/F7) and store, or raw partial sums for split-K.
+//  * Index bytes come from the index pre-pass (A's per-block basis bytes packed into 32-bit
+//    records [word][row], F3's first byte pre-XORed to A0^A1): one conflict-free LDS.32 per
+//    (row, record word), a PRMT and a LEA per lookup.
+//  * Schedules: SCHED 0 serial, 1 pipelined (double-buffered table), 2 warp-specialized
+//    (4 builder warps build block s+1 while 8 lookup warps consume block s; FULL / EMPTY named
+//    barriers; B's rows staged by one TMA tensor copy per block and A's index words by 1-D bulk
+//    copies, both completing on mbarriers; setmaxnreg moves registers from the builder
+//    warpgroup to the lookup warpgroups, whose code is compiled separately (ROLE)).
+//  * Epilogue: canonical reduce (F5 mod 15 -> mod 5, F7 fold) and store, or canonical partial
+//    sums for split-K / stream-K.
 #pragma once
 #include <cstdio>
 
