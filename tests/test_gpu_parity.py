@@ -639,3 +639,16 @@ def test_m4rm_not_slower_than_classical_f3_1024():
     t_m4rm = med(lambda: sg.m4rm_multiply(A, B, sg.M4rmParams(8)))
     t_cls = med(lambda: m4rm_mod.classical_multiply(A, B))
     assert t_m4rm <= t_cls, (t_m4rm, t_cls)
+
+
+def test_c_host_example():
+    """examples/c_api_demo.c: the ABI from a plain C host (sg_m4rm_host and sg_pack -> sg_m4rm ->
+    sg_unpack), checked against a schoolbook product inside the program."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "c_api_demo")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(root, "examples")], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "bit-exact" in out.stdout
