@@ -162,59 +162,114 @@ cudaError_t launch_sum_slices(int field, const SliceSet& s, uint32_t* out, int64
 // C(tile t) = sum of the compact slots of the CTAs whose unit ranges intersect tile t's
 // [t nb, (t+1) nb), canonicalized.  One thread per (tile row, word); slots are summed in CTA
 // order (the field sums are exact, so any order gives the same bits).
+// Tiles with more than 64 contributors (forced stream-K plans with a few units per CTA).
+template <int F>
+__device__ __noinline__ void reduce_streamk_tile_slow(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m,
+                                                      int wc32, int rows_cta, int slabs, int64_t t, int nb,
+                                                      int64_t U, int G) {
+  constexpr int R = Traits<F>::R;
+  const int64_t lo = t * nb, hi = lo + nb;
+  int64_t c0 = lo * G / U;
+  while (c0 > 0 && c0 * U / G > lo) --c0;
+  while ((c0 + 1) * U / G <= lo) ++c0;
+  const int64_t row0 = (t / slabs) * rows_cta;
+  const int word0 = (int)(t % slabs) * SLAB_WORDS;
+  for (int lr = blockIdx.y * blockDim.x + threadIdx.x; lr < rows_cta; lr += gridDim.y * blockDim.x) {
+    const int64_t row = row0 + lr;
+    if (row >= m) break;
+    V<F> acc[4];
+    bool first = true;
+    for (int64_t c = c0; c < G && c * U / G < hi; ++c) {
+      const int64_t u0 = c * U / G;
+      if ((c + 1) * U / G == u0) continue;
+      const int64_t slot = c * SK_SLOTS + (u0 / nb == t ? 0 : 1);
+      V<F> b[4];
+#pragma unroll
+      for (int d = 0; d < R; ++d) {
+        const uint4 x = *reinterpret_cast<const uint4*>(P2 + ((slot * R + d) * rows_cta + lr) * 4);
+        b[0].p[d] = x.x; b[1].p[d] = x.y; b[2].p[d] = x.z; b[3].p[d] = x.w;
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        if (first) acc[w] = b[w];
+        else vadd<F>(acc[w], b[w]);
+      }
+      first = false;
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) vcanon<F>(acc[w]);
+#pragma unroll
+    for (int d = 0; d < R; ++d)
+      for (int w = 0; w < 4 && word0 + w < wc32; ++w) C[((int64_t)d * m + row) * wc32 + word0 + w] = acc[w].p[d];
+  }
+}
+
 template <int F>
 __global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m,
                                                              int wc32, int rows_cta, int slabs, int64_t tiles, int nb,
                                                              int64_t U, int G) {
   constexpr int R = Traits<F>::R;
   pdl_wait();  // launched with PDL behind the product kernel
-  // blockIdx.x = tile; the CTAs whose unit ranges touch it are found once per block
+  // blockIdx.x = tile; the slots of the CTAs whose unit ranges touch it are listed once per block
+  constexpr int MAXS = 64;
   const int64_t t = blockIdx.x;
-  __shared__ int c_range[2];
+  __shared__ int slots[MAXS + 1];  // [0] = count (0: the tile was written by the product kernel)
   if (threadIdx.x == 0) {
     const int64_t lo = t * nb, hi = lo + nb;
     int64_t c = lo * G / U;
     while (c > 0 && c * U / G > lo) --c;
     while ((c + 1) * U / G <= lo) ++c;
-    int64_t c1 = c;
-    while (c1 + 1 < G && (c1 + 1) * U / G < hi) ++c1;
-    c_range[0] = (int)c;
-    c_range[1] = (int)c1;
+    int n = 0;
+    // a tile inside one CTA's range was written to C by the product kernel itself
+    const bool whole = c * U / G <= lo && (c + 1) * U / G >= hi;
+    for (; !whole && c < G && c * U / G < hi; ++c) {
+      const int64_t u0 = c * U / G;
+      if ((c + 1) * U / G == u0) continue;  // an empty range owns no slot
+      // the tile holds c's first segment (slot 2c) or its last (slot 2c + 1)
+      if (n < MAXS) slots[1 + n] = (int)(c * SK_SLOTS + (u0 / nb == t ? 0 : 1));
+      ++n;
+    }
+    slots[0] = n;
   }
   __syncthreads();
-  const int c0 = c_range[0], c1 = c_range[1];
-  // a tile inside one CTA's range was written to C by the product kernel itself
-  if ((int64_t)c0 * U / G <= t * nb && ((int64_t)c0 + 1) * U / G >= (t + 1) * nb) return;
+  const int n = slots[0];
+  if (n == 0) return;
+  if (n > MAXS) {  // very short CTA ranges (forced plans): enumerate per thread
+    reduce_streamk_tile_slow<F>(P2, C, m, wc32, rows_cta, slabs, t, nb, U, G);
+    return;
+  }
   const int64_t row0 = (t / slabs) * rows_cta;
   const int word0 = (int)(t % slabs) * SLAB_WORDS;
   for (int lr = blockIdx.y * blockDim.x + threadIdx.x; lr < rows_cta; lr += gridDim.y * blockDim.x) {
     const int64_t row = row0 + lr;
     if (row >= m) break;
     uint4 acc[R];
-    bool first = true;
-    for (int c = c0; c <= c1; ++c) {
-      const int64_t u0 = (int64_t)c * U / G;
-      if ((int64_t)(c + 1) * U / G == u0) continue;  // an empty range owns no slot
-      // the tile holds c's first segment (slot 2c) or its last (slot 2c + 1)
-      const int64_t slot = (int64_t)c * SK_SLOTS + (u0 / nb == t ? 0 : 1);
-      uint4 x[R];
+    // slots two at a time: both loads in flight before the adds (latency, not bandwidth, bound)
+    for (int j = 0; j < n; j += 2) {
+      const bool two = j + 1 < n;
+      const u32* s0 = P2 + ((int64_t)slots[1 + j] * R * rows_cta + lr) * 4;
+      const u32* s1 = P2 + ((int64_t)slots[1 + (two ? j + 1 : j)] * R * rows_cta + lr) * 4;
+      uint4 x[R], y[R];
 #pragma unroll
-      for (int d = 0; d < R; ++d) x[d] = *reinterpret_cast<const uint4*>(P2 + ((slot * R + d) * rows_cta + lr) * 4);
-      if (first) {
-#pragma unroll
-        for (int d = 0; d < R; ++d) acc[d] = x[d];
-        first = false;
-        continue;
+      for (int d = 0; d < R; ++d) {
+        x[d] = *reinterpret_cast<const uint4*>(s0 + (int64_t)d * rows_cta * 4);
+        y[d] = *reinterpret_cast<const uint4*>(s1 + (int64_t)d * rows_cta * 4);
       }
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         V<F> a, b;
 #pragma unroll
         for (int d = 0; d < R; ++d) {
-          a.p[d] = comp4(acc[d], w);
-          b.p[d] = comp4(x[d], w);
+          a.p[d] = comp4(x[d], w);
+          b.p[d] = comp4(y[d], w);
         }
-        vadd<F>(a, b);
+        if (two) vadd<F>(a, b);
+        if (j > 0) {
+          V<F> c;
+#pragma unroll
+          for (int d = 0; d < R; ++d) c.p[d] = comp4(acc[d], w);
+          vadd<F>(a, c);
+        }
 #pragma unroll
         for (int d = 0; d < R; ++d) set4(acc[d], w, a.p[d]);
       }
