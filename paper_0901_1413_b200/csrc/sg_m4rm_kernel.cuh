@@ -482,6 +482,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
       const int bt = tid - NT;
       auto bsync = [] { nbar_sync(5, NBT); };
       issue_b(s_begin, bt, NBT);
+      pdl_wait();  // A's index words come from the pre-pass (B's first rows are already on the way)
       issue_a(s_begin, bt, NBT);
       cp_async_commit();
       issue_b(s_begin + 1, bt, NBT);
@@ -556,8 +557,9 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
       if (s + 2 < s_end) nbar_arrive(EMPTY(s), NB);
     }
   } else if constexpr (!PIPE) {
+    for (int i = 0; i < PD; ++i) issue_b(s_begin + i);
+    pdl_wait();  // A's index words come from the pre-pass
     for (int i = 0; i < PD; ++i) {
-      issue_b(s_begin + i);
       issue_a(s_begin + i);
       cp_async_commit();
     }
@@ -581,6 +583,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
     }
   } else {
     for (int i = 0; i < PD; ++i) issue_b(s_begin + i);
+    pdl_wait();  // A's index words come from the pre-pass
     for (int i = 0; i < PDA; ++i) issue_a(s_begin + i);
     cp_async_commit();
     cp_async_wait<0>();
@@ -708,7 +711,8 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ROWS = RT * NT;
   if (a.early_trigger) pdl_trigger();
-  pdl_wait();  // launched with PDL behind the index pre-pass: wait for its writes
+  // launched with PDL behind the index pre-pass: each schedule waits for it (pdl_wait) just
+  // before its first read of A's index words, so the B staging overlaps the pre-pass's tail
   constexpr int R = Traits<F>::R;
   constexpr int NSLOT = K == 8 ? 3 : 2;
   constexpr int NAP = K == 8 ? 1 : R;
