@@ -348,6 +348,7 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
         Ch.copy_(C.planes, non_blocking=True)
         torch.cuda.synchronize()
 
+    s0 = L.sg_host_streamed_count()
     for _ in range(max(1, args.warmup)):
         one()
     if world > 1:
@@ -362,9 +363,15 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
         dist.all_reduce(total, op=dist.ReduceOp.MAX)
     per = float(total.item()) / args.steps
     h2d = Ah.numel() * 8 + (Bh.numel() * 8 if rank == 0 else 0)
+    extra = {}
+    if world == 1:
+        # the host-path result must equal the device path's (outside the timed region)
+        extra["verified_vs_device_path"] = bool(torch.equal(sg.m4rm_multiply(A, B).planes.cpu(), Ch))
+        extra["streamed_b_calls"] = int(L.sg_host_streamed_count() - s0)
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8),
-            "path": ("sg_m4rm_host (C ABI; pinned host planes; H2D, multiply, D2H pipelined over k-chunks and row pieces)"
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8), **extra,
+            "path": ("sg_m4rm_host (C ABI; pinned host planes; A and C in row pieces, the first piece's product "
+                     "consuming B's k-chunks as they land, D2H of each piece behind its product)"
                      if world == 1 else "rank-0 H2D of B + broadcast in row blocks overlapped with the chunk products "
                      "(dist.sharded_multiply), per-rank H2D of A rows, D2H of C rows (wall clock, max over ranks)")}
 

@@ -127,7 +127,10 @@ int sg_plane_op(int op, uint64_t* const* dst, const uint64_t* const* src, int64_
 int64_t sg_m4rm_workspace_bytes(int field, int64_t m, int64_t l, int64_t n, int k);
 int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l,
             int64_t n, int k, void* workspace, int64_t workspace_bytes, void* stream);
-/* Same with host buffers: copies in, multiplies on `device`, copies C back; synchronous. */
+/* Same with host buffers: copies in, multiplies on `device`, copies C back; synchronous.  The
+ * copies overlap the products: A and C move in row pieces, and where the plan allows it
+ * (stream-K, warp-specialized TMA schedule) the first piece's product starts before B is up and
+ * consumes B's k-chunks as they land (sg_host_streamed_count counts those calls). */
 int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
                  int64_t l, int64_t n, int k, int device);
 
@@ -174,6 +177,7 @@ int sg_set_timing(int enable);                              /* event-time each i
 int sg_debug_ablation(int mask);
 int sg_last_timing(double* transpose_ms, double* m4rm_ms, double* reduce_ms);
 int64_t sg_launch_count(void);                              /* kernels launched by this library */
+int64_t sg_host_streamed_count(void);         /* sg_m4rm_host calls whose product streamed B */
 /* compiled M4RM instantiation `index` (0 .. count-1; returns the count, or -1 for a bad index):
  * field, k, rows per thread, lookup threads, schedule, CTAs per SM on `device`, registers per
  * thread, dynamic shared memory bytes (any pointer may be NULL) */

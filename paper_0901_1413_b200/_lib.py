@@ -33,7 +33,7 @@ EXPORTS = (
     "sg_abi_version", "sg_last_error", "sg_field_planes", "sg_pack", "sg_unpack",
     "sg_reduce_canonical", "sg_plane_op", "sg_m4rm_workspace_bytes", "sg_m4rm", "sg_m4rm_host", "sg_m4rm_multi",
     "sg_build_table", "sg_m4rm_block", "sg_plan", "sg_set_plan_override", "sg_set_sm_reserve", "sg_set_timing",
-    "sg_last_timing", "sg_launch_count", "sg_kernel_info", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
+    "sg_last_timing", "sg_launch_count", "sg_host_streamed_count", "sg_kernel_info", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
 )
 
 _lib = None
@@ -78,13 +78,18 @@ def load():
         "sg_set_timing": ([i32], i32),
         "sg_last_timing": ([dp, dp, dp], i32),
         "sg_launch_count": ([], i64),
+        "sg_host_streamed_count": ([], i64),
         "sg_kernel_info": ([i32, i32, ip, ip, ip, ip, ip, ip, ip, ip], i32),
         "sg_probe_peaks": ([i32, dp, dp, dp], i32),
         "sg_debug_ablation": ([i32], i32),
         "sg_classical": ([i32, vp, vp, vp, i64, i64, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
-        fn = getattr(L, name)
+        fn = getattr(L, name, None)
+        if fn is None and path != LIB_PATH:
+            continue  # an older build under A/B (SG_LIB_PATH)
+        if fn is None:
+            raise ImportError(f"{path} does not export {name}: rebuild it")
         fn.argtypes = args
         fn.restype = res
     _lib = L

@@ -25,6 +25,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_streamed{0};  // host-buffer products that streamed B (sg_host_streamed_count)
 int g_override_rt = 0, g_override_splits = 0, g_override_pipe = -1, g_override_threads = 0, g_ablation = 0;
 int g_sm_reserve = 0;  // SMs the planner leaves free (for a collective running concurrently)
 bool g_timing = false;
@@ -62,6 +63,7 @@ DevState& dev_state(int device) {
     for (int i = 0; i < m4rm_kernel_count(); ++i) {
       KernelInfo* k = m4rm_kernel_at(i);
       cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
+      if (k->fn_stream) cudaFuncSetAttribute(k->fn_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
       cudaFuncAttributes fa;
       if (cudaFuncGetAttributes(&fa, k->fn) == cudaSuccess) k->regs = fa.numRegs;
       int occ = 0;
@@ -409,6 +411,78 @@ int check_mul_args(int field, const void* A, const void* B, const void* C, int64
   return SG_OK;
 }
 
+// ---------------------------------------------------------------- streamed B (sg_m4rm_host)
+// A product whose B arrives chunk by chunk while it runs (see M4rmArgs.ready).
+struct StreamIn {
+  const unsigned* ready;
+  unsigned epoch;
+  int chunk_blocks;
+  unsigned* err;
+};
+
+// One stream-K wave of the warp-specialized kernel: its builder warps stage every k-block by
+// TMA, so they can wait for each block's chunk; the 4-block group order needs nblocks % 4 == 0.
+bool streamable(const Plan& p) {
+  return p.streamk && p.ki->sched == 2 && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 && p.tiles > 0 &&
+         (int64_t)p.tiles * (p.nblocks / 4) <= (int64_t)1 << 24;
+}
+
+typedef std::tuple<int, int, int64_t, int64_t, int64_t, unsigned> PermKey;
+std::map<PermKey, int*> g_perm;  // device copies of streamed_order, per (device, plan)
+PermKey perm_key(const Plan& p, int dev, int64_t m, int64_t l, int64_t n) {
+  return PermKey{dev, p.kernel_index, m, l, n, p.grid.x};
+}
+
+// Per tile, the order in which a streamed product consumes B's 4-block groups.  Each group gets
+// the earliest time (k-blocks into its CTA's range) at which one of the tile's stream-K segments
+// needs it, and groups are numbered in that order: B goes up in k order, so every CTA starts on
+// blocks that arrive first, and a tile's contributors share the arrivals instead of some CTAs
+// waiting for blocks deep in k.  virtual group v of tile t -> real group perm[t * ng + v].
+std::vector<int> streamed_order(const Plan& p) {
+  const int nb = p.nblocks, ng = nb / 4;
+  const int64_t U = p.units, G = p.grid.x;
+  std::vector<int> perm((size_t)p.tiles * ng);
+  std::vector<std::pair<int64_t, int>> need(ng);
+  for (int64_t t = 0; t < p.tiles; ++t) {
+    for (int g = 0; g < ng; ++g) need[g] = {INT64_MAX, g};
+    const int64_t lo = t * nb, hi = lo + nb;
+    int64_t c = lo * G / U;
+    while (c > 0 && c * U / G > lo) --c;
+    while ((c + 1) * U / G <= lo) ++c;
+    for (; c < G && c * U / G < hi; ++c) {
+      const int64_t u0 = c * U / G, u1 = (c + 1) * U / G;
+      const int64_t a = std::max(u0, lo), b = std::min(u1, hi);
+      for (int64_t g = (a - lo) / 4; a < b && g <= (b - 1 - lo) / 4; ++g) {
+        const int64_t first = std::max(a, lo + 4 * g);  // the segment's first block in group g
+        need[g].first = std::min(need[g].first, first - u0);
+      }
+    }
+    std::sort(need.begin(), need.end());  // by (time, group)
+    for (int i = 0; i < ng; ++i) perm[t * ng + need[i].second] = i;
+  }
+  return perm;
+}
+
+// Plan a streamed product and upload its group order (callers hold g_mu).  Returns SG_OK, or
+// SG_EUNSUPPORTED when the product cannot stream (the caller then uploads B first).
+int prepare_streamed(int field, int64_t m, int64_t l, int64_t n, int k, int dev, Plan* out) {
+  int rc = make_plan(field, m, l, n, k, dev, out);
+  if (rc != SG_OK) return rc;
+  if (!streamable(*out)) return SG_EUNSUPPORTED;
+  const PermKey key = perm_key(*out, dev, m, l, n);
+  if (g_perm.count(key)) return SG_OK;
+  const std::vector<int> perm = streamed_order(*out);
+  int* d = nullptr;
+  SG_CUDA(cudaMalloc(&d, perm.size() * sizeof(int)), "streamed order alloc");
+  SG_CUDA(cudaMemcpy(d, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice), "streamed order upload");
+  if (g_perm.size() > 256) g_perm.clear();  // (leaks the old device arrays; bounded by the cap)
+  g_perm[key] = d;
+  return SG_OK;
+}
+
+int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
+                int k, void* workspace, int64_t workspace_bytes, cudaStream_t stream, const StreamIn* sin);
+
 }  // namespace
 
 // ==================================================================== C ABI
@@ -418,6 +492,7 @@ int sg_abi_version(void) { return SG_ABI_VERSION; }
 const char* sg_last_error(void) { return g_err.c_str(); }
 int sg_field_planes(int field) { return valid_field(field) ? planes(field) : -1; }
 int64_t sg_launch_count(void) { return g_launches.load(); }
+int64_t sg_host_streamed_count(void) { return g_streamed.load(); }
 
 int sg_kernel_info(int index, int device, int* field, int* k, int* rows_per_thread, int* threads, int* schedule,
                    int* occupancy, int* regs, int* smem_bytes) {
@@ -604,9 +679,17 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
 
 int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
             int k, void* workspace, int64_t workspace_bytes, void* stream) {
+  return m4rm_device(field, A, B, C, m, l, n, k, workspace, workspace_bytes, (cudaStream_t)stream, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
+                int k, void* workspace, int64_t workspace_bytes, cudaStream_t stream, const StreamIn* sin) {
   int rc = check_mul_args(field, A, B, C, m, l, n, k);
   if (rc != SG_OK) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
+  cudaStream_t st = stream;
   const int R = planes(field);
   if (m == 0 || n == 0) return SG_OK;
   if (l == 0) {  // empty inner dimension: C = 0
@@ -619,6 +702,15 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   Plan p;
   rc = make_plan(field, m, l, n, k, dev, &p);
   if (rc != SG_OK) return rc;
+  const int* perm = nullptr;
+  if (sin) {
+    // streamed B: the plan must be one the builder warps can pace (streamable) and its group
+    // order must have been uploaded beforehand (prepare_streamed: no allocation may happen
+    // while a streamed product waits for its chunks)
+    auto it = g_perm.find(perm_key(p, dev, m, l, n));
+    if (!streamable(p) || it == g_perm.end()) return fail(SG_EINVAL, "product is not prepared for streamed B");
+    perm = it->second;
+  }
   const int64_t need = workspace_bytes_for(p, field);
   char* ws = (char*)workspace;
   if (ws) {
@@ -669,12 +761,25 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
     // GF(4) 8192^3 stream-K +2.6 %; SG_TMA=2 forces it, for experiments)
     a.tma_a = a.tma_b && (tma_env == 2 || !p.streamk);
   }
+  if (sin && !a.tma_b) return fail(SG_EINVAL, "streamed B needs the TMA staging path");
   a.streamk = p.streamk;
   a.units = p.units;
   a.slabs = p.slabs;
   a.P2 = p.streamk ? partial : nullptr;
   if (p.streamk) a.C = (uint32_t*)C;
-  SG_CUDA(launch_m4rm(*p.ki, a, tmB, p.grid, st), "sg_m4rm kernel");
+  if (sin) {
+    M4rmStreamArgs sa;
+    static_cast<M4rmArgs&>(sa) = a;
+    sa.ready = sin->ready;
+    sa.epoch = sin->epoch;
+    sa.chunk_blocks = sin->chunk_blocks;
+    sa.perm = perm;
+    sa.ngroups = p.nblocks / 4;
+    sa.err = sin->err;
+    SG_CUDA(launch_m4rm_streamed(*p.ki, sa, tmB, p.grid, st), "sg_m4rm streamed kernel");
+  } else {
+    SG_CUDA(launch_m4rm(*p.ki, a, tmB, p.grid, st), "sg_m4rm kernel");
+  }
   g_launches++;
   if (g_timing) cudaEventRecord(ev[2], st);
   if (p.streamk) {
@@ -701,6 +806,156 @@ int sg_m4rm(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_
   }
   return SG_OK;
 }
+
+// Per-device state of the host-buffer pipeline (sg_m4rm_host).
+struct Io {
+  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  cudaEvent_t ev_in[8], ev_comp[16];
+  Buf buf;
+  std::mutex busy;  // one host-buffer product per device at a time (the staging buffers are shared)
+  // streamed B: chunk flags [64] + error word, the call epoch, the error word's pinned host copy
+  unsigned* ready = nullptr;
+  unsigned epoch = 0;
+  unsigned* err_host = nullptr;
+};
+std::map<int, Io> io_state;
+
+PFN_cuStreamWriteValue32_v11070 write_value_fn() {
+  static PFN_cuStreamWriteValue32_v11070 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
+  }();
+  return fn;
+}
+
+constexpr int MAX_BCHUNKS = 64;
+
+// Streamed variant of the row-piece pipeline (B uploaded whole, A and C in Pr row pieces): the
+// product of piece 0 is launched as soon as A's piece 0 is up and reads B's k-chunks as they
+// land -- the upload stream publishes chunk j by writing the call's epoch to ready[j] right
+// behind the chunk's copy (cuStreamWriteValue32, no SM involved) and the builder warps wait per
+// k-block (M4rmArgs.ready), consuming each tile's k-blocks in arrival order (streamed_order).
+// Later pieces find B complete.  Returns SG_EUNSUPPORTED when the product cannot stream.
+int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
+                  int64_t l, int64_t n, int k, int device, int Pr) {
+  const char* nch_e = getenv("SG_HOST_BCHUNKS");  // experiments: number of B chunks
+  const int nch_env = nch_e ? atoi(nch_e) : 0;
+  const PFN_cuStreamWriteValue32_v11070 wv = write_value_fn();
+  if (!wv) return SG_EUNSUPPORTED;
+  const int R = planes(field);
+  const int64_t wa = w64_of(l), wc = w64_of(n);
+  auto rcut = [&](int r) { return m * r / Pr; };
+  // everything that may allocate or synchronize happens before the first copy is queued
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Plan p0;
+    int rc = prepare_streamed(field, rcut(1), l, n, k, device, &p0);
+    if (rc != SG_OK) return rc;
+    int64_t ws_need = 0;
+    for (int r = 0; r < Pr; ++r) {
+      const int64_t rows = rcut(r + 1) - rcut(r);
+      if (rows <= 0) continue;
+      Plan q;
+      if ((rc = make_plan(field, rows, l, n, k, device, &q)) != SG_OK) return rc;
+      ws_need = std::max(ws_need, workspace_bytes_for(q, field));
+    }
+    cudaError_t e;
+    if (!workspace_for(device, d->comp, (size_t)ws_need, &e)) return cuda_fail(e, "sg_m4rm_host workspace");
+    SG_CUDA(preload_aux_kernels(field), "sg_m4rm_host preload");
+    if (!d->ready) {
+      SG_CUDA(cudaMalloc(&d->ready, (MAX_BCHUNKS + 1) * sizeof(unsigned)), "sg_m4rm_host flags");
+      SG_CUDA(cudaMemset(d->ready, 0, (MAX_BCHUNKS + 1) * sizeof(unsigned)), "sg_m4rm_host flags");
+      SG_CUDA(cudaMallocHost(&d->err_host, sizeof(unsigned)), "sg_m4rm_host flags");
+      // first use of the stream memory operations while nothing waits on them
+      if (wv((CUstream)d->in, (CUdeviceptr)(d->ready + MAX_BCHUNKS), 0u, 0) != CUDA_SUCCESS) {
+        cudaGetLastError();
+        return SG_EUNSUPPORTED;
+      }
+      SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host flags");
+    }
+  }
+  unsigned* err = d->ready + MAX_BCHUNKS;
+  const unsigned epoch = ++d->epoch;
+  // B chunks: whole 4-block groups (32 rows), >= 128 KB each, at most MAX_BCHUNKS
+  const int64_t groups = (l + 31) / 32;
+  const size_t b_bytes = (size_t)R * l * wc * 8;
+  int nch = nch_env > 0 ? nch_env : (int)std::min<int64_t>(16, std::max<int64_t>(1, (int64_t)(b_bytes >> 17)));
+  nch = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)nch, groups, (int64_t)MAX_BCHUNKS}));
+  const int64_t gpc = (groups + nch - 1) / nch;  // groups per chunk
+  nch = (int)((groups + gpc - 1) / gpc);
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  char* cur = dbuf;
+  uint64_t* dB = (uint64_t*)cur;
+  cur += up(b_bytes);
+  uint64_t* dAp[4];
+  for (int r = 0; r < Pr; ++r) {
+    dAp[r] = (uint64_t*)cur;
+    cur += up((size_t)R * (rcut(r + 1) - rcut(r)) * wa * 8);
+  }
+  uint64_t* dC = (uint64_t*)cur;  // pieces back to back, each [R][rows][wc]
+  auto upload_a = [&](int r) -> int {
+    const int64_t q0 = rcut(r), rows = rcut(r + 1) - q0;
+    if (rows > 0)
+      SG_CUDA(cudaMemcpy2DAsync(dAp[r], rows * wa * 8, A + q0 * wa, m * wa * 8, rows * wa * 8, R,
+                                cudaMemcpyHostToDevice, d->in),
+              "sg_m4rm_host H2D A");
+    SG_CUDA(cudaEventRecord(d->ev_in[r], d->in), "sg_m4rm_host event");
+    return SG_OK;
+  };
+  auto product = [&](int r, const StreamIn* sin) -> int {
+    const int64_t q0 = rcut(r), rows = rcut(r + 1) - q0;
+    SG_CUDA(cudaStreamWaitEvent(d->comp, d->ev_in[r], 0), "sg_m4rm_host wait");
+    if (rows <= 0) return SG_OK;
+    uint64_t* piece = dC + (int64_t)R * q0 * wc;
+    int rc = m4rm_device(field, dAp[r], dB, piece, rows, l, n, k, nullptr, 0, d->comp, sin);
+    if (rc != SG_OK) return rc;
+    SG_CUDA(cudaEventRecord(d->ev_comp[r], d->comp), "sg_m4rm_host event");
+    SG_CUDA(cudaStreamWaitEvent(d->out, d->ev_comp[r], 0), "sg_m4rm_host wait");
+    SG_CUDA(cudaMemcpy2DAsync(C + q0 * wc, m * wc * 8, piece, rows * wc * 8, rows * wc * 8, R,
+                              cudaMemcpyDeviceToHost, d->out),
+            "sg_m4rm_host D2H C");
+    return SG_OK;
+  };
+  int rc;
+  // Every upload is queued before the first product: with pageable host buffers a copy call may
+  // block the host until the stream's earlier work is done, and piece 0's product must never be
+  // waiting for chunk flags that are not queued yet.  Order: A's piece 0, B chunk by chunk (each
+  // followed by its flag), A's other pieces.
+  if ((rc = upload_a(0)) != SG_OK) return rc;
+  for (int j = 0; j < nch; ++j) {
+    const int64_t r0 = j * gpc * 32, rows = std::min<int64_t>(l, (j + 1) * gpc * 32) - r0;
+    SG_CUDA(cudaMemcpy2DAsync(dB + r0 * wc, l * wc * 8, B + r0 * wc, l * wc * 8, rows * wc * 8, R,
+                              cudaMemcpyHostToDevice, d->in),
+            "sg_m4rm_host H2D B");
+    if (wv((CUstream)d->in, (CUdeviceptr)(d->ready + j), epoch, 0) != CUDA_SUCCESS)
+      return fail(SG_ECUDA, "sg_m4rm_host: cuStreamWriteValue32 failed");
+  }
+  for (int r = 1; r < Pr; ++r)
+    if ((rc = upload_a(r)) != SG_OK) return rc;
+  const StreamIn sin{d->ready, epoch, (int)(gpc * 4), err};
+  for (int r = 0; r < Pr; ++r)
+    if ((rc = product(r, r == 0 ? &sin : nullptr)) != SG_OK) return rc;
+  SG_CUDA(cudaMemcpyAsync(d->err_host, err, sizeof(unsigned), cudaMemcpyDeviceToHost, d->comp), "sg_m4rm_host");
+  SG_CUDA(cudaStreamSynchronize(d->out), "sg_m4rm_host sync");
+  SG_CUDA(cudaStreamSynchronize(d->comp), "sg_m4rm_host sync");
+  SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host sync");
+  if (*d->err_host) {
+    const unsigned c = *d->err_host - 1;
+    cudaMemset(err, 0, sizeof(unsigned));
+    return fail(SG_ECUDA, "sg_m4rm_host: a streamed product timed out waiting for B chunk " + std::to_string(c) +
+                              " of " + std::to_string(nch));
+  }
+  g_streamed++;
+  return SG_OK;
+}
+
+}  // namespace
+
+extern "C" {
 
 int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
                  int k, int device) {
@@ -741,13 +996,6 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   if (const char* e = getenv("SG_HOST_CCHUNKS")) Pc = std::max(1, std::min(4, atoi(e)));  // experiments
   Pc = (int)std::max<int64_t>(1, std::min<int64_t>(Pc, wc));
   if (Pc > 1) Pk = 1;
-  struct Io {
-    cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
-    cudaEvent_t ev_in[8], ev_comp[16];
-    Buf buf;
-    std::mutex busy;  // one host-buffer product per device at a time (the staging buffers are shared)
-  };
-  static std::map<int, Io> io_state;
   Io* d;
   char* dbuf = nullptr;
   {
@@ -781,6 +1029,11 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
       d->buf.bytes = need;
     }
     dbuf = (char*)d->buf.p;
+  }
+  const char* stream_e = getenv("SG_HOST_STREAM");  // experiments: 0 = upload B before the products
+  if ((!stream_e || atoi(stream_e) != 0) && Pk == 1 && Pc == 1 && l > 0 && Pr <= 4) {
+    rc = host_streamed(d, dbuf, field, A, B, C, m, l, n, k, device, Pr);
+    if (rc != SG_EUNSUPPORTED) return rc;
   }
   if (Pc > 1) {
     // ---- Pr x Pc grid: uploads in order of first use, products row-major, pieces down as done

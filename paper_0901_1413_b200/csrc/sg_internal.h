@@ -70,10 +70,25 @@ struct M4rmArgs {
                        // B 16-B aligned)
   int tma_a;           // ... and A's index words with 1-D bulk copies (with tma_b only)
 };
+// Streamed B (sg_m4rm_host; stream-K warp-specialized TMA plans, the STRM kernel instantiations):
+// B's k-blocks [c cb, (c+1) cb) may be read once ready[c] - epoch >= 0 (written by the upload
+// stream behind chunk c's copy).  perm: per tile, the order of its 4-block groups (virtual group
+// -> real group) that lets each segment start on blocks that arrive first.  err: set (to the
+// chunk + 1) when a wait times out; the product is then garbage and reported failed.
+struct M4rmStreamArgs : M4rmArgs {
+  const unsigned* ready;
+  unsigned epoch;
+  int chunk_blocks;
+  const int* perm;
+  int ngroups;
+  unsigned* err;
+};
 constexpr int SK_SLOTS = 2;  // compact partial slots per stream-K CTA: its first and last segment
 
+typedef void (*KernelFn)(M4rmArgs, CUtensorMap);  // (args, B as a 3-D u32 tensor map for TMA staging)
+typedef void (*StreamKernelFn)(M4rmStreamArgs, CUtensorMap);
 struct KernelInfo {
-  void (*fn)(M4rmArgs, CUtensorMap);  // (args, B as a 3-D u32 tensor map for TMA staging)
+  KernelFn fn;
   int field, k, rt, threads;  // threads = lookup threads (rows = rt * threads)
   int launch_threads;  // threads + 32 for the warp-specialized schedule
   int sched;           // 0 serial, 1 pipelined (double-buffered table), 2 warp-specialized
@@ -81,6 +96,7 @@ struct KernelInfo {
   int regs;            // filled in lazily from cudaFuncGetAttributes
   int occupancy;       // CTAs per SM, filled lazily
   int ablation;        // experiments only: never planned unless sg_set_ablation selects it
+  StreamKernelFn fn_stream;  // the same variant reading streamed B (M4rmStreamArgs), or nullptr
 };
 
 // Registry of compiled M4RM instantiations (sg_m4rm.cu).
@@ -92,6 +108,8 @@ cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT
                                int wa32, int nwords, cudaStream_t st);
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorMap& tmB, dim3 grid,
                         cudaStream_t st);
+cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, const CUtensorMap& tmB, dim3 grid,
+                                 cudaStream_t st);
 // up to SLICES_MAX equally shaped R-plane row slices with their own plane strides (u32 words)
 constexpr int SLICES_MAX = 8;
 struct SliceSet {
@@ -105,6 +123,9 @@ cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int6
                                  int wc32, int splits, cudaStream_t st);
 cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,
                                   int slabs, int64_t tiles, int nblocks, int64_t units, int ctas, cudaStream_t st);
+
+// load every auxiliary kernel of `field` (index pre-pass, reductions) ahead of a streamed product
+cudaError_t preload_aux_kernels(int field);
 
 // sg_pack.cu
 cudaError_t launch_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld,

@@ -343,6 +343,11 @@ cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorM
                         cudaStream_t st) {
   return launch_pdl(ki.fn, grid, dim3(ki.launch_threads), ki.smem_bytes, st, a, tmB);
 }
+cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, const CUtensorMap& tmB, dim3 grid,
+                                 cudaStream_t st) {
+  if (!ki.fn_stream) return cudaErrorInvalidDeviceFunction;
+  return launch_pdl(ki.fn_stream, grid, dim3(ki.launch_threads), ki.smem_bytes, st, a, tmB);
+}
 
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
                                int wa32, int nwords, cudaStream_t st) {
@@ -356,6 +361,21 @@ cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT
   const int R = field == F2 ? 1 : (field == F5 || field == F7 || field == GF8 || field == Z8) ? 3 : 2;
   dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), R);
   transpose_a_kernel<<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, field == F3);
+  return cudaGetLastError();
+}
+
+cudaError_t preload_aux_kernels(int field) {
+  // Load the pre-pass and reduction kernels of a field now: a lazily loaded kernel may wait for
+  // the device to drain, which a streamed product (waiting on its upload) must never meet.
+  cudaFuncAttributes fa;
+#define SG_PL(FF)                                                  \
+  cudaFuncGetAttributes(&fa, index_words_kernel<FF>);             \
+  cudaFuncGetAttributes(&fa, reduce_streamk_kernel<FF>);          \
+  cudaFuncGetAttributes(&fa, reduce_splits_kernel<FF>);           \
+  cudaFuncGetAttributes(&fa, sum_slices_kernel<FF>)
+  SG_FOR_EACH_FIELD_CASE(field, SG_PL)
+#undef SG_PL
+  cudaFuncGetAttributes(&fa, transpose_a_kernel);
   return cudaGetLastError();
 }
 

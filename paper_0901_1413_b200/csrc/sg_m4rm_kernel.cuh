@@ -30,6 +30,7 @@
 //    sums for split-K / stream-K.
 #pragma once
 #include <cstdio>
+#include <type_traits>
 
 #include "sg_field.cuh"
 #include "sg_internal.h"
@@ -82,6 +83,28 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Streamed B: wait until the upload stream has published chunk c (ready[c] - epoch >= 0, a
+// cyclic compare), then order the TMA (async proxy) reads of that chunk after the acquire.
+// A wait longer than 10 s flags an error and gives up instead of hanging the GPU.
+__device__ __forceinline__ void wait_chunk(const unsigned* ready, int c, unsigned epoch, unsigned* err) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
+  if ((int)(v - epoch) < 0) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      __nanosleep(100);
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) {
+        atomicExch(err, (unsigned)c + 1u);  // the chunk it gave up on, + 1
+        break;
+      }
+    } while ((int)(v - epoch) < 0);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 template <int F> __device__ __forceinline__ V<F> vzero() {
   V<F> v;
@@ -214,8 +237,8 @@ __host__ __device__ constexpr int ws_builders(int sched) { return sched == 2 ? 1
 // ROLE (warp-specialized schedule only): 1 = the builder warps' part, 2 = the lookup warps' part;
 // 0 = everything (the other schedules).  The two roles run separately compiled code so that each
 // can live with its own register budget (setmaxnreg in m4rm_kernel).
-template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE>
-__device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMap* tmB, unsigned char* smem,
+template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE, bool STRM, typename AT>
+__device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB, unsigned char* smem,
                                              const int word0,
                                              const int64_t row0, const int s_begin, const int s_end,
                                              const int mode, const int slot) {
@@ -262,6 +285,22 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
   const bool tma_a = tma_b && a.tma_a;
 
   int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
+  // Streamed products (a.perm, k = 8 only): virtual k-block s of this tile is real block
+  // real_block(s); the 4-block groups are permuted, blocks inside a group keep their order, so
+  // an index record word (RPW blocks) maps to one real record word.  Staging slots, barrier
+  // phases and the F5 offset count virtual blocks.
+  // (compiled into the STRM instantiations only: the resident-B kernels are unchanged)
+  static_assert(!STRM || (WS && K == 8), "streamed B needs the warp-specialized TMA schedule");
+  const int* perm_t = nullptr;
+  if constexpr (STRM) perm_t = a.perm + ((row0 / ROWS) * a.slabs + word0 / SLAB_WORDS) * a.ngroups;
+  auto real_block = [&](int s) -> int {
+    if constexpr (!STRM) return s;
+    return __ldg(perm_t + (s >> 2)) * 4 + (s & 3);
+  };
+  auto real_word = [&](int w) -> int {
+    if constexpr (!STRM || !IW) return w;
+    return real_block(w * RPW) / RPW;
+  };
   // Stage block s's B rows (K x R x 16 B) into bst[s % 3].
   auto issue_b = [&](int s, int t0 = -1, int nthr = NT) {
     if (t0 < 0) t0 = tid;
@@ -270,8 +309,10 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
       // copy (rows past l arrive zero-filled) completing on mbar_b[s % 3]
       if constexpr (K == 8) {
         if (s < s_end && t0 == 0) {
+          const int rs = real_block(s);
+          if constexpr (STRM) wait_chunk(a.ready, rs / a.chunk_blocks, a.epoch, a.err);
           mbar_expect_tx(&mbar_b[s % 3], (unsigned)(K * R * 16));
-          tma_load_3d(bst + (s % 3) * K * R * 4, tmB, word0, s * K, 0, &mbar_b[s % 3]);
+          tma_load_3d(bst + (s % 3) * K * R * 4, tmB, word0, rs * K, 0, &mbar_b[s % 3]);
         }
       }
       return;
@@ -280,7 +321,7 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
       u32* bdst = bst + (s % 3) * K * R * 4;
       for (int q = t0; q < K * R * 2; q += nthr) {
         const int i = q / (R * 2), d = (q >> 1) % R, half = q & 1;
-        const int64_t row = (int64_t)s * K + i;
+        const int64_t row = (int64_t)real_block(s) * K + i;
         const int w = word0 + 2 * half;
         const bool ok = row < a.l && w < a.wc32;
         const u32* src = ok ? a.B + ((int64_t)d * a.l + row) * a.wc32 + w : a.B;
@@ -299,7 +340,8 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
             if (t0 == 0) {
               const int sl = next_word % NSLOT;
               mbar_expect_tx(&mbar_a[sl], ROWS * 4);
-              tma_load_1d(ast + sl * ROWS, a.AT + (int64_t)next_word * a.mpad + row0, ROWS * 4, &mbar_a[sl]);
+              tma_load_1d(ast + sl * ROWS, a.AT + (int64_t)real_word(next_word) * a.mpad + row0, ROWS * 4,
+                         &mbar_a[sl]);
             }
           }
         }
@@ -311,9 +353,10 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
       for (; next_word <= whi; ++next_word) {
         u32* adst = ast + (next_word % NSLOT) * NAP * ROWS;
         const bool ok = next_word < a.wa32;
+        const int rw = real_word(next_word);
         for (int q = t0; q < NAP * ROWS / 4; q += nthr) {
           const int d = q / (ROWS / 4), r4 = q % (ROWS / 4);
-          const u32* src = ok ? a.AT + ((int64_t)d * a.wa32 + next_word) * a.mpad + row0 + 4 * r4 : a.AT;
+          const u32* src = ok ? a.AT + ((int64_t)d * a.wa32 + rw) * a.mpad + row0 + 4 * r4 : a.AT;
           cp_async16(adst + d * ROWS + 4 * r4, src, ok ? 16 : 0);
         }
       }
@@ -663,14 +706,14 @@ __device__ __forceinline__ void m4rm_segment(const M4rmArgs& a, const CUtensorMa
 // U = tiles x k-blocks: a partial tail of one tile, whole tiles, a partial head of another; the
 // partial segments land in compact slots and reduce_streamk sums the slots of every tile.  Otherwise one segment
 // per CTA: (slab, row group, k-split) = blockIdx.
-template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE>
-__device__ __forceinline__ void run_segments(const M4rmArgs& a, const CUtensorMap* tmB, unsigned char* smem,
+template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE, bool STRM, typename AT>
+__device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB, unsigned char* smem,
                                              uint64_t* mbar) {
   constexpr int ROWS = RT * NT;
   constexpr bool TMA_OK = SCHED == 2 && K == 8;
   if (!a.streamk) {
     const int s_begin = blockIdx.z * a.bps;
-    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE>(a, tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS,
+    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE, STRM>(a, tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS,
                                                  s_begin, min(a.nblocks, s_begin + a.bps), a.partial ? 1 : 0,
                                                  blockIdx.z);
     return;
@@ -686,7 +729,7 @@ __device__ __forceinline__ void run_segments(const M4rmArgs& a, const CUtensorMa
     // a whole tile goes straight to C; a partial one (only the range's first or last segment can
     // be partial) to compact slot 2c (first) or 2c + 1 (last), summed by reduce_streamk_kernel
     const bool whole = s0 == 0 && s1 == a.nblocks;
-    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE>(a, tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS,
+    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE, STRM>(a, tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS,
                                                  (tile / a.slabs) * ROWS, s0, s1, whole ? 0 : 2,
                                                  (int)(blockIdx.x * SK_SLOTS + (u == u0 ? 0 : 1)));
     u += s1 - s0;
@@ -705,9 +748,9 @@ __device__ __forceinline__ void run_segments(const M4rmArgs& a, const CUtensorMa
   }
 }
 
-template <int F, int K, int RT, int SCHED, int NT, int ABL = 0>
+template <int F, int K, int RT, int SCHED, int NT, int ABL = 0, bool STRM = false>
 __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
-    m4rm_kernel(const M4rmArgs a, const __grid_constant__ CUtensorMap tmB) {
+    m4rm_kernel(const std::conditional_t<STRM, M4rmStreamArgs, M4rmArgs> a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ROWS = RT * NT;
   if (a.early_trigger) pdl_trigger();
@@ -732,13 +775,13 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
     constexpr int BREGS = 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
     if (threadIdx.x >= NT) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(BREGS));
-      run_segments<F, K, RT, SCHED, NT, ABL, 1>(a, &tmB, smem, mbar);
+      run_segments<F, K, RT, SCHED, NT, ABL, 1, STRM>(a, &tmB, smem, mbar);
     } else {
       asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LREGS));
-      run_segments<F, K, RT, SCHED, NT, ABL, 2>(a, &tmB, smem, mbar);
+      run_segments<F, K, RT, SCHED, NT, ABL, 2, STRM>(a, &tmB, smem, mbar);
     }
   } else {
-    run_segments<F, K, RT, SCHED, NT, ABL, 0>(a, &tmB, smem, mbar);
+    run_segments<F, K, RT, SCHED, NT, ABL, 0, STRM>(a, &tmB, smem, mbar);
   }
 }
 
@@ -752,10 +795,17 @@ constexpr int smem_bytes_for() {
          NSLOT * NAP * RT * NT * 4 + 6 * 8;  // + the B- and A-slot mbarriers
 }
 
+// the streamed-B instantiation of a warp-specialized k = 8 variant (nullptr for the others)
+template <int F, int K, int RT, int P, int NT>
+constexpr StreamKernelFn stream_variant() {
+  if constexpr (P == 2 && K == 8) return m4rm_kernel<F, K, RT, P, NT, 0, true>;
+  else return nullptr;
+}
+
 #define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \
-                               smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0}
+                               smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0, stream_variant<F, K, RT, P, NT>()}
 #define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (NT) + ws_builders(P), P, \
-                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A}
+                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr}
 // k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
 #define SG_KSET8(F)                                                                                 \
   SG_K(F, 8, 1, 0, 256), SG_K(F, 8, 2, 0, 256), SG_K(F, 8, 4, 0, 256), SG_K(F, 8, 8, 0, 256), \

@@ -61,6 +61,8 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
         a = A.planes.contiguous()
         b = B.planes.contiguous()
         C = BitslicedMatrix.zero(field, m, n, device="cpu") if out is None else out
+        if out is None and a.is_pinned() and b.is_pinned():
+            C.planes = C.planes.pin_memory()  # page-locked in, page-locked out: async copies
         if m and n:
             _lib.check(L.sg_m4rm_host(field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k,
                                       torch.cuda.current_device()))

@@ -10,7 +10,7 @@ import torch
 
 import oracle
 import paper_0901_1413_b200 as sg
-from paper_0901_1413_b200 import _core_cuda, m4rm as m4rm_mod
+from paper_0901_1413_b200 import _core_cuda, _lib, m4rm as m4rm_mod
 from tests import _golden
 
 pytestmark = pytest.mark.gpu
@@ -262,6 +262,56 @@ def test_host_buffers_pipelined_chunks():
         os.environ.pop("SG_HOST_KCHUNKS", None)
         os.environ.pop("SG_HOST_CHUNKS", None)
         os.environ.pop("SG_HOST_CCHUNKS", None)
+
+
+def test_host_streamed_b():
+    """sg_m4rm_host with B streamed into a running product (host_streamed, sg_api.cu): the first
+    row piece's product waits per k-block for B's chunk flags and takes each tile's k-blocks in
+    arrival order (streamed_order).  Forced stream-K warp-specialized plans, every field, ragged
+    m / l, 1..64 B chunks, 1..3 row pieces: bit-exact against the oracle, and the streamed path
+    must have run (sg_host_streamed_count); l with k-blocks % 4 != 0 falls back."""
+    L = _lib.load()
+    rt = {"f2": 16, "f3": 8, "gf4": 8, "z4": 8, "f5": 4, "f7": 4, "gf8": 4, "z8": 4}
+    try:
+        for fname in FIELDS:
+            for (m, l, n) in ((2500, 1024, 384), (700, 990, 512), (1800, 2048, 256)):
+                A = oracle.random_dense(fname, m, l, m + 7)
+                B = oracle.random_dense(fname, l, n, n + 3)
+                want = expect(fname, A, B)
+                Ah = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, A), l, device="cpu")
+                Bh = sg.BitslicedMatrix.from_planes(FIELDS[fname], oracle.pack(fname, B), n, device="cpu")
+                Ap = sg.BitslicedMatrix(FIELDS[fname], m, l, Ah.planes.pin_memory())
+                Bp = sg.BitslicedMatrix(FIELDS[fname], l, n, Bh.planes.pin_memory())
+                m4rm_mod.set_plan_override(rt[fname], -1, 2)
+                try:
+                    for rows in (m, m // 3):
+                        m4rm_mod.plan(FIELDS[fname], rows, l, n)
+                    forced = True
+                except Exception:  # no stream-K warp-specialized variant fits (F2: 2 CTAs per SM)
+                    m4rm_mod.set_plan_override(0, 0)
+                    forced = False
+                for nch, pr, pinned in (("1", "1", 0), ("3", "2", 1), ("16", "3", 0), ("64", "2", 1), ("7", "1", 1)):
+                    os.environ["SG_HOST_BCHUNKS"], os.environ["SG_HOST_CHUNKS"] = nch, pr
+                    c0 = L.sg_host_streamed_count()
+                    try:
+                        C = sg.m4rm_multiply(*((Ap, Bp) if pinned else (Ah, Bh)), sg.M4rmParams(8))
+                    except Exception as e:
+                        raise AssertionError((fname, m, l, n, nch, pr, pinned)) from e
+                    assert C.planes.is_pinned() == bool(pinned)
+                    assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, nch, pr)
+                    if forced:
+                        assert L.sg_host_streamed_count() == c0 + 1, (fname, m, l, n, nch, pr)
+        A = oracle.random_dense("f5", 2500, 1000, 1)  # 125 k-blocks: not streamable
+        B = oracle.random_dense("f5", 1000, 256, 2)
+        Ah = sg.BitslicedMatrix.from_planes(sg.F5, oracle.pack("f5", A), 1000, device="cpu")
+        Bh = sg.BitslicedMatrix.from_planes(sg.F5, oracle.pack("f5", B), 256, device="cpu")
+        m4rm_mod.set_plan_override(rt["f5"], -1, 2)
+        c0 = L.sg_host_streamed_count()
+        assert np.array_equal(sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8)).planes_numpy(), expect("f5", A, B))
+        assert L.sg_host_streamed_count() == c0
+    finally:
+        os.environ.pop("SG_HOST_BCHUNKS", None)
+        os.environ.pop("SG_HOST_CHUNKS", None)
 
 
 def test_elementwise_ops_match_dense():
