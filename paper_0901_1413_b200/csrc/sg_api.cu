@@ -817,6 +817,9 @@ struct Io {
   unsigned* ready = nullptr;
   unsigned epoch = 0;
   unsigned* err_host = nullptr;
+  cudaStream_t flags = nullptr;  // writes the chunk flags behind the copies' events
+  cudaEvent_t ev_chunk[64];
+  std::map<int, bool> preloaded;  // fields whose auxiliary kernels are loaded
 };
 std::map<int, Io> io_state;
 
@@ -865,25 +868,32 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
     }
     cudaError_t e;
     if (!workspace_for(device, d->comp, (size_t)ws_need, &e)) return cuda_fail(e, "sg_m4rm_host workspace");
-    SG_CUDA(preload_aux_kernels(field), "sg_m4rm_host preload");
+    if (!d->preloaded[field]) {
+      SG_CUDA(preload_aux_kernels(field), "sg_m4rm_host preload");
+      d->preloaded[field] = true;
+    }
     if (!d->ready) {
+      SG_CUDA(cudaStreamCreateWithFlags(&d->flags, cudaStreamNonBlocking), "sg_m4rm_host stream");
+      for (int i = 0; i < MAX_BCHUNKS; ++i)
+        SG_CUDA(cudaEventCreateWithFlags(&d->ev_chunk[i], cudaEventDisableTiming), "sg_m4rm_host event");
       SG_CUDA(cudaMalloc(&d->ready, (MAX_BCHUNKS + 1) * sizeof(unsigned)), "sg_m4rm_host flags");
       SG_CUDA(cudaMemset(d->ready, 0, (MAX_BCHUNKS + 1) * sizeof(unsigned)), "sg_m4rm_host flags");
       SG_CUDA(cudaMallocHost(&d->err_host, sizeof(unsigned)), "sg_m4rm_host flags");
       // first use of the stream memory operations while nothing waits on them
-      if (wv((CUstream)d->in, (CUdeviceptr)(d->ready + MAX_BCHUNKS), 0u, 0) != CUDA_SUCCESS) {
+      if (wv((CUstream)d->flags, (CUdeviceptr)(d->ready + MAX_BCHUNKS), 0u, 0) != CUDA_SUCCESS) {
         cudaGetLastError();
         return SG_EUNSUPPORTED;
       }
-      SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host flags");
+      SG_CUDA(cudaStreamSynchronize(d->flags), "sg_m4rm_host flags");
     }
   }
   unsigned* err = d->ready + MAX_BCHUNKS;
   const unsigned epoch = ++d->epoch;
-  // B chunks: whole 4-block groups (32 rows), >= 128 KB each, at most MAX_BCHUNKS
+  // B chunks: whole 4-block groups (32 rows), >= 512 KB each, at most 16 by default
   const int64_t groups = (l + 31) / 32;
   const size_t b_bytes = (size_t)R * l * wc * 8;
-  int nch = nch_env > 0 ? nch_env : (int)std::min<int64_t>(16, std::max<int64_t>(1, (int64_t)(b_bytes >> 17)));
+  // (F5 4096^3, tools/e2e_sweep.py: 8-16 chunks of 0.4-0.8 MB best; 32 lose to per-copy setup)
+  int nch = nch_env > 0 ? nch_env : (int)std::min<int64_t>(16, std::max<int64_t>(1, (int64_t)(b_bytes >> 19)));
   nch = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)nch, groups, (int64_t)MAX_BCHUNKS}));
   const int64_t gpc = (groups + nch - 1) / nch;  // groups per chunk
   nch = (int)((groups + gpc - 1) / gpc);
@@ -897,6 +907,17 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
     cur += up((size_t)R * (rcut(r + 1) - rcut(r)) * wa * 8);
   }
   uint64_t* dC = (uint64_t*)cur;  // pieces back to back, each [R][rows][wc]
+  // SG_HOST_TRACE=1 (experiments): event timestamps of the pipeline steps on stderr
+  static const bool trace = getenv("SG_HOST_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  auto mark = [&](const std::string& what, cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.push_back({what, e});
+  };
+  mark("start", d->in);
   auto upload_a = [&](int r) -> int {
     const int64_t q0 = rcut(r), rows = rcut(r + 1) - q0;
     if (rows > 0)
@@ -904,6 +925,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
                                 cudaMemcpyHostToDevice, d->in),
               "sg_m4rm_host H2D A");
     SG_CUDA(cudaEventRecord(d->ev_in[r], d->in), "sg_m4rm_host event");
+    mark("in: A piece " + std::to_string(r) + " up", d->in);
     return SG_OK;
   };
   auto product = [&](int r, const StreamIn* sin) -> int {
@@ -911,13 +933,16 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
     SG_CUDA(cudaStreamWaitEvent(d->comp, d->ev_in[r], 0), "sg_m4rm_host wait");
     if (rows <= 0) return SG_OK;
     uint64_t* piece = dC + (int64_t)R * q0 * wc;
+    mark("comp: product " + std::to_string(r) + " queued (inputs up)", d->comp);
     int rc = m4rm_device(field, dAp[r], dB, piece, rows, l, n, k, nullptr, 0, d->comp, sin);
     if (rc != SG_OK) return rc;
     SG_CUDA(cudaEventRecord(d->ev_comp[r], d->comp), "sg_m4rm_host event");
     SG_CUDA(cudaStreamWaitEvent(d->out, d->ev_comp[r], 0), "sg_m4rm_host wait");
+    mark("comp: product " + std::to_string(r) + " done", d->comp);
     SG_CUDA(cudaMemcpy2DAsync(C + q0 * wc, m * wc * 8, piece, rows * wc * 8, rows * wc * 8, R,
                               cudaMemcpyDeviceToHost, d->out),
             "sg_m4rm_host D2H C");
+    mark("out: piece " + std::to_string(r) + " down", d->out);
     return SG_OK;
   };
   int rc;
@@ -928,11 +953,18 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   if ((rc = upload_a(0)) != SG_OK) return rc;
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = j * gpc * 32, rows = std::min<int64_t>(l, (j + 1) * gpc * 32) - r0;
+    // Each flag goes out on its own stream behind its copy's event.  (Measured on B200: B's
+    // chunks still arrive at ~30 GB/s against ~50 GB/s for one large copy -- every chunk pays
+    // the copy setup; alternating two upload streams made the arrival order worse.)
+    cudaStream_t cs = d->in;
     SG_CUDA(cudaMemcpy2DAsync(dB + r0 * wc, l * wc * 8, B + r0 * wc, l * wc * 8, rows * wc * 8, R,
-                              cudaMemcpyHostToDevice, d->in),
+                              cudaMemcpyHostToDevice, cs),
             "sg_m4rm_host H2D B");
-    if (wv((CUstream)d->in, (CUdeviceptr)(d->ready + j), epoch, 0) != CUDA_SUCCESS)
+    SG_CUDA(cudaEventRecord(d->ev_chunk[j], cs), "sg_m4rm_host event");
+    SG_CUDA(cudaStreamWaitEvent(d->flags, d->ev_chunk[j], 0), "sg_m4rm_host wait");
+    if (wv((CUstream)d->flags, (CUdeviceptr)(d->ready + j), epoch, 0) != CUDA_SUCCESS)
       return fail(SG_ECUDA, "sg_m4rm_host: cuStreamWriteValue32 failed");
+    if (j == 0 || j == nch - 1 || j == nch / 2) mark("in: B chunk " + std::to_string(j) + " up", d->in);
   }
   for (int r = 1; r < Pr; ++r)
     if ((rc = upload_a(r)) != SG_OK) return rc;
@@ -943,6 +975,16 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   SG_CUDA(cudaStreamSynchronize(d->out), "sg_m4rm_host sync");
   SG_CUDA(cudaStreamSynchronize(d->comp), "sg_m4rm_host sync");
   SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host sync");
+  SG_CUDA(cudaStreamSynchronize(d->flags), "sg_m4rm_host sync");
+  if (trace) {
+    fprintf(stderr, "host_streamed trace Pr=%d nch=%d\n", Pr, nch);
+    for (auto& mk : marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, marks[0].second, mk.second);
+      fprintf(stderr, "  %8.3f ms  %s\n", ms, mk.first.c_str());
+    }
+    for (auto& mk : marks) cudaEventDestroy(mk.second);
+  }
   if (*d->err_host) {
     const unsigned c = *d->err_host - 1;
     cudaMemset(err, 0, sizeof(unsigned));
