@@ -63,7 +63,9 @@ DevState& dev_state(int device) {
     for (int i = 0; i < m4rm_kernel_count(); ++i) {
       KernelInfo* k = m4rm_kernel_at(i);
       cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
-      if (k->fn_stream) cudaFuncSetAttribute(k->fn_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
+      if (k->fn_stream &&
+          cudaFuncSetAttribute(k->fn_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_stream) != cudaSuccess)
+        k->fn_stream = nullptr;  // does not fit this device: no streamed variant
       cudaFuncAttributes fa;
       if (cudaFuncGetAttributes(&fa, k->fn) == cudaSuccess) k->regs = fa.numRegs;
       int occ = 0;
@@ -416,15 +418,15 @@ int check_mul_args(int field, const void* A, const void* B, const void* C, int64
 struct StreamIn {
   const unsigned* ready;
   unsigned epoch;
-  int chunk_blocks;
+  int first_groups;  // B's chunk j = 4-block groups [g0 (2^j - 1), g0 (2^(j+1) - 1)), g0 = first_groups
   unsigned* err;
 };
 
 // One stream-K wave of the warp-specialized kernel: its builder warps stage every k-block by
 // TMA, so they can wait for each block's chunk; the 4-block group order needs nblocks % 4 == 0.
 bool streamable(const Plan& p) {
-  return p.streamk && p.ki->sched == 2 && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 && p.tiles > 0 &&
-         (int64_t)p.tiles * (p.nblocks / 4) <= (int64_t)1 << 24;
+  return p.streamk && p.ki->sched == 2 && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 &&
+         p.tiles > 0 && p.nblocks / 4 <= STRM_MAX_GROUPS && (int64_t)p.tiles * (p.nblocks / 4) <= (int64_t)1 << 24;
 }
 
 typedef std::tuple<int, int, int64_t, int64_t, int64_t, unsigned> PermKey;
@@ -772,7 +774,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
     static_cast<M4rmArgs&>(sa) = a;
     sa.ready = sin->ready;
     sa.epoch = sin->epoch;
-    sa.chunk_blocks = sin->chunk_blocks;
+    sa.first_groups = sin->first_groups;
     sa.perm = perm;
     sa.ngroups = p.nblocks / 4;
     sa.err = sin->err;
@@ -845,8 +847,6 @@ constexpr int MAX_BCHUNKS = 64;
 // Later pieces find B complete.  Returns SG_EUNSUPPORTED when the product cannot stream.
 int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
                   int64_t l, int64_t n, int k, int device, int Pr) {
-  const char* nch_e = getenv("SG_HOST_BCHUNKS");  // experiments: number of B chunks
-  const int nch_env = nch_e ? atoi(nch_e) : 0;
   const PFN_cuStreamWriteValue32_v11070 wv = write_value_fn();
   if (!wv) return SG_EUNSUPPORTED;
   const int R = planes(field);
@@ -889,14 +889,21 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   }
   unsigned* err = d->ready + MAX_BCHUNKS;
   const unsigned epoch = ++d->epoch;
-  // B chunks: whole 4-block groups (32 rows), >= 512 KB each, at most 16 by default
+  // B chunks: whole 4-block groups (32 rows) in geometrically growing chunks, g0, 2 g0, 4 g0, ...
+  // (chunk j = groups [g0 (2^j - 1), g0 (2^(j+1) - 1))): the first chunk is small so the product
+  // starts early, later ones large so fewer copies pay the per-copy setup, and each arrives
+  // before the product needs it (the product consumes B at a steady rate while the upload's
+  // lead grows).  g0 = groups / 32 by default (F5 4096^3, tools/e2e_sweep.py: 4 of 128 groups
+  // 0.716 ms, 2: 0.725, 8: 0.776; equal chunks of 8-16 groups: 0.72).
   const int64_t groups = (l + 31) / 32;
   const size_t b_bytes = (size_t)R * l * wc * 8;
-  // (F5 4096^3, tools/e2e_sweep.py: 8-16 chunks of 0.4-0.8 MB best; 32 lose to per-copy setup)
-  int nch = nch_env > 0 ? nch_env : (int)std::min<int64_t>(16, std::max<int64_t>(1, (int64_t)(b_bytes >> 19)));
-  nch = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)nch, groups, (int64_t)MAX_BCHUNKS}));
-  const int64_t gpc = (groups + nch - 1) / nch;  // groups per chunk
-  nch = (int)((groups + gpc - 1) / gpc);
+  const char* g0_e = getenv("SG_HOST_BFIRST");  // experiments: groups in the first chunk
+  int64_t g0 = g0_e ? atoll(g0_e) : (groups + 31) / 32;
+  g0 = std::max<int64_t>(1, std::min<int64_t>(g0, groups));
+  auto chunk_lo = [&](int j) { return std::min<int64_t>(groups, g0 * (((int64_t)1 << j) - 1)); };
+  int nch = 1;
+  while (chunk_lo(nch) < groups) ++nch;
+  if (nch > MAX_BCHUNKS) return SG_EUNSUPPORTED;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   char* cur = dbuf;
   uint64_t* dB = (uint64_t*)cur;
@@ -952,7 +959,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   // followed by its flag), A's other pieces.
   if ((rc = upload_a(0)) != SG_OK) return rc;
   for (int j = 0; j < nch; ++j) {
-    const int64_t r0 = j * gpc * 32, rows = std::min<int64_t>(l, (j + 1) * gpc * 32) - r0;
+    const int64_t r0 = chunk_lo(j) * 32, rows = std::min<int64_t>(l, chunk_lo(j + 1) * 32) - r0;
     // Each flag goes out on its own stream behind its copy's event.  (Measured on B200: B's
     // chunks still arrive at ~30 GB/s against ~50 GB/s for one large copy -- every chunk pays
     // the copy setup; alternating two upload streams made the arrival order worse.)
@@ -968,7 +975,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   }
   for (int r = 1; r < Pr; ++r)
     if ((rc = upload_a(r)) != SG_OK) return rc;
-  const StreamIn sin{d->ready, epoch, (int)(gpc * 4), err};
+  const StreamIn sin{d->ready, epoch, (int)g0, err};
   for (int r = 0; r < Pr; ++r)
     if ((rc = product(r, r == 0 ? &sin : nullptr)) != SG_OK) return rc;
   SG_CUDA(cudaMemcpyAsync(d->err_host, err, sizeof(unsigned), cudaMemcpyDeviceToHost, d->comp), "sg_m4rm_host");

@@ -71,14 +71,15 @@ struct M4rmArgs {
   int tma_a;           // ... and A's index words with 1-D bulk copies (with tma_b only)
 };
 // Streamed B (sg_m4rm_host; stream-K warp-specialized TMA plans, the STRM kernel instantiations):
-// B's k-blocks [c cb, (c+1) cb) may be read once ready[c] - epoch >= 0 (written by the upload
-// stream behind chunk c's copy).  perm: per tile, the order of its 4-block groups (virtual group
+// B's chunk c -- 4-block groups [g0 (2^c - 1), g0 (2^(c+1) - 1)), g0 = first_groups: chunks
+// double in size -- may be read once ready[c] - epoch >= 0 (written by the upload stream behind
+// chunk c's copy).  perm: per tile, the order of its 4-block groups (virtual group
 // -> real group) that lets each segment start on blocks that arrive first.  err: set (to the
 // chunk + 1) when a wait times out; the product is then garbage and reported failed.
 struct M4rmStreamArgs : M4rmArgs {
   const unsigned* ready;
   unsigned epoch;
-  int chunk_blocks;
+  int first_groups;
   const int* perm;
   int ngroups;
   unsigned* err;
@@ -97,7 +98,10 @@ struct KernelInfo {
   int occupancy;       // CTAs per SM, filled lazily
   int ablation;        // experiments only: never planned unless sg_set_ablation selects it
   StreamKernelFn fn_stream;  // the same variant reading streamed B (M4rmStreamArgs), or nullptr
+  int smem_stream;           // ... and its dynamic shared memory (+ the staged group order)
 };
+// streamed products stage their tile's group order in shared memory: at most this many groups
+constexpr int STRM_MAX_GROUPS = 2048;
 
 // Registry of compiled M4RM instantiations (sg_m4rm.cu).
 int m4rm_kernel_count();

@@ -346,7 +346,7 @@ cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorM
 cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, const CUtensorMap& tmB, dim3 grid,
                                  cudaStream_t st) {
   if (!ki.fn_stream) return cudaErrorInvalidDeviceFunction;
-  return launch_pdl(ki.fn_stream, grid, dim3(ki.launch_threads), ki.smem_bytes, st, a, tmB);
+  return launch_pdl(ki.fn_stream, grid, dim3(ki.launch_threads), ki.smem_stream, st, a, tmB);
 }
 
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,

@@ -89,13 +89,13 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // A wait longer than 10 s flags an error and gives up instead of hanging the GPU.
 __device__ __forceinline__ void wait_chunk(const unsigned* ready, int c, unsigned epoch, unsigned* err) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
   if ((int)(v - epoch) < 0) {
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     do {
       __nanosleep(100);
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 10000000000ull) {
         atomicExch(err, (unsigned)c + 1u);  // the chunk it gave up on, + 1
@@ -103,7 +103,8 @@ __device__ __forceinline__ void wait_chunk(const unsigned* ready, int c, unsigne
       }
     } while ((int)(v - epoch) < 0);
   }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");        // the chunk's data after the flag ...
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // ... for the TMA (async proxy) reads too
 }
 
 template <int F> __device__ __forceinline__ V<F> vzero() {
@@ -275,6 +276,8 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
   uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ROWS);  // [3] B-slot barriers
   uint64_t* mbar_a = mbar_b + 3;                                               // [3] A-slot barriers
+  // STRM only: this segment's tile's group order, staged by the builder warps ([ngroups] u16)
+  unsigned short* perm_s = reinterpret_cast<unsigned short*>(mbar_a + 3);
 
   const int tid = threadIdx.x;
   if (s_begin >= s_end) return;
@@ -291,12 +294,13 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // phases and the F5 offset count virtual blocks.
   // (compiled into the STRM instantiations only: the resident-B kernels are unchanged)
   static_assert(!STRM || (WS && K == 8), "streamed B needs the warp-specialized TMA schedule");
-  const int* perm_t = nullptr;
-  if constexpr (STRM) perm_t = a.perm + ((row0 / ROWS) * a.slabs + word0 / SLAB_WORDS) * a.ngroups;
   auto real_block = [&](int s) -> int {
     if constexpr (!STRM) return s;
-    return __ldg(perm_t + (s >> 2)) * 4 + (s & 3);
+    return (int)perm_s[s >> 2] * 4 + (s & 3);
   };
+  // STRM: chunks up to ready_upto are known to have landed (the upload stream publishes them in
+  // order), so a block of an earlier chunk needs no flag read
+  int ready_upto = -1;
   auto real_word = [&](int w) -> int {
     if constexpr (!STRM || !IW) return w;
     return real_block(w * RPW) / RPW;
@@ -310,7 +314,13 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       if constexpr (K == 8) {
         if (s < s_end && t0 == 0) {
           const int rs = real_block(s);
-          if constexpr (STRM) wait_chunk(a.ready, rs / a.chunk_blocks, a.epoch, a.err);
+          if constexpr (STRM) {
+            const int c = 31 - __clz((rs >> 2) / a.first_groups + 1);
+            if (c > ready_upto) {
+              wait_chunk(a.ready, c, a.epoch, a.err);
+              ready_upto = c;
+            }
+          }
           mbar_expect_tx(&mbar_b[s % 3], (unsigned)(K * R * 16));
           tma_load_3d(bst + (s % 3) * K * R * 4, tmB, word0, rs * K, 0, &mbar_b[s % 3]);
         }
@@ -524,6 +534,11 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       // ------------------------------------------------ builder warps
       const int bt = tid - NT;
       auto bsync = [] { nbar_sync(5, NBT); };
+      if constexpr (STRM) {
+        const int* pt = a.perm + ((row0 / ROWS) * a.slabs + word0 / SLAB_WORDS) * a.ngroups;
+        for (int g = bt; g < a.ngroups; g += NBT) perm_s[g] = (unsigned short)__ldg(pt + g);
+        bsync();
+      }
       issue_b(s_begin, bt, NBT);
       pdl_wait();  // A's index words come from the pre-pass (B's first rows are already on the way)
       issue_a(s_begin, bt, NBT);
@@ -803,9 +818,10 @@ constexpr StreamKernelFn stream_variant() {
 }
 
 #define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \
-                               smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0, stream_variant<F, K, RT, P, NT>()}
+                               smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0, stream_variant<F, K, RT, P, NT>(), \
+                               smem_bytes_for<F, K, RT, P, NT>() + 2 * STRM_MAX_GROUPS}
 #define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (NT) + ws_builders(P), P, \
-                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr}
+                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr, 0}
 // k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
 #define SG_KSET8(F)                                                                                 \
   SG_K(F, 8, 1, 0, 256), SG_K(F, 8, 2, 0, 256), SG_K(F, 8, 4, 0, 256), SG_K(F, 8, 8, 0, 256), \

@@ -268,7 +268,7 @@ def test_host_streamed_b():
     """sg_m4rm_host with B streamed into a running product (host_streamed, sg_api.cu): the first
     row piece's product waits per k-block for B's chunk flags and takes each tile's k-blocks in
     arrival order (streamed_order).  Forced stream-K warp-specialized plans, every field, ragged
-    m / l, 1..64 B chunks, 1..3 row pieces: bit-exact against the oracle, and the streamed path
+    m / l, first B chunk of 1..64 groups (chunks double), 1..3 row pieces: bit-exact against the oracle, and the streamed path
     must have run (sg_host_streamed_count); l with k-blocks % 4 != 0 falls back."""
     L = _lib.load()
     rt = {"f2": 16, "f3": 8, "gf4": 8, "z4": 8, "f5": 4, "f7": 4, "gf8": 4, "z8": 4}
@@ -290,17 +290,17 @@ def test_host_streamed_b():
                 except Exception:  # no stream-K warp-specialized variant fits (F2: 2 CTAs per SM)
                     m4rm_mod.set_plan_override(0, 0)
                     forced = False
-                for nch, pr, pinned in (("1", "1", 0), ("3", "2", 1), ("16", "3", 0), ("64", "2", 1), ("7", "1", 1)):
-                    os.environ["SG_HOST_BCHUNKS"], os.environ["SG_HOST_CHUNKS"] = nch, pr
+                for g0, pr, pinned in (("1", "1", 0), ("3", "2", 1), ("16", "3", 0), ("64", "2", 1), ("7", "1", 1)):
+                    os.environ["SG_HOST_BFIRST"], os.environ["SG_HOST_CHUNKS"] = g0, pr
                     c0 = L.sg_host_streamed_count()
                     try:
                         C = sg.m4rm_multiply(*((Ap, Bp) if pinned else (Ah, Bh)), sg.M4rmParams(8))
                     except Exception as e:
-                        raise AssertionError((fname, m, l, n, nch, pr, pinned)) from e
+                        raise AssertionError((fname, m, l, n, g0, pr, pinned)) from e
                     assert C.planes.is_pinned() == bool(pinned)
-                    assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, nch, pr)
+                    assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, g0, pr)
                     if forced:
-                        assert L.sg_host_streamed_count() == c0 + 1, (fname, m, l, n, nch, pr)
+                        assert L.sg_host_streamed_count() == c0 + 1, (fname, m, l, n, g0, pr)
         A = oracle.random_dense("f5", 2500, 1000, 1)  # 125 k-blocks: not streamable
         B = oracle.random_dense("f5", 1000, 256, 2)
         Ah = sg.BitslicedMatrix.from_planes(sg.F5, oracle.pack("f5", A), 1000, device="cpu")
@@ -310,7 +310,7 @@ def test_host_streamed_b():
         assert np.array_equal(sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8)).planes_numpy(), expect("f5", A, B))
         assert L.sg_host_streamed_count() == c0
     finally:
-        os.environ.pop("SG_HOST_BCHUNKS", None)
+        os.environ.pop("SG_HOST_BFIRST", None)
         os.environ.pop("SG_HOST_CHUNKS", None)
 
 

@@ -1,6 +1,6 @@
-"""e2e sweep of the streamed host pipeline: row pieces x B chunks (SG_HOST_CHUNKS, SG_HOST_BCHUNKS).
+"""e2e sweep of the streamed host pipeline: row pieces x first B chunk in 32-row groups (SG_HOST_CHUNKS, SG_HOST_BFIRST).
 
-python tools/e2e_sweep.py [--config 1] [--pieces 1,2,3,4] [--bchunks 4,8,16,32] [--stream 0,1]"""
+python tools/e2e_sweep.py [--config 1] [--pieces 1,2,3,4] [--bfirst 2,4,8,16] [--stream 0,1]"""
 import argparse
 import os
 import subprocess
@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="1")
 ap.add_argument("--pieces", default="1,2,3,4")
-ap.add_argument("--bchunks", default="4,8,16,32")
+ap.add_argument("--bfirst", default="2,4,8,16")
 ap.add_argument("--stream", default="1")
 a = ap.parse_args()
 code = f"""
@@ -34,7 +34,7 @@ print(name, 'min %.3f med %.3f ms' % (1e3 * ts[0], 1e3 * ts[len(ts) // 2]), flus
 """
 for st in a.stream.split(","):
     for pr in a.pieces.split(","):
-        for bc in a.bchunks.split(","):
-            env = dict(os.environ, SG_HOST_STREAM=st, SG_HOST_CHUNKS=pr, SG_HOST_BCHUNKS=bc)
+        for bc in a.bfirst.split(","):
+            env = dict(os.environ, SG_HOST_STREAM=st, SG_HOST_CHUNKS=pr, SG_HOST_BFIRST=bc)
             out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
-            print(f"stream={st} pieces={pr} bchunks={bc} |", out.stdout.strip(), out.stderr.strip()[-300:], flush=True)
+            print(f"stream={st} pieces={pr} bfirst={bc} |", out.stdout.strip(), out.stderr.strip()[-300:], flush=True)
