@@ -419,6 +419,7 @@ struct StreamIn {
   const unsigned* ready;
   unsigned epoch;
   int first_groups;  // B's chunk j = 4-block groups [g0 (2^j - 1), g0 (2^(j+1) - 1)), g0 = first_groups
+  int nchunks;
   unsigned* err;
 };
 
@@ -775,6 +776,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
     sa.ready = sin->ready;
     sa.epoch = sin->epoch;
     sa.first_groups = sin->first_groups;
+    sa.nchunks = sin->nchunks;
     sa.perm = perm;
     sa.ngroups = p.nblocks / 4;
     sa.err = sin->err;
@@ -975,7 +977,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   }
   for (int r = 1; r < Pr; ++r)
     if ((rc = upload_a(r)) != SG_OK) return rc;
-  const StreamIn sin{d->ready, epoch, (int)g0, err};
+  const StreamIn sin{d->ready, epoch, (int)g0, nch, err};
   for (int r = 0; r < Pr; ++r)
     if ((rc = product(r, r == 0 ? &sin : nullptr)) != SG_OK) return rc;
   SG_CUDA(cudaMemcpyAsync(d->err_host, err, sizeof(unsigned), cudaMemcpyDeviceToHost, d->comp), "sg_m4rm_host");

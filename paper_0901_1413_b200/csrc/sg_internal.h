@@ -80,6 +80,7 @@ struct M4rmStreamArgs : M4rmArgs {
   const unsigned* ready;
   unsigned epoch;
   int first_groups;
+  int nchunks;
   const int* perm;
   int ngroups;
   unsigned* err;

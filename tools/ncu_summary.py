@@ -25,7 +25,8 @@ STALLS = "smsp__average_warps_issue_stalled_"
 
 
 def main(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = (open(path).read() if path.endswith(".csv") else  # a saved `--page raw --csv` export
+           subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:

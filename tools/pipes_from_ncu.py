@@ -19,7 +19,8 @@ tag = sys.argv[1]
 out = {"_source": f"profiles/{tag}_pipes.json from ncu --set full captures of the M4RM kernel"}
 for arg in sys.argv[2:]:
     name, rep = arg.split("::", 1)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = (open(rep).read() if rep.endswith(".csv") else  # a saved `--page raw --csv` export
+           subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(io.StringIO(raw)))
     d = dict(zip(rows[0], rows[2]))
     out[name] = {k: float(d[v]) for k, v in M.items() if v in d and d[v]}

@@ -11,7 +11,8 @@ tag = sys.argv[1]
 out = {"_source": f"profiles/{tag}_traffic.json from ncu --set full captures of the M4RM kernel"}
 for arg in sys.argv[2:]:
     name, rep = arg.split("::", 1)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = (open(rep).read() if rep.endswith(".csv") else  # a saved `--page raw --csv` export
+           subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = dict(zip(hdr, vals))
