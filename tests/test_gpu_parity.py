@@ -265,7 +265,7 @@ def test_host_buffers_pipelined_chunks():
 
 
 def test_host_streamed_b():
-    """sg_m4rm_host with B streamed into a running product (host_streamed, sg_api.cu): the first
+    """sg_m4rm_host with B streamed into a running product (host_streamed, sg_host.cu): the first
     row piece's product waits per k-block for B's chunk flags and takes each tile's k-blocks in
     arrival order (streamed_order).  Forced stream-K warp-specialized plans, every field, ragged
     m / l, first B chunk of 1..64 groups (chunks double), 1..3 row pieces: bit-exact against the oracle, and the streamed path

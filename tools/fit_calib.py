@@ -1,4 +1,4 @@
-"""Fit the planner's per-variant cost constants (g_calib in csrc/sg_api.cu) from tools/tune.py output.
+"""Fit the planner's per-variant cost constants (g_calib in csrc/sg_plan.cu) from tools/tune.py output.
 
 python tools/fit_calib.py tune1.jsonl [tune2.jsonl ...]   -> C++ table rows on stdout
 
