@@ -566,6 +566,49 @@ def test_host_path_thread_safety():
     assert not errors, errors
 
 
+def test_host_streamed_thread_safety():
+    """Concurrent streamed-B host products (pinned buffers, the headline's F5 shape class at
+    2048 x 1024 x 512) from several threads on one device: each gets its own correct result, and
+    the streamed path ran for every call (the per-device pipeline state is serialized, the chunk
+    flags carry per-call epochs)."""
+    import threading
+    L = _lib.load()
+    jobs = []
+    for i, fname in enumerate(("f5", "f7", "f3", "gf4")):
+        m, l, n = 2048 + 256 * i, 1024, 512
+        A = oracle.random_dense(fname, m, l, 60 + i)
+        B = oracle.random_dense(fname, l, n, 70 + i)
+        Ah = sg.BitslicedMatrix(FIELDS[fname], m, l, sg.BitslicedMatrix.from_planes(
+            FIELDS[fname], oracle.pack(fname, A), l, device="cpu").planes.pin_memory())
+        Bh = sg.BitslicedMatrix(FIELDS[fname], l, n, sg.BitslicedMatrix.from_planes(
+            FIELDS[fname], oracle.pack(fname, B), n, device="cpu").planes.pin_memory())
+        jobs.append((fname, Ah, Bh, expect(fname, A, B)))
+    m4rm_mod.set_plan_override(0, -1, 2)  # stream-K, warp-specialized: streamable
+    errors = []
+    c0 = L.sg_host_streamed_count()
+
+    def run(job):
+        fname, Ah, Bh, want = job
+        try:
+            for _ in range(4):
+                C = sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8))
+                if not np.array_equal(C.planes_numpy(), want):
+                    errors.append(fname)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    try:
+        threads = [threading.Thread(target=run, args=(j,)) for j in jobs]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+    finally:
+        m4rm_mod.set_plan_override(0, 0)
+    assert not errors, errors
+    assert L.sg_host_streamed_count() - c0 == 4 * len(jobs)
+
+
 @pytest.mark.parametrize("fname", ["f3", "f5", "f7", "gf4", "f2"])
 def test_extreme_aspect_ratios(fname):
     """Matrix-vector and long-inner-dimension shapes: one tile over 12500 k-blocks (every CTA of
