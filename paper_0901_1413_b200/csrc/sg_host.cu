@@ -2,6 +2,7 @@
 // upload / compute / download / flag streams; the streamed-B pipeline for the shapes that allow
 // it) and sg_m4rm_multi (rows of A and C split over devices, B replicated by peer copies).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -57,6 +58,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
                   int64_t l, int64_t n, int k, int device, int Pr) {
   const PFN_cuStreamWriteValue32_v11070 wv = write_value_fn();
   if (!wv) return SG_EUNSUPPORTED;
+  const auto t_entry = std::chrono::steady_clock::now();
   const int R = planes(field);
   const int64_t wa = w64_of(l), wc = w64_of(n);
   auto rcut = [&](int r) { return m * r / Pr; };
@@ -166,6 +168,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   // waiting for chunk flags that are not queued yet.  Order: A's piece 0, B chunk by chunk (each
   // followed by its flag), A's other pieces.
   if ((rc = upload_a(0)) != SG_OK) return rc;
+  const auto t_first = std::chrono::steady_clock::now();
   for (int j = 0; j < nch; ++j) {
     const int64_t r0 = chunk_lo(j) * 32, rows = std::min<int64_t>(l, chunk_lo(j + 1) * 32) - r0;
     // Each flag goes out on its own stream behind its copy's event.  (Measured on B200: B's
@@ -187,12 +190,17 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   for (int r = 0; r < Pr; ++r)
     if ((rc = product(r, r == 0 ? &sin : nullptr)) != SG_OK) return rc;
   SG_CUDA(cudaMemcpyAsync(d->err_host, err, sizeof(unsigned), cudaMemcpyDeviceToHost, d->comp), "sg_m4rm_host");
+  const auto t_queued = std::chrono::steady_clock::now();
   SG_CUDA(cudaStreamSynchronize(d->out), "sg_m4rm_host sync");
   SG_CUDA(cudaStreamSynchronize(d->comp), "sg_m4rm_host sync");
   SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host sync");
   SG_CUDA(cudaStreamSynchronize(d->flags), "sg_m4rm_host sync");
   if (trace) {
-    fprintf(stderr, "host_streamed trace Pr=%d nch=%d\n", Pr, nch);
+    auto us = [&](std::chrono::steady_clock::time_point t) {
+      return std::chrono::duration<double, std::micro>(t - t_entry).count();
+    };
+    fprintf(stderr, "host_streamed trace Pr=%d nch=%d (host: first copy queued %.1f us, all queued %.1f us, "
+            "synced %.1f us after entry)\n", Pr, nch, us(t_first), us(t_queued), us(std::chrono::steady_clock::now()));
     for (auto& mk : marks) {
       float ms = 0;
       cudaEventElapsedTime(&ms, marks[0].second, mk.second);

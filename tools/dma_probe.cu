@@ -84,6 +84,26 @@ int main() {
              w * rows / 1e6, best, w * rows / best / 1e6);
     }
   }
+  // the host pipeline's shapes: A's row piece (3 planes x 1 MB, pitch 2 MB) and a B chunk
+  // (3 planes x 256 KB, pitch 2 MB), against the same bytes contiguous
+  for (int rep2 = 0; rep2 < 2; ++rep2) {
+    for (size_t width : {(size_t)1 << 20, (size_t)256 << 10}) {
+      float b2d = 1e9, b1d = 1e9;
+      for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0, s1);
+        CK(cudaMemcpy2DAsync(d, width, h, 2 * width, width, 3, cudaMemcpyHostToDevice, s1));
+        cudaEventRecord(e1, s1);
+        CK(cudaMemcpyAsync(d, h, 3 * width, cudaMemcpyHostToDevice, s1));
+        cudaEventRecord(e2, s1);
+        cudaEventSynchronize(e2);
+        float ms, ms1; cudaEventElapsedTime(&ms, e0, e1); cudaEventElapsedTime(&ms1, e1, e2);
+        if (ms < b2d) b2d = ms;
+        if (ms1 < b1d) b1d = ms1;
+      }
+      printf("pipeline shape: 3 x %zu B (pitch %zu): 2-D %.4f ms %.1f GB/s | contiguous %.4f ms %.1f GB/s\n", width,
+             2 * width, b2d, 3 * width / b2d / 1e6, b1d, 3 * width / b1d / 1e6);
+    }
+  }
   // contiguous copies of various sizes (latency + bandwidth)
   for (size_t sz : {(size_t)64 << 10, (size_t)256 << 10, (size_t)1 << 20, (size_t)3 << 20, (size_t)12 << 20}) {
     float best = 1e9;
