@@ -204,6 +204,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
     sa.epoch = sin->epoch;
     sa.first_groups = sin->first_groups;
     sa.nchunks = sin->nchunks;
+    sa.poll_ns = sin->poll_ns;
     sa.perm = perm;
     sa.ngroups = p.nblocks / 4;
     sa.err = sin->err;

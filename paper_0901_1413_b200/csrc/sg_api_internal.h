@@ -85,6 +85,7 @@ struct StreamIn {
   unsigned epoch;
   int first_groups;  // B's chunk j = 4-block groups [g0 (2^j - 1), g0 (2^(j+1) - 1)), g0 = first_groups
   int nchunks;
+  unsigned poll_ns;
   unsigned* err;
 };
 

@@ -182,11 +182,19 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
     SG_CUDA(cudaStreamWaitEvent(d->flags, d->ev_chunk[j], 0), "sg_m4rm_host wait");
     if (wv((CUstream)d->flags, (CUdeviceptr)(d->ready + j), epoch, 0) != CUDA_SUCCESS)
       return fail(SG_ECUDA, "sg_m4rm_host: cuStreamWriteValue32 failed");
-    if (j == 0 || j == nch - 1 || j == nch / 2) mark("in: B chunk " + std::to_string(j) + " up", d->in);
+    mark("in: B chunk " + std::to_string(j) + " up", d->in);
   }
   for (int r = 1; r < Pr; ++r)
     if ((rc = upload_a(r)) != SG_OK) return rc;
-  const StreamIn sin{d->ready, epoch, (int)g0, nch, err};
+  const char* poll_e = getenv("SG_HOST_POLL_NS");  // experiments: flag polling interval
+  const StreamIn sin{d->ready, epoch, (int)g0, nch, poll_e ? (unsigned)atoi(poll_e) : 100u, err};
+  // SG_HOST_STREAM=2 (experiments): the streamed kernel on fully uploaded inputs (its cost
+  // without any waiting, in a warm L2)
+  if (const char* e = getenv("SG_HOST_STREAM"))
+    if (atoi(e) == 2) {
+      SG_CUDA(cudaStreamSynchronize(d->in), "sg_m4rm_host sync");
+      SG_CUDA(cudaStreamSynchronize(d->flags), "sg_m4rm_host sync");
+    }
   for (int r = 0; r < Pr; ++r)
     if ((rc = product(r, r == 0 ? &sin : nullptr)) != SG_OK) return rc;
   SG_CUDA(cudaMemcpyAsync(d->err_host, err, sizeof(unsigned), cudaMemcpyDeviceToHost, d->comp), "sg_m4rm_host");

@@ -81,6 +81,7 @@ struct M4rmStreamArgs : M4rmArgs {
   unsigned epoch;
   int first_groups;
   int nchunks;
+  unsigned poll_ns;  // sleep between two polls of a flag that has not landed
   const int* perm;
   int ngroups;
   unsigned* err;

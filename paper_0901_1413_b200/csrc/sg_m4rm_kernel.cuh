@@ -90,14 +90,15 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // reads of every chunk up to it); then order the TMA (async proxy) reads after it.  A wait longer
 // than 10 s flags an error and gives up instead of hanging the GPU.  (A fence.acq_rel per chunk
 // cost ~1.4 us each: 17 us per 2048-row F5 product even with every flag already set.)
-__device__ __forceinline__ int wait_chunk(const unsigned* ready, int c, int nchunks, unsigned epoch, unsigned* err) {
+__device__ __forceinline__ int wait_chunk(const unsigned* ready, int c, int nchunks, unsigned epoch, unsigned* err,
+                                          unsigned poll_ns) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
   if ((int)(v - epoch) < 0) {
     unsigned long long t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     do {
-      __nanosleep(100);
+      __nanosleep(poll_ns);
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + c) : "memory");
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 10000000000ull) {
@@ -326,7 +327,8 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
           const int rs = real_block(s);
           if constexpr (STRM) {
             if ((rs >> 2) >= ready_groups) {  // chunk c = groups [g0 (2^c - 1), g0 (2^(c+1) - 1))
-              const int c = wait_chunk(a.ready, 31 - __clz((rs >> 2) / a.first_groups + 1), a.nchunks, a.epoch, a.err);
+              const int c = wait_chunk(a.ready, 31 - __clz((rs >> 2) / a.first_groups + 1), a.nchunks, a.epoch, a.err,
+                                       a.poll_ns);
               ready_groups = a.first_groups * ((2 << c) - 1);
             }
           }
