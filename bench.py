@@ -368,6 +368,23 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
         # the host-path result must equal the device path's (outside the timed region)
         extra["verified_vs_device_path"] = bool(torch.equal(sg.m4rm_multiply(A, B).planes.cpu(), Ch))
         extra["streamed_b_calls"] = int(L.sg_host_streamed_count() - s0)
+        # context: this process's plain pinned copy bandwidth right now (PCIe on a shared host varies)
+        Ad = torch.empty_like(Ah, device=device)
+
+        def copy_ms(dst, src):
+            best = 1e9
+            for _ in range(5):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                dst.copy_(src, non_blocking=True)
+                torch.cuda.synchronize()
+                best = min(best, time.perf_counter() - t0)
+            return best
+
+        nb = Ah.numel() * 8
+        extra["pcie_gbs"] = {"h2d": nb / copy_ms(Ad, Ah) / 1e9, "d2h": nb / copy_ms(Ah, Ad) / 1e9,
+                             "note": "one %.1f MB pinned copy each way, best of 5, after the timed loop" % (nb / 1e6)}
+        del Ad
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8), **extra,
             "path": ("sg_m4rm_host (C ABI; pinned host planes; A and C in row pieces, the first piece's product "
