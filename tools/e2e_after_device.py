@@ -51,5 +51,19 @@ for i in range(10):
     sg.m4rm_multiply(A, B, sg.M4rmParams(8), out=C)
 torch.cuda.synchronize()
 print("after device products:", calls(), flush=True)
+with bench.ClockSampler(0):
+    for i in range(10):
+        flush.fill_(i)
+        sg.m4rm_multiply(A, B, sg.M4rmParams(8), out=C)
+    torch.cuda.synchronize()
+print("after device products under the nvidia-smi sampler:", calls(), flush=True)
+sg.m4rm.set_timing(True)
+for i in range(5):
+    flush.fill_(i)
+    sg.m4rm_multiply(A, B, sg.M4rmParams(8), out=C)
+sg.m4rm.set_timing(False)
+print("after set_timing products:", calls(), flush=True)
 peaks = sg.m4rm.probe_peaks(0)
 print("after probe_peaks:", calls(), flush=True)
+time.sleep(2)
+print("after 2 s idle:", calls(), flush=True)
