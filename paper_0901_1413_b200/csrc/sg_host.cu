@@ -162,6 +162,10 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
     mark("out: piece " + std::to_string(r) + " down", d->out);
     return SG_OK;
   };
+  // SG_HOST_DROP_FLAG=j (tests only): never publish chunk j, so the streamed product must give up
+  // after its 10 s wait limit and the call must fail cleanly instead of hanging the GPU
+  const char* drop_e = getenv("SG_HOST_DROP_FLAG");
+  const int drop_flag = drop_e ? atoi(drop_e) : -1;
   int rc;
   // Every upload is queued before the first product: with pageable host buffers a copy call may
   // block the host until the stream's earlier work is done, and piece 0's product must never be
@@ -180,6 +184,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
             "sg_m4rm_host H2D B");
     SG_CUDA(cudaEventRecord(d->ev_chunk[j], cs), "sg_m4rm_host event");
     SG_CUDA(cudaStreamWaitEvent(d->flags, d->ev_chunk[j], 0), "sg_m4rm_host wait");
+    if (j == drop_flag) continue;  // test hook: a chunk that is never published
     if (wv((CUstream)d->flags, (CUdeviceptr)(d->ready + j), epoch, 0) != CUDA_SUCCESS)
       return fail(SG_ECUDA, "sg_m4rm_host: cuStreamWriteValue32 failed");
     mark("in: B chunk " + std::to_string(j) + " up", d->in);

@@ -566,6 +566,31 @@ def test_host_path_thread_safety():
     assert not errors, errors
 
 
+def test_host_streamed_missing_chunk_fails_cleanly():
+    """A B chunk that never lands (SG_HOST_DROP_FLAG test hook): the streamed product's builder
+    warps give up after their 10 s wait limit, sg_m4rm_host reports the chunk, and the next call
+    on the same device works -- the spin-wait can never hang the GPU."""
+    f = sg.F5
+    A = oracle.random_dense("f5", 2048, 1024, 81)
+    B = oracle.random_dense("f5", 1024, 512, 82)
+    want = expect("f5", A, B)
+    Ah = sg.BitslicedMatrix(f, 2048, 1024, sg.BitslicedMatrix.from_planes(
+        f, oracle.pack("f5", A), 1024, device="cpu").planes.pin_memory())
+    Bh = sg.BitslicedMatrix(f, 1024, 512, sg.BitslicedMatrix.from_planes(
+        f, oracle.pack("f5", B), 512, device="cpu").planes.pin_memory())
+    m4rm_mod.set_plan_override(8, -1, 2)
+    try:
+        os.environ["SG_HOST_DROP_FLAG"] = "0"
+        with pytest.raises(_lib.SliceGemmError, match="timed out waiting for B chunk 0"):
+            sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8))
+        os.environ.pop("SG_HOST_DROP_FLAG")
+        C = sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8))
+        assert np.array_equal(C.planes_numpy(), want)
+    finally:
+        os.environ.pop("SG_HOST_DROP_FLAG", None)
+        m4rm_mod.set_plan_override(0, 0)
+
+
 def test_host_streamed_thread_safety():
     """Concurrent streamed-B host products (pinned buffers, the headline's F5 shape class at
     2048 x 1024 x 512) from several threads on one device: each gets its own correct result, and
