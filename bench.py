@@ -548,6 +548,15 @@ def main():
     # e2e last, on fresh inputs of the headline config: the host<->device copies are the part of
     # this run most exposed to the shared host's PCIe, so they go after everything else
     res["e2e"] = e2e_for(head, args, world, rank, device)
+    if world == 1 and not args.no_per_config:
+        # the host-buffer path on the other configs too (5 steps each; informational)
+        class Short:
+            steps, warmup = min(args.steps, 5), 3
+        for i, cfg in enumerate(CONFIGS):
+            if i != args.config and cfg[0] in per_config:
+                e = e2e_for(cfg, Short, world, rank, device)
+                per_config[cfg[0]]["e2e"] = {k: e[k] for k in ("value", "ms_per_step", "verified_vs_device_path",
+                                                               "streamed_b_calls", "pcie_gbs")}
     if world > 1:
         dist.barrier()
     if rank == 0:
