@@ -107,11 +107,22 @@ __device__ __forceinline__ int wait_chunk(const unsigned* ready, int c, int nchu
       }
     } while ((int)(v - epoch) < 0);
   }
+  // the run of landed chunks after c, 4 flags per round with the loads in flight together (one
+  // dependent round trip per flag cost ~0.7 us each, ~5 us per segment start)
   int last = c;
-  for (int j = c + 1; j < nchunks; ++j) {
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + j) : "memory");
-    if ((int)(v - epoch) < 0) break;
-    last = j;
+  for (int j0 = c + 1; j0 < nchunks; j0 += 4) {
+    unsigned f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[i] = epoch - 1u;  // past nchunks: not landed
+      if (j0 + i < nchunks)
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f[i]) : "l"(ready + j0 + i) : "memory");
+    }
+    int run = 0;
+#pragma unroll
+    for (int i = 3; i >= 0; --i) run = (int)(f[i] - epoch) >= 0 ? run + 1 : 0;
+    last = j0 + run - 1;
+    if (run < 4) break;
   }
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + last) : "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");  // ... for the TMA (async proxy) reads too
@@ -798,7 +809,8 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
   if constexpr (SCHED == 2) {
     // warp-specialized: the builder warpgroup hands registers to the two lookup warpgroups,
     // whose row accumulators need them (384 x 168 = 128 x BREGS + 256 x LREGS)
-    constexpr int BREGS = 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
+    // (the streamed-B variant's builders also check chunk flags: 64 registers for them)
+    constexpr int BREGS = STRM ? 64 : 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
     if (threadIdx.x >= NT) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(BREGS));
       run_segments<F, K, RT, SCHED, NT, ABL, 1, STRM>(a, &tmB, smem, mbar);
