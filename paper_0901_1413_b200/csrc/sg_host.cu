@@ -50,9 +50,9 @@ constexpr int MAX_BCHUNKS = 64;
 
 // Streamed variant of the row-piece pipeline (B uploaded whole, A and C in Pr row pieces): the
 // product of piece 0 is launched as soon as A's piece 0 is up and reads B's k-chunks as they
-// land -- the upload stream publishes chunk j by writing the call's epoch to ready[j] right
-// behind the chunk's copy (cuStreamWriteValue32, no SM involved) and the builder warps wait per
-// k-block (M4rmArgs.ready), consuming each tile's k-blocks in arrival order (streamed_order).
+// land -- an event behind chunk j's copy releases, on the flags stream, a cuStreamWriteValue32 of
+// the call's epoch into ready[j] (no SM involved), and the builder warps wait per k-block
+// (M4rmStreamArgs.ready), consuming each tile's k-blocks in arrival order (streamed_order).
 // Later pieces find B complete.  Returns SG_EUNSUPPORTED when the product cannot stream.
 int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
                   int64_t l, int64_t n, int k, int device, int Pr) {
