@@ -809,8 +809,10 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
   if constexpr (SCHED == 2) {
     // warp-specialized: the builder warpgroup hands registers to the two lookup warpgroups,
     // whose row accumulators need them (384 x 168 = 128 x BREGS + 256 x LREGS)
-    // (the streamed-B variant's builders also check chunk flags: 64 registers for them)
-    constexpr int BREGS = STRM ? 64 : 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
+    // (F5: 72 / 216 measured ~1 % faster than 56 / 224 -- its builders' carry-save table adds
+    // need the registers, its lookups fit in 216; F7 and GF(4) lost 1-2 % with the same split.
+    // The streamed-B variant's builders also check chunk flags: at least 64 for them.)
+    constexpr int BREGS = F == F5 ? 72 : STRM ? 64 : 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
     if (threadIdx.x >= NT) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(BREGS));
       run_segments<F, K, RT, SCHED, NT, ABL, 1, STRM>(a, &tmB, smem, mbar);
