@@ -20,8 +20,8 @@ m, l, n = int(m), int(l), int(n)
 dev = torch.device("cuda", 0)
 f, A, B = bench.make_inputs(fld, m, l, n, 0, dev, True)
 C = sg.BitslicedMatrix.zero(f, m, n, device=dev)
-plans = [(0, 0, -1, 0)] + [(rt, sp, pipe, nt) for rt in (1, 2, 4, 8) for nt in (256,) for pipe in (0, 1)
-                           for sp in (1, 4, 8, 16, 32, -1)]
+plans = [(0, 0, -1, 0)] + [(rt, sp, pipe, nt) for rt in (1, 2, 4, 8) for nt in (256,) for pipe in (0, 1, 2)
+                           for sp in (4, 8, 16, 32, -1)]
 for ov in plans:
     M.set_plan_override(*ov)
     try:
