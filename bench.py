@@ -402,6 +402,9 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
         extra["pcie_gbs"] = {"h2d": nb / copy_ms(Ad, Ah) / 1e9, "d2h": nb / copy_ms(Ah, Ad) / 1e9,
                              "note": "one %.1f MB pinned copy each way, best of 5, after the timed loop" % (nb / 1e6)}
         del Ad
+    if world == 1:  # the per-step spread (PCIe on the shared host varies; value is the mean)
+        extra["step_ms_min"] = 1e3 * min(times)
+        extra["step_ms_median"] = 1e3 * statistics.median(times)
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8), **extra,
             "path": ("sg_m4rm_host (C ABI; pinned host planes; A and C in row pieces, the first piece's product "
