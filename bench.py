@@ -484,6 +484,35 @@ def run_reference(args, world, rank):
 
 
 # ----------------------------------------------------------------------------- main
+def relaunch_cmd(gpus, argv, port):
+    """torch.distributed.run command that runs this script with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def relaunch(gpus, argv):
+    """`bench.py --gpus N` without a launcher: re-run under torch.distributed.run (NCCL ranks)."""
+    import socket
+    if not os.environ.get("SG_BENCH_BACKEND"):
+        try:
+            import torch
+            have = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            have = 0
+        if have < gpus:
+            log(f"error: --gpus {gpus} needs {gpus} visible GPUs, this host has {have}")
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr: proof of the NCCL ranks
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    log("bench.py: launching %d ranks: %s" % (gpus, " ".join(relaunch_cmd(gpus, argv, port))))
+    return subprocess.call(relaunch_cmd(gpus, argv, port), env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -494,9 +523,18 @@ def main():
     ap.add_argument("--no-per-config", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     args = ap.parse_args()
+    if args.gpus < 1:
+        log(f"error: --gpus must be >= 1 (got {args.gpus})")
+        sys.exit(2)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not under a launcher: start one rank per GPU ourselves (the same command the driver runs)
+        sys.exit(relaunch(args.gpus, sys.argv[1:]))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"error: --gpus {args.gpus} but WORLD_SIZE={world}: the run would not measure {args.gpus} GPUs")
+        sys.exit(2)
 
     if args.impl == "reference":
         sys.exit(run_reference(args, world, rank))

@@ -21,6 +21,8 @@
  *   sg_m4rm_multi            the same over several GPUs of one process (rows sharded, B
  *                            replicated; the reference's row0/row1 partition)
  *   sg_classical             classical_multiply (__init__.py:16)
+ *   sg_classical_block       classical_f2/f3/f5/f7/z4/z8 (_core_py.py:292-366)
+ *   sg_stream_check          the ValueError of from_dense / to_dense
  *
  * Data layout (identical bits to the reference's BitslicedMatrix planes):
  *   a matrix of `rows` x `n` over a field with R planes is R contiguous planes, each `rows` x
@@ -106,11 +108,19 @@ int sg_abi_version(void);
 const char* sg_last_error(void);
 int sg_field_planes(int field);
 
-/* dense uint8 residues (row stride ld bytes, device) <-> planes (device). */
+/* dense uint8 residues (row stride ld bytes, device) <-> planes (device).  Stream-ordered like
+ * every device entry point: the input check runs inside the kernel and never synchronizes.  An
+ * entry that is not a residue (sg_pack) or an F3 lane holding the illegal pattern 10 (sg_unpack)
+ * is recorded in a per-(device, stream) status word and reported by the next sg_stream_check on
+ * that stream (SG_ERANGE / SG_EPATTERN); the output of such a call is unspecified. */
 int sg_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld, uint64_t* planes,
             void* stream);
 int sg_unpack(int field, const uint64_t* planes, int64_t m, int64_t n, uint8_t* dense, int64_t ld,
               void* stream);
+/* Synchronize `stream` (on the current device) and report, then clear, the input-check status of
+ * the sg_pack / sg_unpack calls queued on it since the last check: SG_OK, SG_ERANGE or
+ * SG_EPATTERN (the reference raises ValueError for both). */
+int sg_stream_check(void* stream);
 /* every lane to its canonical pattern (no-op for F2, F3, GF4) */
 int sg_reduce_canonical(int field, uint64_t* planes, int64_t rows, int64_t n, void* stream);
 /* dst (op)= src, lanewise, in place on dst: `dst` and `src` are arrays of R device pointers,
@@ -147,6 +157,14 @@ int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, 
 int sg_classical(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l,
                  int64_t n, void* stream);
 
+/* classical_<field>(C planes, A planes, B planes) of the reference backend (_core_py.py:292-366):
+ * C (m rows of c_words words) += A (m x l, a_words words per row) * B (l rows of c_words words),
+ * in place with the backend's raw semantics (B's rows in order, zero coefficients skipped, no
+ * canonical reduction), so the bits equal the pure backend's.  Plane pointer arrays as in
+ * sg_plane_op; O(m l n / 32) word operations (a cross-check, not a fast path). */
+int sg_classical_block(int field, uint64_t* const* C, int64_t c_words, const uint64_t* const* A,
+                       int64_t a_words, const uint64_t* const* B, int64_t m, int64_t l, void* stream);
+
 /* Block-granularity plugin mirror.  Plane pointer arrays as in sg_plane_op.  T has the
  * reference table layout: per plane 2^kp rows x words 64-bit words, entry g = the sum of B rows
  * row_base + t over the set bits t of g (B: b_rows rows of `words` words per plane; rows past
@@ -171,10 +189,6 @@ int sg_set_plan_override(int rows_per_thread, int splits, int pipe, int threads)
  * (the NCCL broadcast of B's next row block in dist.sharded_multiply); 0 = all SMs. */
 int sg_set_sm_reserve(int sms);
 int sg_set_timing(int enable);                              /* event-time each internal launch */
-/* performance experiments only: select kernel variants with parts of the work removed
- * (bit 0: table-replica stores, bit 1: field arithmetic, bit 2: lookups); results are WRONG
- * while a nonzero mask is set.  0 restores normal operation. */
-int sg_debug_ablation(int mask);
 int sg_last_timing(double* transpose_ms, double* m4rm_ms, double* reduce_ms);
 int64_t sg_launch_count(void);                              /* kernels launched by this library */
 int64_t sg_host_streamed_count(void);         /* sg_m4rm_host calls whose product streamed B */

@@ -7,8 +7,9 @@ SPEC.md:198-431) over hand-written sm_100a kernels in libslicegemm_b200.so, call
 C ABI in include/slicegemm_b200.h.  There is no CPU fallback.
 """
 
-from .fields import F2, F3, F5, F7, GF4, GF8, Z4, Z8, FIELDS, FieldSpec, by_name
-from .matrix import BitslicedMatrix
+from .fields import F2, F3, F5, F7, GF4, GF8, Z4, Z8, FIELDS, BasisElement, FieldSpec, by_name
+from .matrix import BitslicedMatrix, RowRef, row_accumulate
+from .dense import DenseMatrix
 from .m4rm import M4rmParams, build_table, choose_k, classical_multiply, m4rm_multiply, plan
 from .extension import EXT_FIELDS, F4, F8, F9, F25, F27, ExtFieldSpec, ExtMatrix, ext_multiply, poly_reduce
 from . import _core_cuda
@@ -22,7 +23,7 @@ def backend_name() -> str:
 
 
 __all__ = [
-    "BitslicedMatrix", "ExtFieldSpec", "ExtMatrix", "M4rmParams", "FieldSpec",
+    "BitslicedMatrix", "DenseMatrix", "RowRef", "row_accumulate", "ExtFieldSpec", "ExtMatrix", "M4rmParams", "FieldSpec",
     "F2", "F3", "F4", "F5", "F7", "F8", "F9", "F25", "F27", "GF4", "GF8", "Z4", "Z8", "FIELDS", "EXT_FIELDS",
     "backend_name", "build_table", "by_name", "choose_k", "classical_multiply", "ext_multiply", "m4rm_multiply", "plan", "poly_reduce",
 ]

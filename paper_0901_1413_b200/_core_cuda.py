@@ -89,7 +89,22 @@ def _block(field_code, C, A, col0, kp, T, row0, row1):
     c, cb = _as_dev(C)
     a, _ = _as_dev(A)
     t, _ = _as_dev(T)
-    cw, aw = _shape(c[0])[1], _shape(a[0])[1]
+    (crows, cw), (arows, aw) = _shape(c[0]), _shape(a[0])
+    # the reference block driver indexes numpy arrays and raises IndexError / ValueError on these
+    # (_core_py.py:205-281); here they would be out-of-bounds device accesses, so check first
+    for group, what in ((c, "C"), (a, "A"), (t, "T")):
+        if any(_shape(x) != _shape(group[0]) for x in group):
+            raise ValueError(f"{what} planes differ in shape")
+    row0, row1, col0, kp = int(row0), int(row1), int(col0), int(kp)
+    if not 0 <= row0 <= row1 <= crows or row1 > arows:
+        raise IndexError(f"rows [{row0}, {row1}) outside C ({crows} rows) or A ({arows} rows)")
+    if kp < 0 or col0 < 0 or col0 + kp > 64 * aw:
+        raise IndexError(f"block columns [{col0}, {col0 + kp}) outside A ({64 * aw} columns)")
+    trows, tw = _shape(t[0])
+    if row1 > row0 and kp > 0 and trows < (1 << kp):
+        raise IndexError(f"table has {trows} entries, block needs {1 << kp}")
+    if tw != cw:
+        raise ValueError(f"table rows have {tw} words, C rows {cw}")
     cp, _k1 = _lib.ptr_array([x.data_ptr() for x in c])
     ap, _k2 = _lib.ptr_array([x.data_ptr() for x in a])
     tp, _k3 = _lib.ptr_array([x.data_ptr() for x in t])
@@ -129,3 +144,58 @@ def m4rm_block_z4(C0, C1, A0, A1, col0, kp, T0, T1, row0, row1):
 
 def m4rm_block_z8(C0, C1, C2, A0, A1, A2, col0, kp, T0, T1, T2, row0, row1):
     _block(_lib.SG_Z8, [C0, C1, C2], [A0, A1, A2], col0, kp, [T0, T1, T2], row0, row1)
+
+
+# ---------------------------------------------------------------- classical drivers
+def _classical(field_code, C, A, B):
+    """C += A B in place with the pure backend's raw row-accumulate semantics (_core_py.py:292-366)."""
+    c, cb = _as_dev(C)
+    a, _ = _as_dev(A)
+    b, _ = _as_dev(B)
+    (m, cw), (arows, aw), (l, bw) = _shape(c[0]), _shape(a[0]), _shape(b[0])
+    for group, what in ((c, "C"), (a, "A"), (b, "B")):
+        if any(_shape(x) != _shape(group[0]) for x in group):
+            raise ValueError(f"{what} planes differ in shape")
+    if arows != m:
+        raise ValueError(f"A has {arows} rows, C {m}")
+    if bw != cw:
+        raise ValueError(f"B rows have {bw} words, C rows {cw}")
+    if l > 64 * aw:
+        raise IndexError(f"B has {l} rows but A only {64 * aw} columns")
+    cp, _k1 = _lib.ptr_array([x.data_ptr() for x in c])
+    ap, _k2 = _lib.ptr_array([x.data_ptr() for x in a])
+    bp, _k3 = _lib.ptr_array([x.data_ptr() for x in b])
+    with torch.cuda.device(c[0].device):
+        _lib.check(_lib.load().sg_classical_block(field_code, cp, cw, ap, aw, bp, m, l,
+                                                  _lib.current_stream_handle(c[0].device)))
+    _write_back(c, cb)
+
+
+def classical_f2(C0, A0, B0):
+    _classical(_lib.SG_F2, [C0], [A0], [B0])
+
+
+def classical_f3(C0, C1, A0, A1, B0, B1):
+    _classical(_lib.SG_F3, [C0, C1], [A0, A1], [B0, B1])
+
+
+def classical_z4(C0, C1, A0, A1, B0, B1):
+    _classical(_lib.SG_Z4, [C0, C1], [A0, A1], [B0, B1])
+
+
+def classical_f5(C0, C1, C2, A0, A1, A2, B0, B1, B2):
+    _classical(_lib.SG_F5, [C0, C1, C2], [A0, A1, A2], [B0, B1, B2])
+
+
+def classical_f7(C0, C1, C2, A0, A1, A2, B0, B1, B2):
+    _classical(_lib.SG_F7, [C0, C1, C2], [A0, A1, A2], [B0, B1, B2])
+
+
+def classical_z8(C0, C1, C2, A0, A1, A2, B0, B1, B2):
+    _classical(_lib.SG_Z8, [C0, C1, C2], [A0, A1, A2], [B0, B1, B2])
+
+
+# Names of the pure backend (_core_py.py) this module deliberately does not provide: the
+# packed-integer baselines (_core_py.py:372-380) and the program-search engine
+# (_core_py.py:381-661) are outside the M4RM hot path (SURVEY.md 2, DESIGN.md 7).
+OUT_OF_SCOPE = ("packed_z4_add", "packed_f3_add", "run_exhaustive", "run_staged")

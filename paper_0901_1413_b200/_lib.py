@@ -30,10 +30,10 @@ OPS = {
 
 # every symbol include/slicegemm_b200.h declares
 EXPORTS = (
-    "sg_abi_version", "sg_last_error", "sg_field_planes", "sg_pack", "sg_unpack",
+    "sg_abi_version", "sg_last_error", "sg_field_planes", "sg_pack", "sg_unpack", "sg_stream_check",
     "sg_reduce_canonical", "sg_plane_op", "sg_m4rm_workspace_bytes", "sg_m4rm", "sg_m4rm_host", "sg_m4rm_multi",
     "sg_build_table", "sg_m4rm_block", "sg_plan", "sg_set_plan_override", "sg_set_sm_reserve", "sg_set_timing",
-    "sg_last_timing", "sg_launch_count", "sg_host_streamed_count", "sg_kernel_info", "sg_probe_peaks", "sg_debug_ablation", "sg_classical",
+    "sg_last_timing", "sg_launch_count", "sg_host_streamed_count", "sg_kernel_info", "sg_probe_peaks", "sg_classical", "sg_classical_block",
 )
 
 _lib = None
@@ -64,6 +64,7 @@ def load():
         "sg_field_planes": ([i32], i32),
         "sg_pack": ([i32, vp, i64, i64, i64, vp, vp], i32),
         "sg_unpack": ([i32, vp, i64, i64, vp, i64, vp], i32),
+        "sg_stream_check": ([vp], i32),
         "sg_reduce_canonical": ([i32, vp, i64, i64, vp], i32),
         "sg_plane_op": ([i32, pp, pp, i64, i64, u64, i32, vp], i32),
         "sg_m4rm_workspace_bytes": ([i32, i64, i64, i64, i32], i64),
@@ -81,8 +82,8 @@ def load():
         "sg_host_streamed_count": ([], i64),
         "sg_kernel_info": ([i32, i32, ip, ip, ip, ip, ip, ip, ip, ip], i32),
         "sg_probe_peaks": ([i32, dp, dp, dp], i32),
-        "sg_debug_ablation": ([i32], i32),
         "sg_classical": ([i32, vp, vp, vp, i64, i64, i64, vp], i32),
+        "sg_classical_block": ([i32, pp, i64, pp, i64, pp, i64, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name, None)

@@ -68,13 +68,32 @@ DevState& dev_state(int device) {
 
 // Workspace cache keyed by (device, stream): stream-ordered reuse is safe, cross-stream is not.
 std::map<std::pair<int, cudaStream_t>, Buf> g_ws;
-std::map<int, int*> g_flags;  // per-device error flag for pack / unpack
+// Input-check status of sg_pack / sg_unpack, per (device, stream): a word of mapped page-locked
+// host memory that the kernels OR their error bits into (1: entry out of range, 2: illegal F3
+// pattern) -- only when they find bad input, so the check costs nothing on good input and
+// nothing waits for it.  sg_stream_check synchronizes the stream and reads and clears it.
+std::mutex g_flag_mu;  // never held across a synchronization
+std::map<std::pair<int, cudaStream_t>, StatusFlag> g_flags;
 
-int* flag_for(int device, cudaError_t* err) {
-  int*& f = g_flags[device];
+StatusFlag* flag_for(int device, cudaStream_t st, cudaError_t* err) {
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  StatusFlag& f = g_flags[{device, st}];
   *err = cudaSuccess;
-  if (!f) *err = cudaMalloc(&f, 16);
-  return *err == cudaSuccess ? f : nullptr;
+  if (!f.host) {
+    *err = cudaHostAlloc((void**)&f.host, sizeof(int), cudaHostAllocMapped);
+    if (*err != cudaSuccess) {
+      f.host = nullptr;
+      return nullptr;
+    }
+    *f.host = 0;
+    *err = cudaHostGetDevicePointer((void**)&f.dev, f.host, 0);
+    if (*err != cudaSuccess) {
+      cudaFreeHost(f.host);
+      f.host = nullptr;
+      return nullptr;
+    }
+  }
+  return &f;
 }
 
 void* workspace_for(int device, cudaStream_t st, size_t bytes, cudaError_t* err) {
@@ -292,11 +311,16 @@ int sg_set_sm_reserve(int sms) {
   return SG_OK;
 }
 
-int sg_debug_ablation(int mask) {
+#ifdef SG_EXPERIMENTS
+// performance experiments only (tools/ablate.py, `make EXTRA=-DSG_EXPERIMENTS`): select kernel
+// variants with parts of the work removed; every product is WRONG while a nonzero mask is set.
+// Not declared in include/slicegemm_b200.h and not compiled into the production library.
+extern "C" int sg_debug_ablation(int mask) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_ablation = mask;
   return SG_OK;
 }
+#endif
 
 int sg_set_timing(int enable) {
   g_timing = enable != 0;
@@ -317,20 +341,14 @@ int sg_pack(int field, const uint8_t* dense, int64_t m, int64_t n, int64_t ld, u
   if (m == 0 || n == 0) return SG_OK;
   if (!dense || !planes_out) return fail(SG_EINVAL, "null pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
-  cudaGetDevice(&dev);
+  SG_CUDA(cudaGetDevice(&dev), "sg_pack");
   cudaError_t e;
-  int* flag = flag_for(dev, &e);
-  if (!flag) return cuda_fail(e, "sg_pack flag");
-  SG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st), "sg_pack");
-  SG_CUDA(launch_pack(field, dense, m, n, ld, planes_out, flag, st), "sg_pack launch");
+  StatusFlag* flag = flag_for(dev, st, &e);
+  if (!flag) return cuda_fail(e, "sg_pack status flag");
+  SG_CUDA(launch_pack(field, dense, m, n, ld, planes_out, flag->dev, st), "sg_pack launch");
   g_launches++;
-  int h = 0;
-  SG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "sg_pack");
-  SG_CUDA(cudaStreamSynchronize(st), "sg_pack");
-  if (h) return fail(SG_ERANGE, "entries out of range for the field");
-  return SG_OK;
+  return SG_OK;  // an out-of-range entry is reported by sg_stream_check
 }
 
 int sg_unpack(int field, const uint64_t* planes_in, int64_t m, int64_t n, uint8_t* dense, int64_t ld,
@@ -340,19 +358,32 @@ int sg_unpack(int field, const uint64_t* planes_in, int64_t m, int64_t n, uint8_
   if (m == 0 || n == 0) return SG_OK;
   if (!dense || !planes_in) return fail(SG_EINVAL, "null pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
-  cudaGetDevice(&dev);
+  SG_CUDA(cudaGetDevice(&dev), "sg_unpack");
   cudaError_t e;
-  int* flag = flag_for(dev, &e);
-  if (!flag) return cuda_fail(e, "sg_unpack flag");
-  SG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st), "sg_unpack");
-  SG_CUDA(launch_unpack(field, planes_in, m, n, dense, ld, flag, st), "sg_unpack launch");
+  StatusFlag* flag = flag_for(dev, st, &e);
+  if (!flag) return cuda_fail(e, "sg_unpack status flag");
+  SG_CUDA(launch_unpack(field, planes_in, m, n, dense, ld, flag->dev, st), "sg_unpack launch");
   g_launches++;
-  int h = 0;
-  SG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "sg_unpack");
-  SG_CUDA(cudaStreamSynchronize(st), "sg_unpack");
-  if (h) return fail(SG_EPATTERN, "illegal F3 pattern (sign without unit) in planes");
+  return SG_OK;  // an illegal F3 pattern is reported by sg_stream_check
+}
+
+int sg_stream_check(void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  SG_CUDA(cudaGetDevice(&dev), "sg_stream_check");
+  SG_CUDA(cudaStreamSynchronize(st), "sg_stream_check");
+  int bits = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    auto it = g_flags.find({dev, st});
+    if (it != g_flags.end() && it->second.host) {
+      bits = *(volatile int*)it->second.host;
+      *(volatile int*)it->second.host = 0;
+    }
+  }
+  if (bits & 1) return fail(SG_ERANGE, "sg_pack: entries out of range for the field");
+  if (bits & 2) return fail(SG_EPATTERN, "sg_unpack: illegal F3 pattern (sign without unit) in planes");
   return SG_OK;
 }
 
@@ -492,6 +523,21 @@ int sg_classical(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
     c.p[d] = d < R ? C + d * m * wb : nullptr;
   }
   SG_CUDA(launch_classical(field, a, wa, b, wb, c, m, l, (cudaStream_t)stream), "sg_classical");
+  g_launches++;
+  return SG_OK;
+}
+
+int sg_classical_block(int field, uint64_t* const* C, int64_t c_words, const uint64_t* const* A, int64_t a_words,
+                       const uint64_t* const* B, int64_t m, int64_t l, void* stream) {
+  if (!valid_field(field)) return fail(SG_EINVAL, "unknown field code");
+  if (m < 0 || l < 0 || c_words < 0 || a_words < 0) return fail(SG_EINVAL, "negative dimension");
+  if (l > a_words * 64) return fail(SG_EINVAL, "A has fewer columns than B has rows");
+  if (m == 0 || l == 0 || c_words == 0) return SG_OK;
+  Planes c, a, b;
+  const int R = planes(field);
+  if (!fill_planes(&c, (const uint64_t* const*)C, R) || !fill_planes(&a, A, R) || !fill_planes(&b, B, R))
+    return fail(SG_EINVAL, "null plane pointer");
+  SG_CUDA(launch_classical_block(field, c, c_words, a, a_words, b, m, l, (cudaStream_t)stream), "sg_classical_block");
   g_launches++;
   return SG_OK;
 }

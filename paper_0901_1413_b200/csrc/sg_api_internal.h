@@ -51,7 +51,11 @@ struct Buf {
   size_t bytes = 0;
 };
 
-int* flag_for(int device, cudaError_t* err);
+struct StatusFlag {
+  int* host = nullptr;  // mapped page-locked word (sg_stream_check reads it)
+  int* dev = nullptr;   // its device alias (the kernels write it)
+};
+StatusFlag* flag_for(int device, cudaStream_t st, cudaError_t* err);
 void* workspace_for(int device, cudaStream_t st, size_t bytes, cudaError_t* err);
 int check_mul_args(int field, const void* A, const void* B, const void* C, int64_t m, int64_t l, int64_t n, int k);
 

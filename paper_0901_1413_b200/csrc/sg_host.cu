@@ -31,7 +31,16 @@ struct Io {
   cudaStream_t flags = nullptr;  // writes the chunk flags behind the copies' events
   cudaEvent_t ev_chunk[64];
   std::map<int, bool> preloaded;  // fields whose auxiliary kernels are loaded
+  int stream_ops = 0;  // cuStreamWriteValue32 on this device: 0 untested, 1 works, -1 unsupported
 };
+
+// After a failed call, wait for every copy already queued on the device's pipeline streams: the
+// caller may free or reuse its host buffers as soon as the call returns.
+void drain(Io* d) {
+  for (cudaStream_t s : {d->in, d->flags, d->comp, d->out})
+    if (s) cudaStreamSynchronize(s);
+  cudaGetLastError();
+}
 std::map<int, Io> io_state;
 
 PFN_cuStreamWriteValue32_v11070 write_value_fn() {
@@ -57,7 +66,7 @@ constexpr int MAX_BCHUNKS = 64;
 int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m,
                   int64_t l, int64_t n, int k, int device, int Pr) {
   const PFN_cuStreamWriteValue32_v11070 wv = write_value_fn();
-  if (!wv) return SG_EUNSUPPORTED;
+  if (!wv || d->stream_ops < 0) return SG_EUNSUPPORTED;
   const auto t_entry = std::chrono::steady_clock::now();
   const int R = planes(field);
   const int64_t wa = w64_of(l), wc = w64_of(n);
@@ -89,12 +98,17 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
       SG_CUDA(cudaMalloc(&d->ready, (MAX_BCHUNKS + 1) * sizeof(unsigned)), "sg_m4rm_host flags");
       SG_CUDA(cudaMemset(d->ready, 0, (MAX_BCHUNKS + 1) * sizeof(unsigned)), "sg_m4rm_host flags");
       SG_CUDA(cudaMallocHost(&d->err_host, sizeof(unsigned)), "sg_m4rm_host flags");
-      // first use of the stream memory operations while nothing waits on them
-      if (wv((CUstream)d->flags, (CUdeviceptr)(d->ready + MAX_BCHUNKS), 0u, 0) != CUDA_SUCCESS) {
+    }
+    if (d->stream_ops == 0) {
+      // first use of the stream memory operations while nothing waits on them; the outcome is
+      // kept, so a device without them falls back on every call, not just the first
+      if (wv((CUstream)d->flags, (CUdeviceptr)(d->ready + MAX_BCHUNKS), 0u, 0) != CUDA_SUCCESS ||
+          cudaStreamSynchronize(d->flags) != cudaSuccess) {
         cudaGetLastError();
+        d->stream_ops = -1;
         return SG_EUNSUPPORTED;
       }
-      SG_CUDA(cudaStreamSynchronize(d->flags), "sg_m4rm_host flags");
+      d->stream_ops = 1;
     }
   }
   unsigned* err = d->ready + MAX_BCHUNKS;
@@ -286,6 +300,8 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
     d = &io_state[device];  // std::map nodes are stable: d stays valid
   }
   std::lock_guard<std::mutex> busy(d->busy);  // held to the end of the call (after the final syncs)
+  // the pipeline proper; on failure, the copies it already queued are waited for before returning
+  auto pipeline = [&]() -> int {
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   // device layout: B chunks | A chunks (last one as row pieces) | chunk partials | last-chunk
   // pieces | C
@@ -514,6 +530,10 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
     cudaEventDestroy(t0);
   }
   return SG_OK;
+  };
+  rc = pipeline();
+  if (rc != SG_OK) drain(d);
+  return rc;
 }
 
 int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, int64_t m, int64_t l, int64_t n,
@@ -530,16 +550,23 @@ int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, 
   cudaGetDevice(&cur);
   const int R = planes(field);
   const int64_t wa = w64_of(l), wc = w64_of(n);
-  const size_t b_bytes = (size_t)R * l * wc * 8;
+  const size_t a_bytes = (size_t)R * m * wa * 8, b_bytes = (size_t)R * l * wc * 8, c_bytes = (size_t)R * m * wc * 8;
+  // B travels in NBC row chunks (whole 64-bit words of rows) so the tree's hops pipeline
+  constexpr int NBC = 8;
   struct Dev {
-    cudaStream_t st = nullptr;
-    cudaEvent_t ev = nullptr;
+    cudaStream_t st = nullptr;   // A up, products, C down
+    cudaStream_t cst = nullptr;  // B chunks arriving on this device (H2D or peer copy)
+    cudaEvent_t ev_b[NBC];       // chunk c of B is on this device
+    cudaEvent_t ev_all = nullptr;
     Buf buf;
   };
   static std::map<int, Dev> state;
   static std::mutex multi_mu;
   std::lock_guard<std::mutex> busy(multi_mu);  // one multi-device product at a time
-  // per distinct device: B, then the A and C slabs of every shard it runs
+  // distinct devices in order of first appearance; devices[0] receives B from the host
+  std::vector<int> uniq;
+  for (int g = 0; g < ngpus; ++g)
+    if (std::find(uniq.begin(), uniq.end(), devices[g]) == uniq.end()) uniq.push_back(devices[g]);
   std::map<int, size_t> need;
   std::vector<int64_t> r0(ngpus), r1(ngpus);
   for (int g = 0; g < ngpus; ++g) {
@@ -547,49 +574,120 @@ int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, 
     r1[g] = m * (g + 1) / ngpus;
     need[devices[g]] += ((size_t)R * (r1[g] - r0[g]) * (wa + wc) * 8 + 2 * 256);
   }
-  for (auto& kv : need) {
-    kv.second += b_bytes + 256;
-    Dev& d = state[kv.first];
-    SG_CUDA(cudaSetDevice(kv.first), "sg_m4rm_multi set device");
+  for (int dv : uniq) {
+    size_t& bytes = need[dv];
+    bytes += b_bytes + 256;
+    Dev& d = state[dv];
+    SG_CUDA(cudaSetDevice(dv), "sg_m4rm_multi set device");
     if (!d.st) {
       SG_CUDA(cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking), "sg_m4rm_multi stream");
-      SG_CUDA(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming), "sg_m4rm_multi event");
+      SG_CUDA(cudaStreamCreateWithFlags(&d.cst, cudaStreamNonBlocking), "sg_m4rm_multi stream");
+      for (int c = 0; c < NBC; ++c)
+        SG_CUDA(cudaEventCreateWithFlags(&d.ev_b[c], cudaEventDisableTiming), "sg_m4rm_multi event");
+      SG_CUDA(cudaEventCreateWithFlags(&d.ev_all, cudaEventDisableTiming), "sg_m4rm_multi event");
     }
-    if (d.buf.bytes < kv.second) {
+    if (d.buf.bytes < bytes) {
       if (d.buf.p) {
         cudaDeviceSynchronize();
         cudaFree(d.buf.p);
       }
       d.buf.p = nullptr;
       d.buf.bytes = 0;
-      SG_CUDA(cudaMalloc(&d.buf.p, kv.second), "sg_m4rm_multi alloc");
-      d.buf.bytes = kv.second;
+      SG_CUDA(cudaMalloc(&d.buf.p, bytes), "sg_m4rm_multi alloc");
+      d.buf.bytes = bytes;
     }
   }
+  // Host buffers: page-locked for the duration of the call unless they already are, so every
+  // copy is asynchronous and the devices run concurrently (a copy from or to pageable memory
+  // would make the host wait for each device in turn).
+  std::vector<void*> registered;
+  auto pin = [&](const void* p, size_t bytes) -> int {
+    if (!bytes) return SG_OK;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost) return SG_OK;
+    cudaGetLastError();
+    const cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterPortable);
+    if (e == cudaSuccess) registered.push_back(const_cast<void*>(p));
+    else cudaGetLastError();  // e.g. already registered by the caller: the copies still work
+    return SG_OK;
+  };
+  auto finish = [&](int code) {
+    for (int dv : uniq) {  // never return while a queued copy may still touch the caller's buffers
+      cudaSetDevice(dv);
+      cudaStreamSynchronize(state[dv].cst);
+      cudaStreamSynchronize(state[dv].st);
+    }
+    for (void* p : registered) cudaHostUnregister(p);
+    cudaGetLastError();
+    cudaSetDevice(cur);
+    return code;
+  };
+  pin(A, a_bytes);
+  pin(B, b_bytes);
+  pin(C, c_bytes);
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  // B: host -> devices[0], then peer copies to every other device (one hop each over NVSwitch)
-  const int d0 = devices[0];
-  uint64_t* B0 = (uint64_t*)state[d0].buf.p;
-  SG_CUDA(cudaSetDevice(d0), "sg_m4rm_multi set device");
-  if (b_bytes) SG_CUDA(cudaMemcpyAsync(B0, B, b_bytes, cudaMemcpyHostToDevice, state[d0].st), "sg_m4rm_multi H2D B");
-  SG_CUDA(cudaEventRecord(state[d0].ev, state[d0].st), "sg_m4rm_multi event");
-  for (auto& kv : need) {
-    if (kv.first == d0 || !b_bytes) continue;
-    Dev& d = state[kv.first];
-    SG_CUDA(cudaSetDevice(kv.first), "sg_m4rm_multi set device");
+  // B: host -> uniq[0] in NBC row chunks, then a doubling tree of peer copies over NVLink /
+  // NVSwitch -- in round t, device i < 2^t sends to device i + 2^t -- pipelined by chunk: chunk
+  // c's hop to device j waits only for chunk c on its sender (ev_b), so hops of different chunks
+  // and rounds overlap.  Every device receives B once, ceil(log2 G) hops deep, instead of G-1
+  // copies leaving one device.
+  const int G = (int)uniq.size();
+  const int64_t bw = wc;  // words per B row
+  auto brow = [&](int c) { return std::min<int64_t>(l, ((wa * c / NBC) * 64)); };  // chunk c = rows [brow(c), brow(c+1))
+  auto copy_chunk = [&](int dst, int src, int c) -> int {
+    const int64_t q0 = c == 0 ? 0 : brow(c), q1 = c == NBC - 1 ? l : brow(c + 1);
+    Dev& d = state[uniq[dst]];
+    SG_CUDA(cudaSetDevice(uniq[dst]), "sg_m4rm_multi set device");
+    if (q1 > q0) {
+      // R planes, rows [q0, q1) of each: one 2-D copy (pitch = a plane's bytes)
+      char* dbase = (char*)d.buf.p;
+      if (src < 0) {
+        SG_CUDA(cudaMemcpy2DAsync(dbase + q0 * bw * 8, l * bw * 8, (const char*)B + q0 * bw * 8, l * bw * 8,
+                                  (q1 - q0) * bw * 8, R, cudaMemcpyHostToDevice, d.cst),
+                "sg_m4rm_multi H2D B");
+      } else {
+        Dev& s = state[uniq[src]];
+        SG_CUDA(cudaStreamWaitEvent(d.cst, s.ev_b[c], 0), "sg_m4rm_multi wait");
+        for (int p = 0; p < R; ++p)
+          SG_CUDA(cudaMemcpyPeerAsync(dbase + ((int64_t)p * l + q0) * bw * 8, uniq[dst],
+                                      (char*)s.buf.p + ((int64_t)p * l + q0) * bw * 8, uniq[src],
+                                      (q1 - q0) * bw * 8, d.cst),
+                  "sg_m4rm_multi peer copy B");
+      }
+    }
+    SG_CUDA(cudaEventRecord(d.ev_b[c], d.cst), "sg_m4rm_multi event");
+    return SG_OK;
+  };
+  for (int i = 1; i < G; ++i) {  // peer access for every tree edge (sender (i - 2^t) -> i)
+    int hb = 1;
+    while (hb * 2 <= i) hb *= 2;
+    const int from = uniq[i - hb];
+    SG_CUDA(cudaSetDevice(uniq[i]), "sg_m4rm_multi set device");
     int can = 0;
-    cudaDeviceCanAccessPeer(&can, kv.first, d0);
+    cudaDeviceCanAccessPeer(&can, uniq[i], from);
     if (can) {
-      const cudaError_t e = cudaDeviceEnablePeerAccess(d0, 0);
-      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "sg_m4rm_multi peer access");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(from, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return finish(cuda_fail(e, "sg_m4rm_multi peer access"));
       cudaGetLastError();
     }
-    SG_CUDA(cudaStreamWaitEvent(d.st, state[d0].ev, 0), "sg_m4rm_multi wait");
-    SG_CUDA(cudaMemcpyPeerAsync(d.buf.p, kv.first, B0, d0, b_bytes, d.st), "sg_m4rm_multi peer copy B");
   }
-  // shards: A rows up, multiply, C rows down (each device's stream; shards on one device in order)
+  if (b_bytes) {
+    for (int c = 0; c < NBC; ++c) {
+      if ((rc = copy_chunk(0, -1, c)) != SG_OK) return finish(rc);
+      for (int span = 1; span < G; span *= 2)  // chunk c down the tree, round by round
+        for (int i = 0; i < span && i + span < G; ++i)
+          if ((rc = copy_chunk(i + span, i, c)) != SG_OK) return finish(rc);
+    }
+  }
+  for (int dv : uniq) {
+    Dev& d = state[dv];
+    SG_CUDA(cudaSetDevice(dv), "sg_m4rm_multi set device");
+    SG_CUDA(cudaEventRecord(d.ev_all, d.cst), "sg_m4rm_multi event");
+  }
+  // every shard's A upload and product first (all devices busy), the C downloads after
   std::map<int, size_t> offset;
-  for (auto& kv : need) offset[kv.first] = up(b_bytes);
+  for (int dv : uniq) offset[dv] = up(b_bytes);
+  std::vector<uint64_t*> dCs(ngpus, nullptr);
   for (int g = 0; g < ngpus; ++g) {
     const int dv = devices[g];
     Dev& d = state[dv];
@@ -600,27 +698,30 @@ int sg_m4rm_multi(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, 
     uint64_t* dB = (uint64_t*)base;
     uint64_t* dA = (uint64_t*)(base + offset[dv]);
     offset[dv] += up((size_t)R * rows * wa * 8);
-    uint64_t* dC = (uint64_t*)(base + offset[dv]);
+    dCs[g] = (uint64_t*)(base + offset[dv]);
     offset[dv] += up((size_t)R * rows * wc * 8);
     if (wa)
       SG_CUDA(cudaMemcpy2DAsync(dA, rows * wa * 8, A + r0[g] * wa, m * wa * 8, rows * wa * 8, R,
                                 cudaMemcpyHostToDevice, d.st),
               "sg_m4rm_multi H2D A");
-    rc = sg_m4rm(field, dA, dB, dC, rows, l, n, k, nullptr, 0, d.st);
-    if (rc != SG_OK) {
-      cudaSetDevice(cur);
-      return rc;
-    }
-    SG_CUDA(cudaMemcpy2DAsync(C + r0[g] * wc, m * wc * 8, dC, rows * wc * 8, rows * wc * 8, R,
-                              cudaMemcpyDeviceToHost, d.st),
+    SG_CUDA(cudaStreamWaitEvent(d.st, d.ev_all, 0), "sg_m4rm_multi wait");  // all of B is here
+    rc = sg_m4rm(field, dA, dB, dCs[g], rows, l, n, k, nullptr, 0, d.st);
+    if (rc != SG_OK) return finish(rc);
+  }
+  for (int g = 0; g < ngpus; ++g) {
+    if (!dCs[g]) continue;
+    const int64_t rows = r1[g] - r0[g];
+    SG_CUDA(cudaSetDevice(devices[g]), "sg_m4rm_multi set device");
+    SG_CUDA(cudaMemcpy2DAsync(C + r0[g] * wc, m * wc * 8, dCs[g], rows * wc * 8, rows * wc * 8, R,
+                              cudaMemcpyDeviceToHost, state[devices[g]].st),
             "sg_m4rm_multi D2H C");
   }
-  for (auto& kv : need) {
-    SG_CUDA(cudaSetDevice(kv.first), "sg_m4rm_multi set device");
-    SG_CUDA(cudaStreamSynchronize(state[kv.first].st), "sg_m4rm_multi sync");
+  for (int dv : uniq) {
+    SG_CUDA(cudaSetDevice(dv), "sg_m4rm_multi set device");
+    const cudaError_t e = cudaStreamSynchronize(state[dv].st);
+    if (e != cudaSuccess) return finish(cuda_fail(e, "sg_m4rm_multi sync"));
   }
-  cudaSetDevice(cur);
-  return SG_OK;
+  return finish(SG_OK);
 }
 
 }  // extern "C"

@@ -151,6 +151,8 @@ cudaError_t launch_build_table(int field, Planes B, int64_t b_rows, int64_t row_
                                Planes T, cudaStream_t st);
 cudaError_t launch_classical(int field, Planes A, int64_t wa64, Planes B, int64_t wb64, Planes C, int64_t m,
                              int64_t l, cudaStream_t st);
+cudaError_t launch_classical_block(int field, Planes C, int64_t wc64, Planes A, int64_t wa64, Planes B, int64_t m,
+                                   int64_t l, cudaStream_t st);
 
 // sg_peaks.cu
 int probe_peaks(int device, double* lop3_per_clk_sm, double* lds_bytes_per_clk_sm, double* sm_mhz);

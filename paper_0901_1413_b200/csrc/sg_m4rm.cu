@@ -16,26 +16,29 @@ __global__ void transpose_a_kernel(const u32* __restrict__ A, u32* __restrict__ 
   __shared__ u32 tile[32][33];
   pdl_trigger();
   const int d = blockIdx.z;
-  const int64_t rbase = (int64_t)blockIdx.y * 32;
   const int wbase = blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  // row tiles blockIdx.y, blockIdx.y + gridDim.y, ... (grid.y is capped at 65535)
+  for (int64_t rbase = (int64_t)blockIdx.y * 32; rbase < mpad; rbase += (int64_t)gridDim.y * 32) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t row = rbase + ty + 8 * i;
-    const int w = wbase + tx;
-    u32 v = 0;
-    if (row < m && w < wa32) {
-      v = A[((int64_t)d * m + row) * wa32 + w];
-      if (f3 && d == 0) v ^= A[(m + row) * wa32 + w];
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = rbase + ty + 8 * i;
+      const int w = wbase + tx;
+      u32 v = 0;
+      if (row < m && w < wa32) {
+        v = A[((int64_t)d * m + row) * wa32 + w];
+        if (f3 && d == 0) v ^= A[(m + row) * wa32 + w];
+      }
+      tile[ty + 8 * i][tx] = v;
     }
-    tile[ty + 8 * i][tx] = v;
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int w = wbase + ty + 8 * i;
-    const int64_t row = rbase + tx;
-    if (w < wa32 && row < mpad) AT[((int64_t)d * wa32 + w) * mpad + row] = tile[tx][ty + 8 * i];
+    for (int i = 0; i < 4; ++i) {
+      const int w = wbase + ty + 8 * i;
+      const int64_t row = rbase + tx;
+      if (w < wa32 && row < mpad) AT[((int64_t)d * wa32 + w) * mpad + row] = tile[tx][ty + 8 * i];
+    }
+    __syncthreads();
   }
 }
 
@@ -51,40 +54,43 @@ __global__ void index_words_kernel(const u32* __restrict__ A, u32* __restrict__ 
   constexpr int NIP = NI == 3 ? 4 : NI, RPW = 4 / NIP;
   __shared__ u32 tile[R][32][33];
   pdl_trigger();  // the product kernel may launch now; it waits for this grid before reading IW
-  const int64_t rbase = (int64_t)blockIdx.y * 32;
   const int wbase = blockIdx.x * 32;  // A words wbase.. (= k-blocks 4*wbase ..)
   const int tx = threadIdx.x, ty = threadIdx.y;
+  // row tiles blockIdx.y, blockIdx.y + gridDim.y, ... (grid.y is capped at 65535)
+  for (int64_t rbase = (int64_t)blockIdx.y * 32; rbase < mpad; rbase += (int64_t)gridDim.y * 32) {
 #pragma unroll
-  for (int d = 0; d < R; ++d)
+    for (int d = 0; d < R; ++d)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t row = rbase + ty + 8 * i;
-      const int w = wbase + tx;
-      tile[d][ty + 8 * i][tx] = (row < m && w < wa32) ? A[((int64_t)d * m + row) * wa32 + w] : 0u;
-    }
-  __syncthreads();
-  // 128 k-blocks per tile -> 128 / RPW output words
-  for (int q = ty; q < 128 / RPW; q += 8) {
-    const int oq = (wbase * 4) / RPW + q;
-    const int64_t row = rbase + tx;
-    if (oq >= nwords || row >= mpad) continue;
-    u32 v = 0;
-#pragma unroll
-    for (int b = 0; b < RPW; ++b) {
-      const int sl = q * RPW + b;  // k-block within the tile
-      const int aw = sl >> 2, sh = 8 * (sl & 3);
-#pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        u32 byte;
-        if constexpr (F == F3) {
-          byte = i == 0 ? ((tile[0][tx][aw] ^ tile[1][tx][aw]) >> sh) : (tile[1][tx][aw] >> sh);
-        } else {
-          byte = tile[i][tx][aw] >> sh;
-        }
-        v |= (byte & 0xFFu) << (8 * (b * NIP + i));
+      for (int i = 0; i < 4; ++i) {
+        const int64_t row = rbase + ty + 8 * i;
+        const int w = wbase + tx;
+        tile[d][ty + 8 * i][tx] = (row < m && w < wa32) ? A[((int64_t)d * m + row) * wa32 + w] : 0u;
       }
+    __syncthreads();
+    // 128 k-blocks per tile -> 128 / RPW output words
+    for (int q = ty; q < 128 / RPW; q += 8) {
+      const int oq = (wbase * 4) / RPW + q;
+      const int64_t row = rbase + tx;
+      if (oq >= nwords || row >= mpad) continue;
+      u32 v = 0;
+#pragma unroll
+      for (int b = 0; b < RPW; ++b) {
+        const int sl = q * RPW + b;  // k-block within the tile
+        const int aw = sl >> 2, sh = 8 * (sl & 3);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          u32 byte;
+          if constexpr (F == F3) {
+            byte = i == 0 ? ((tile[0][tx][aw] ^ tile[1][tx][aw]) >> sh) : (tile[1][tx][aw] >> sh);
+          } else {
+            byte = tile[i][tx][aw] >> sh;
+          }
+          v |= (byte & 0xFFu) << (8 * (b * NIP + i));
+        }
+      }
+      IW[(int64_t)oq * mpad + row] = v;
     }
-    IW[(int64_t)oq * mpad + row] = v;
+    __syncthreads();
   }
 }
 
@@ -352,14 +358,14 @@ cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, 
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
                                int wa32, int nwords, cudaStream_t st) {
   if (k == 8) {
-    dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), 1);
+    dim3 grid((wa32 + 31) / 32, (unsigned)std::min<int64_t>((mpad + 31) / 32, 65535), 1);
 #define SG_IW(FF) index_words_kernel<FF><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords)
     SG_FOR_EACH_FIELD_CASE(field, SG_IW)
 #undef SG_IW
     return cudaGetLastError();
   }
   const int R = field == F2 ? 1 : (field == F5 || field == F7 || field == GF8 || field == Z8) ? 3 : 2;
-  dim3 grid((wa32 + 31) / 32, (unsigned)((mpad + 31) / 32), R);
+  dim3 grid((wa32 + 31) / 32, (unsigned)std::min<int64_t>((mpad + 31) / 32, 65535), R);
   transpose_a_kernel<<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, field == F3);
   return cudaGetLastError();
 }

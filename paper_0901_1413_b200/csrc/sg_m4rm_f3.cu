@@ -10,6 +10,7 @@ static KernelInfo g_table[] = {
     SG_KSET8(F3),
     SG_KSET8_2PLANE(F3),
     SG_KLOW(F3),
+#ifdef SG_EXPERIMENTS  // ablation variants (tools/ablate.py): results are wrong by design
     SG_KA(F3, 8, 16, 0, 256, 1),
     SG_KA(F3, 8, 16, 0, 256, 2),
     SG_KA(F3, 8, 16, 0, 256, 4),
@@ -20,6 +21,7 @@ static KernelInfo g_table[] = {
     SG_KA(F3, 8, 16, 2, 256, 1),
     SG_KA(F3, 8, 16, 2, 256, 2),
     SG_KA(F3, 8, 16, 2, 256, 4),
+#endif
 };
 
 int kernels_f3(KernelInfo** out) {

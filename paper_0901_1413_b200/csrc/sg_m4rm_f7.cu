@@ -11,11 +11,13 @@ static KernelInfo g_table[] = {
     SG_K(F7, 8, 8, 1, 256),
     SG_K(F7, 8, 4, 1, 512),
     SG_KLOW(F7),
+#ifdef SG_EXPERIMENTS  // ablation variants (tools/ablate.py): results are wrong by design
     SG_KA(F7, 8, 8, 1, 256, 1),
     SG_KA(F7, 8, 8, 1, 256, 2),
     SG_KA(F7, 8, 8, 1, 256, 4),
     SG_KA(F7, 8, 8, 2, 256, 2),
     SG_KA(F7, 8, 8, 2, 256, 4),
+#endif
 };
 
 int kernels_f7(KernelInfo** out) {

@@ -72,6 +72,15 @@ __device__ __forceinline__ void pack_word(const uint8_t* __restrict__ src, bool 
   }
 }
 
+// Bad input: OR `bit` into the caller's status word (mapped page-locked host memory, read by
+// sg_stream_check).  Every writer of one kernel sets the same bit and the kernels of one stream
+// run in order, so a plain read-or-write suffices (no system-scope atomics over PCIe).
+__device__ __forceinline__ void flag_error(int* err, int bit) {
+  volatile int* v = err;
+  *v = *v | bit;
+  __threadfence_system();
+}
+
 template <int F>
 __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ dense, int64_t m, int64_t n,
                                                    int64_t ld, u32* __restrict__ planes, int wc32, int* err) {
@@ -95,7 +104,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ d
       if (row2 < m) __stcs(planes + ((int64_t)d * m + row2) * wc32 + w, p2[d]);
     }
   }
-  if (bad) atomicOr(err, 1);
+  if (bad) flag_error(err, 1);
 }
 
 template <int F>
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const u32* __restrict__ pla
       }
     }
   }
-  if (bad) atomicOr(err, 2);
+  if (bad) flag_error(err, 2);
 }
 
 __global__ void canonicalize_kernel(int field, uint64_t* __restrict__ p, int64_t n_words) {
@@ -306,6 +315,9 @@ __global__ void block_driver_kernel(Planes C, int64_t wc64, Planes A, int64_t wa
       g[d] = x;
     }
     if (F == F3) g[0] ^= g[1];  // pos = A0 ^ A1, neg = A1
+    // the reference skips a row whose indices are all zero without touching C or T[0]
+    // (_core_py.py:208-209, 218-222, 230-231, 247-248); F3 skips its add and its sub separately
+    if ((g[0] | g[1] | g[2]) == 0u) continue;
     uint64_t out[3] = {0, 0, 0};
     for (int half = 0; half < 2; ++half) {
       const int sh = 32 * half;
@@ -315,15 +327,15 @@ __global__ void block_driver_kernel(Planes C, int64_t wc64, Planes A, int64_t wa
       if constexpr (F == F2) {
         c.p[0] ^= T_(0, g[0]);
       } else if constexpr (F == F3) {
-        f3_add(c.p[0], c.p[1], T_(0, g[0]), T_(1, g[0]));
-        f3_sub(c.p[0], c.p[1], T_(0, g[1]), T_(1, g[1]));
+        if (g[0]) f3_add(c.p[0], c.p[1], T_(0, g[0]), T_(1, g[0]));
+        if (g[1]) f3_sub(c.p[0], c.p[1], T_(0, g[1]), T_(1, g[1]));
       } else if constexpr (F == GF4) {
         const u32 q1 = T_(1, g[1]);
         c.p[0] ^= T_(0, g[0]) ^ q1;
         c.p[1] ^= T_(1, g[0]) ^ T_(0, g[1]) ^ q1;
       } else if constexpr (F == Z4) {  // acc = 2 T[g1] + T[g0]; C += acc  (_core_py.py:225-238)
         u32 a0 = 0u, a1 = T_(0, g[1]);
-        z4_add(a0, a1, T_(0, g[0]), T_(1, g[0]));
+        if (g[0]) z4_add(a0, a1, T_(0, g[0]), T_(1, g[0]));
         z4_add(c.p[0], c.p[1], a0, a1);
       } else if constexpr (F == GF8) {  // power basis: C += T[g0] + x T[g1] + x^2 T[g2]
         u32 x0 = T_(0, g[2]), x1 = T_(1, g[2]), x2 = T_(2, g[2]);
@@ -429,6 +441,67 @@ __global__ void classical_kernel(Planes A, int64_t wa64, Planes B, int64_t wb64,
   }
 }
 
+// The reference backend's classical drivers, raw and in place (_core_py.py:292-366): for every
+// row j of B in order, C_i += a_ij B_j with the reference's per-field expansion -- F2 XOR; F3 sub
+// for -1 (sign bit), else add for 1; Z/4 acc = 2 B_j [a1] + B_j [a0]; F5 / F7 / Z/8 Horner over
+// the bits of a_ij (acc = B_j [a2]; 2 acc (+ B_j [a1]); 2 acc (+ B_j [a0])).  A row whose
+// coefficient is 0 is skipped.  C keeps its raw patterns (no canonical reduction), so the
+// output bits equal the pure backend's for any legal input C.  One thread per (row, 32-bit word).
+template <int F>
+__global__ void classical_block_kernel(Planes C, int64_t wc64, Planes A, int64_t wa64, Planes B, int64_t m,
+                                       int64_t l) {
+  constexpr int R = Traits<F>::R;
+  const int64_t wc32 = 2 * wc64;
+  const int64_t total = m * wc32;
+  const u32* Bp[3];
+  u32* Cp[3];
+  for (int d = 0; d < R; ++d) {
+    Bp[d] = reinterpret_cast<const u32*>(B.p[d]);
+    Cp[d] = reinterpret_cast<u32*>(C.p[d]);
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / wc32, w = i % wc32;
+    V<F> c;
+    for (int d = 0; d < R; ++d) c.p[d] = Cp[d][row * wc32 + w];
+    for (int64_t j = 0; j < l; ++j) {
+      unsigned v = 0;
+      for (int d = 0; d < R; ++d) v |= (unsigned)((A.p[d][row * wa64 + (j >> 6)] >> (j & 63)) & 1ull) << d;
+      if (!v) continue;
+      V<F> b;
+      for (int d = 0; d < R; ++d) b.p[d] = Bp[d][j * wc32 + w];
+      if constexpr (F == F2 || F == GF4 || F == GF8) {
+        // (GF4 / GF8 have no reference driver: power basis, C += sum_d bit_d x^d B_j)
+        V<F> x = b;
+        for (int d = 0; d < R; ++d) {
+          if ((v >> d) & 1)
+            for (int e = 0; e < R; ++e) c.p[e] ^= x.p[e];
+          if constexpr (F == GF4) { const u32 t = x.p[1]; x.p[1] ^= x.p[0]; x.p[0] = t; }
+          if constexpr (F == GF8) gf8_mulx(x.p[0], x.p[1], x.p[2]);
+        }
+      } else if constexpr (F == F3) {
+        if (v & 2) f3_sub(c.p[0], c.p[1], b.p[0], b.p[1]);
+        else f3_add(c.p[0], c.p[1], b.p[0], b.p[1]);
+      } else if constexpr (F == Z4) {
+        u32 a0 = 0u, a1 = (v & 2) ? b.p[0] : 0u;
+        if (v & 1) z4_add(a0, a1, b.p[0], b.p[1]);
+        z4_add(c.p[0], c.p[1], a0, a1);
+      } else {  // F5, F7, Z8
+        V<F> acc;
+        for (int d = 0; d < R; ++d) acc.p[d] = (v & 4) ? b.p[d] : 0u;
+        for (int bit = 1; bit >= 0; --bit) {
+          if constexpr (F == F5) f5_double(acc.p[0], acc.p[1], acc.p[2]);
+          if constexpr (F == F7) f7_double(acc.p[0], acc.p[1], acc.p[2]);
+          if constexpr (F == Z8) { acc.p[2] = acc.p[1]; acc.p[1] = acc.p[0]; acc.p[0] = 0u; }
+          if ((v >> bit) & 1) vadd<F>(acc, b);
+        }
+        vadd<F>(c, acc);
+      }
+    }
+    for (int d = 0; d < R; ++d) Cp[d][row * wc32 + w] = c.p[d];
+  }
+}
+
 static unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -521,6 +594,15 @@ cudaError_t launch_classical(int field, Planes A, int64_t wa64, Planes B, int64_
   if (work <= 0) return cudaSuccess;
   const unsigned g = grid_for(work, 256);
   SG_FIELD_SWITCH(field, classical_kernel, A, wa64, B, wb64, C, m, l);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_classical_block(int field, Planes C, int64_t wc64, Planes A, int64_t wa64, Planes B, int64_t m,
+                                   int64_t l, cudaStream_t st) {
+  const int64_t work = m * 2 * wc64;
+  if (work <= 0) return cudaSuccess;
+  const unsigned g = grid_for(work, 256);
+  SG_FIELD_SWITCH(field, classical_block_kernel, C, wc64, A, wa64, B, m, l);
   return cudaGetLastError();
 }
 }  // namespace sg

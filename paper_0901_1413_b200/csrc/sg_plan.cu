@@ -206,6 +206,7 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       const int bps = (nblocks + sp - 1) / sp;
       const int splits = (nblocks + bps - 1) / bps;
       if (splits != sp) continue;
+      if (rgroups > 65535 || splits > 65535) continue;  // grid.y / grid.z limits (stream-K has none)
       const double ctas = (double)slabs * rgroups * splits;
       // calibrated variants: measured per-block and per-CTA clocks; others: the analytic
       // model with a 25 % penalty, so a measured variant wins unless clearly worse
@@ -228,7 +229,9 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       }
     }
   }
-  if (!best.ki) return fail(SG_EUNSUPPORTED, "no compiled M4RM kernel matches the request (check sg_set_plan_override)");
+  if (!best.ki)
+    return fail(SG_EUNSUPPORTED, "no compiled M4RM kernel matches the request (check sg_set_plan_override; more "
+                                 "than 65535 row groups need the k = 8 stream-K plan)");
   best.K = K;
   best.nblocks = nblocks;
   best.wa32 = (int)wa32;

@@ -60,9 +60,25 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
             raise RuntimeError("no CUDA device is available: the B200 path has no CPU fallback")
         a = A.planes.contiguous()
         b = B.planes.contiguous()
-        C = BitslicedMatrix.zero(field, m, n, device="cpu") if out is None else out
-        if out is None and a.is_pinned() and b.is_pinned():
-            C.planes = C.planes.pin_memory()  # page-locked in, page-locked out: async copies
+        if out is None:
+            C = BitslicedMatrix.zero(field, m, n, device="cpu")
+            if a.is_pinned() and b.is_pinned():
+                C.planes = C.planes.pin_memory()  # page-locked in, page-locked out: async copies
+        else:
+            # sg_m4rm_host writes R*m*W words through this pointer: the same checks as on the
+            # device, plus host residency (a device pointer is not a host buffer)
+            if not isinstance(out, BitslicedMatrix) or out.field is not field or (out.nrows, out.ncols) != (m, n):
+                raise ValueError("out has the wrong field or shape")
+            if out.device.type != "cpu":
+                raise ValueError("out must be a host matrix when both operands are on the host")
+            if not out.planes.is_contiguous():
+                out.planes = out.planes.contiguous()
+            for t in (a, b):
+                lo, hi = t.data_ptr(), t.data_ptr() + t.numel() * 8
+                if t.numel() and out.planes.numel() and lo < out.planes.data_ptr() + out.planes.numel() * 8 \
+                        and out.planes.data_ptr() < hi:
+                    raise ValueError("out must not overlap the operands")
+            C = out
         if m and n:
             _lib.check(L.sg_m4rm_host(field.code, _vp(a), _vp(b), _vp(C.planes), m, l, n, k,
                                       torch.cuda.current_device()))

@@ -97,14 +97,19 @@ class BitslicedMatrix:
         if isinstance(entries, torch.Tensor):
             if entries.dtype.is_floating_point:
                 raise ValueError("entries must be integers")
-            if entries.numel() and (int(entries.min()) < 0 or int(entries.max()) >= field.order):
+            if entries.dtype != torch.uint8 and entries.numel() and (
+                    int(entries.min()) < 0 or int(entries.max()) >= field.order):
                 raise ValueError(f"entries out of range for {field.name}")
             dense = entries.to(torch.uint8)
         else:
             arr = np.asarray(entries)
             if arr.ndim != 2:
                 raise ValueError("entries must be two-dimensional")
-            if arr.size and (arr.min() < 0 or arr.max() >= field.order):
+            if not np.issubdtype(arr.dtype, np.integer):
+                raise ValueError("entries must be integers")
+            # wider integer types must be checked before the uint8 cast (256 would wrap to 0);
+            # uint8 entries are range-checked by the pack kernel itself
+            if arr.dtype != np.uint8 and arr.size and (arr.min() < 0 or arr.max() >= field.order):
                 raise ValueError(f"entries out of range for {field.name}")
             dense = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint8))
         if dense.dim() != 2:
@@ -117,8 +122,10 @@ class BitslicedMatrix:
         if m and n:
             dd = dense.to(gpu, non_blocking=False).contiguous()
             with torch.cuda.device(gpu):
-                _lib.check(_lib.load().sg_pack(field.code, _vp(dd), m, n, n, _vp(out.planes),
-                                               _lib.current_stream_handle(gpu)))
+                st = _lib.current_stream_handle(gpu)
+                L = _lib.load()
+                _lib.check(L.sg_pack(field.code, _vp(dd), m, n, n, _vp(out.planes), st))
+                _lib.check(L.sg_stream_check(st))  # ValueError on an entry that is not a residue
         return out if target.type == "cuda" else out.to(target)
 
     @classmethod
@@ -126,12 +133,8 @@ class BitslicedMatrix:
         """Deterministic uniform residues: the DenseMatrix.random stream (oracle.py:47-50)."""
         if isinstance(field, str):
             field = by_name(field)
-        g = np.random.Generator(np.random.PCG64(seed))
-        dense = np.empty((m, n), dtype=np.uint8)
-        step = max(1, (1 << 24) // max(n, 1))
-        for r0 in range(0, m, step):
-            r1 = min(m, r0 + step)
-            dense[r0:r1] = g.integers(0, field.order, size=(r1 - r0, n), dtype=np.int64)
+        from .dense import DenseMatrix
+        dense = np.asarray(DenseMatrix.random(field, m, n, seed))
         return cls.from_dense(field, dense, device=device)
 
     # ------------------------------------------------------------------ movement
@@ -155,15 +158,26 @@ class BitslicedMatrix:
         return self if self.device.type == "cuda" else self.cuda()
 
     # ------------------------------------------------------------------ dense views
-    def to_dense(self) -> np.ndarray:
+    def to_dense(self) -> "DenseMatrix":
+        """Unpack to a DenseMatrix: residues unpacked on the GPU, returned on the host.
+
+        The result behaves like the reference's DenseMatrix (.field, .nrows, .ncols, .entries as
+        an int64 (m, n) array, ==) and converts to a numpy array with np.asarray (uint8)."""
+        from .dense import DenseMatrix
+        return DenseMatrix._trusted(self.field, self.to_numpy())
+
+    def to_numpy(self) -> np.ndarray:
         """Unpack to dense residues (uint8, shape (m, n)) on the GPU, returned on the host."""
         g = self._on_gpu()
         _require_cuda(g.device)
         out = torch.empty((self.nrows, self.ncols), dtype=torch.uint8, device=g.device)
         if self.nrows and self.ncols:
             with torch.cuda.device(g.device):
-                _lib.check(_lib.load().sg_unpack(self.field.code, _vp(g.planes), self.nrows, self.ncols,
-                                                 _vp(out), self.ncols, _lib.current_stream_handle(g.device)))
+                st = _lib.current_stream_handle(g.device)
+                L = _lib.load()
+                _lib.check(L.sg_unpack(self.field.code, _vp(g.planes), self.nrows, self.ncols, _vp(out),
+                                       self.ncols, st))
+                _lib.check(L.sg_stream_check(st))  # ValueError on an illegal F3 pattern
         return out.cpu().numpy()
 
     def get(self, i: int, j: int) -> int:
@@ -262,5 +276,89 @@ class BitslicedMatrix:
     __eq__ = equals
     __hash__ = None
 
+    def row(self, i: int) -> "RowRef":
+        """A view of row i across every plane."""
+        return RowRef(self, i)
+
     def __repr__(self):
         return f"BitslicedMatrix({self.field.name}, {self.nrows}x{self.ncols}, {self.device})"
+
+
+class RowRef:
+    """One row of a BitslicedMatrix across all R planes: R word slices of words_per_row words
+    (SPEC.md:210-213).  A view -- row_accumulate on it updates the parent matrix in place."""
+
+    __slots__ = ("matrix", "index")
+
+    def __init__(self, matrix: BitslicedMatrix, index: int):
+        if not isinstance(matrix, BitslicedMatrix):
+            raise TypeError("RowRef needs a BitslicedMatrix")
+        if not 0 <= index < matrix.nrows:
+            raise IndexError(f"row {index} out of range for {matrix.nrows} rows")
+        self.matrix = matrix
+        self.index = index
+
+    @property
+    def field(self) -> FieldSpec:
+        return self.matrix.field
+
+    @property
+    def ncols(self) -> int:
+        return self.matrix.ncols
+
+    @property
+    def words(self) -> torch.Tensor:
+        """The (R, words_per_row) int64 view of the row's plane words."""
+        return self.matrix.planes[:, self.index]
+
+    def to_list(self) -> list:
+        return [self.matrix.get(self.index, j) for j in range(self.ncols)]
+
+    def __repr__(self):
+        return f"RowRef({self.field.name}, row {self.index} of {self.matrix.nrows}x{self.ncols})"
+
+
+_ROW_OPS = {("f2", "add"): "f2_add", ("f2", "sub"): "f2_add", ("f3", "add"): "f3_add", ("f3", "sub"): "f3_sub",
+            ("f5", "add"): "f5_add", ("f5", "sub"): "f5_sub", ("f7", "add"): "f7_add", ("f7", "sub"): "f7_sub",
+            ("z4", "add"): "z4_add", ("z4", "sub"): "z4_sub", ("z8", "add"): "z8_add", ("z8", "sub"): "z8_sub",
+            ("gf4", "add"): "gf4_add", ("gf4", "sub"): "gf4_add", ("gf8", "add"): "gf8_add",
+            ("gf8", "sub"): "gf8_add"}
+
+
+def row_accumulate(dst: RowRef, src: RowRef, mode: str = "add") -> None:
+    """dst <- dst +/- src lanewise through the field's plane kernel, in place.
+
+    The row's words are updated on the GPU (one sg_plane_op launch over one row); a row of a
+    host matrix is moved to the GPU and back.  Padding lanes stay zero (F7 sub re-masks them).
+    Errors: field or length mismatch (ValueError), unknown mode."""
+    if not isinstance(dst, RowRef) or not isinstance(src, RowRef):
+        raise TypeError("row_accumulate takes two RowRef")
+    if dst.field is not src.field:
+        raise ValueError(f"field mismatch: {dst.field.name} vs {src.field.name}")
+    if dst.ncols != src.ncols:
+        raise ValueError(f"row lengths differ: {dst.ncols} vs {src.ncols}")
+    if mode not in ("add", "sub"):
+        raise ValueError(f"mode must be 'add' or 'sub', not {mode!r}")
+    f = dst.field
+    W = dst.matrix.words_per_row
+    if W == 0:
+        return
+    M = dst.matrix
+    dev = M.device if M.device.type == "cuda" else _dev("cuda")
+    _require_cuda(dev)
+    on_dev = M.device.type == "cuda"
+    # (R, W): a strided view into the device matrix (updated in place), or a device copy of a host row
+    d = M.planes[:, dst.index] if on_dev else M.planes[:, dst.index].to(dev).contiguous()
+    s = src.matrix.planes[:, src.index].to(dev)
+    R = f.bits
+    # each plane's row is a contiguous run of W words; its pointer is the view's row d
+    stride = d.stride(0) * 8
+    dptr, _k1 = _lib.ptr_array([d.data_ptr() + p * stride for p in range(R)])
+    sptr, _k2 = _lib.ptr_array([s.data_ptr() + p * s.stride(0) * 8 for p in range(R)])
+    rem = M.ncols % 64
+    tail = ((1 << rem) - 1) if rem else (1 << 64) - 1
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().sg_plane_op(_lib.OPS[_ROW_OPS[(f.name, mode)]], dptr, sptr, 1, W, tail, 0,
+                                           _lib.current_stream_handle(dev)))
+    if not on_dev:
+        M.planes[:, dst.index] = d.cpu()

@@ -24,6 +24,12 @@ Outputs (all small, committed):
   m4rm_z4/z8.npz     the reference's ring drivers m4rm_block_z4/z8 (_core_py.py:225-238, 284-286)
   ext_<f>.npz        oracle_ext_multiply over F8, F9, F25, F27 (fields.py:216-219) on seeded
                      coefficient matrices: the targets of the GPU extension-field paths
+  blocks_<f>.npz     one call of the pure backend's m4rm_block_<f> / classical_<f>, reached
+                     through the reference's own backend registry (_core.set_active("pure");
+                     _core.active(), _core.py:15-61), on raw inputs: C holding arbitrary legal
+                     patterns (F5 5/6/7, F7 7), tables from the Gray build or random raw rows
+                     with T[0] != 0, partial row ranges, ragged widths -- the raw output bits
+                     the "cuda" backend must reproduce (_core_cuda)
 
 Usage:  python tests/golden/make_golden.py     (from the repo root, in this container)
 """
@@ -47,13 +53,13 @@ def load_reference():
     pkg.__path__ = [REF]
     sys.modules["slicegemm"] = pkg
     mods = {}
-    for name in ("fields", "programs", "oracle", "_core_py", "kernels"):
+    for name in ("fields", "programs", "oracle", "_core_py", "kernels", "_core"):
         mods[name] = importlib.import_module(f"slicegemm.{name}")
     return mods
 
 
 R = load_reference()
-fields, oracle, core, kernels = R["fields"], R["oracle"], R["_core_py"], R["kernels"]
+fields, oracle, core, kernels, registry = R["fields"], R["oracle"], R["_core_py"], R["kernels"], R["_core"]
 W = 64
 
 
@@ -285,7 +291,83 @@ def ext_fixture(spec, cases):
     return recs
 
 
+def pack_patterns(bits, pat):
+    """Raw patterns (m, n) -> plane-major uint64 words (no canonicalization)."""
+    m, n = pat.shape
+    words = (n + W - 1) // W
+    planes = np.zeros((bits, m, words), dtype=np.uint64)
+    for d in range(bits):
+        b = ((pat >> d) & 1).astype(np.uint8)
+        padded = np.zeros((m, words * W), dtype=np.uint8)
+        padded[:, :n] = b
+        planes[d] = np.packbits(padded.reshape(m, words, W), axis=2, bitorder="little").view("<u8").reshape(m, words)
+    return planes
+
+
+def raw_patterns(field, rng, shape):
+    """Uniform over the field's legal patterns, redundant encodings included (F5 5..7, F7 7)."""
+    legal = np.array(sorted(p for p, e in enumerate(field.decode_table) if e is not None), dtype=np.int64)
+    return legal[rng.integers(0, len(legal), size=shape)]
+
+
+def block_fixture(field, seed):
+    """Raw single calls of the pure backend's block and classical drivers via the registry."""
+    registry.set_active("pure")
+    be = registry.active()
+    assert be.NAME == "pure"
+    rng = np.random.default_rng(seed)
+    recs = {}
+    cases = [(9, 40, 70, 3, 8, 0, 9, "gray"), (33, 130, 200, 64, 8, 5, 30, "gray"), (17, 24, 65, 10, 6, 0, 17, "gray"),
+             (50, 200, 129, 120, 8, 11, 12, "random"), (6, 10, 1, 2, 5, 0, 6, "random"), (70, 70, 64, 62, 8, 1, 69, "gray"),
+             (40, 300, 100, 290, 10, 3, 37, "random"), (12, 16, 16, 8, 8, 0, 12, "gray")]
+    for idx, (m, la, n, col0, kp, row0, row1, tkind) in enumerate(cases):
+        kp = min(kp, la - col0)
+        Cpat = raw_patterns(field, rng, (m, n))
+        Adense = rng.integers(0, field.order, size=(m, la))
+        Ap = pack(field, Adense)
+        Cp = pack_patterns(field.bits, Cpat)
+        if tkind == "gray":
+            Bd = rng.integers(0, field.order, size=(col0 + kp, n))
+            # the table of B rows col0 .. col0+kp-1 (the Gray build over those rows)
+            Bblk = pack(field, Bd[col0:col0 + kp])
+            T = build_table(field, Bblk, 0, kp, kp, n)
+            Tp = np.stack(T)
+        else:
+            Tp = pack_patterns(field.bits, raw_patterns(field, rng, (1 << kp, n)))
+        C = [Cp[d].copy() for d in range(field.bits)]
+        A = [np.ascontiguousarray(Ap[d]) for d in range(field.bits)]
+        Tl = [np.ascontiguousarray(Tp[d]) for d in range(field.bits)]
+        getattr(be, f"m4rm_block_{field.name}")(*C, *A, col0, kp, *Tl, row0, row1)
+        key = f"b{idx}"
+        recs[key + "_args"] = np.array([m, la, n, col0, kp, row0, row1], dtype=np.int64)
+        recs[key + "_C0"], recs[key + "_A"], recs[key + "_T"] = Cp, Ap, Tp
+        recs[key + "_C1"] = np.stack(C)
+    recs["nblock"] = np.array(len(cases))
+    ccases = [(5, 7, 9), (20, 65, 70), (33, 130, 64), (3, 1, 200), (64, 64, 129)]
+    for idx, (m, l, n) in enumerate(ccases):
+        Cp = pack_patterns(field.bits, raw_patterns(field, rng, (m, n)))
+        Ap = pack(field, rng.integers(0, field.order, size=(m, l)))
+        Bp = pack_patterns(field.bits, raw_patterns(field, rng, (l, n)))
+        C = [Cp[d].copy() for d in range(field.bits)]
+        getattr(be, f"classical_{field.name}")(*C, *[np.ascontiguousarray(Ap[d]) for d in range(field.bits)],
+                                              *[np.ascontiguousarray(Bp[d]) for d in range(field.bits)])
+        key = f"k{idx}"
+        recs[key + "_args"] = np.array([m, l, n], dtype=np.int64)
+        recs[key + "_C0"], recs[key + "_A"], recs[key + "_B"] = Cp, Ap, Bp
+        recs[key + "_C1"] = np.stack(C)
+    recs["nclassical"] = np.array(len(ccases))
+    return recs
+
+
+def main_blocks():
+    for i, fname in enumerate(("f2", "f3", "f5", "f7", "z4", "z8")):
+        recs = block_fixture(fields.FIELDS[fname], 900 + i)
+        np.savez_compressed(os.path.join(OUT, f"blocks_{fname}.npz"), **recs)
+        print(fname, "block cases", int(recs["nblock"]), "classical cases", int(recs["nclassical"]))
+
+
 def main():
+    main_blocks()
     with open(os.path.join(OUT, "kernel_cases.json"), "w") as f:
         json.dump(kernel_cases(), f, indent=0)
     for i, fname in enumerate(("z4", "z8")):
@@ -308,4 +390,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["blocks"]:
+        main_blocks()  # only the block / classical driver fixtures
+    else:
+        main()

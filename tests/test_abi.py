@@ -29,6 +29,8 @@ def test_library_exports_every_declared_symbol():
     assert syms == set(_lib.EXPORTS)
     for s in syms:
         assert getattr(L, s) is not None
+    # no result-corrupting experiment switch in the production library
+    assert not hasattr(L, "sg_debug_ablation")
 
 
 def test_abi_version_and_planes():

@@ -1,11 +1,18 @@
 """Full BASELINE-size checks (BASELINE.json configs 0-4, one GPU).
 
-At these sizes the bitsliced oracle is too slow, so the checks are:
-  * exact: C equals (A_f32 @ B_f32) mod p computed by cuBLAS fp32 with TF32 disabled -- exact,
+Checks, all bit-exact:
+  * the CPU oracle (oracle/sg_oracle.c, the restated reference path, on every host core):
+    C's planes equal the oracle's canonical planes (the north star's "bit-exact C versus the CPU
+    oracle for every config"; oracle.py:74-79 semantics);
+  * the planes are canonical, checked on the device for every size (F3: no sign-without-unit
+    lane; F5: every lane < 5; F7: no lane holding 7; padding lanes zero);
+  * a second, independent route: C equals (A_f32 @ B_f32) mod p computed by cuBLAS fp32 with TF32 disabled -- exact,
     since every partial sum is an integer below l*(p-1)^2 <= 294,912 < 2^24;
   * size-independent: Freivalds' identity C x = A (B x) mod p for random x, computed on the host
     in int64 from the unpacked matrices.
 Inputs are the DenseMatrix.random streams: A = seed 0, B = seed 1."""
+
+import os
 
 import numpy as np
 import pytest
@@ -73,15 +80,39 @@ def freivalds(fname, A, B, C, trials=6):
         assert np.array_equal(_matvec(C, x, p), _matvec(A, _matvec(B, x, p), p))
 
 
+def assert_canonical_on_device(fname, C):
+    """Every lane of C holds its field's canonical pattern, padding lanes zero."""
+    P = C.planes  # (R, m, W) int64 on the device
+    if fname == "f3":
+        bad = P[1] & ~P[0]                 # sign without unit: the illegal pattern 10
+    elif fname == "f5":
+        bad = P[2] & (P[1] | P[0])         # 5, 6, 7 are redundant encodings of 0, 1, 2
+    elif fname == "f7":
+        bad = P[2] & P[1] & P[0]           # 7 is the redundant encoding of 0
+    else:
+        bad = torch.zeros_like(P[0])       # GF(4): every pattern is canonical
+    assert int(torch.count_nonzero(bad)) == 0, f"{fname}: non-canonical lanes in C"
+    rem = C.ncols % 64
+    if rem:
+        tail = P[:, :, -1]
+        pad = torch.tensor(~((1 << rem) - 1) & ((1 << 63) - 1), dtype=torch.int64, device=P.device)
+        pad = pad | torch.tensor(-(1 << 63), dtype=torch.int64, device=P.device)  # bit 63
+        assert int(torch.count_nonzero(tail & pad)) == 0, f"{fname}: padding lanes set"
+
+
 @pytest.mark.parametrize("fname,m,l,n", CONFIGS)
 def test_baseline_config_exact(fname, m, l, n):
     A = oracle.random_dense(fname, m, l, 0)
     B = oracle.random_dense(fname, l, n, 1)
     f = FIELDS[fname]
     C = sg.m4rm_multiply(sg.BitslicedMatrix.from_dense(f, A), sg.BitslicedMatrix.from_dense(f, B), sg.M4rmParams(8))
-    Cd = C.to_dense()
+    assert_canonical_on_device(fname, C)
+    got = C.planes_numpy()
+    # 1. the CPU oracle (restated reference path), every host thread
+    want = oracle.m4rm(fname, oracle.pack(fname, A), oracle.pack(fname, B), l, n, 8, threads=os.cpu_count() or 1)
+    assert np.array_equal(got, want), f"{fname} {m}x{l}x{n}: C differs from the CPU oracle"
+    del want
+    # 2. an independent exact route (fp32 GEMM) and Freivalds' identity on the dense result
+    Cd = np.asarray(C.to_dense())
     freivalds(fname, A, B, Cd)
     assert np.array_equal(Cd, exact_gpu_product(fname, A, B))
-    # the planes are canonical (pack of the dense result is the unique canonical packing)
-    if m * n <= 8192 * 8192:
-        assert np.array_equal(C.planes_numpy(), oracle.pack(fname, Cd))

@@ -1,4 +1,7 @@
-"""Ablation timing of the M4RM kernel (results are wrong while ablating; timing only)."""
+"""Ablation timing of the M4RM kernel (results are wrong while ablating; timing only).
+
+Needs the experiments build: `make -C paper_0901_1413_b200/csrc clean all EXTRA=-DSG_EXPERIMENTS`
+(sg_debug_ablation and the ablated kernel variants are not in the production library)."""
 import os
 import sys
 
