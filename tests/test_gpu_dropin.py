@@ -122,7 +122,7 @@ def test_row_accumulate_spec_examples_and_random_rows():
                 if fname in ("f2", "gf4", "gf8"):
                     want[1] ^= d[3]
                 else:
-                    want[1] = (d[1].astype(int) + (1 if mode == "add" else -1) * d[3]) % q
+                    want[1] = (d[1].astype(int) + (1 if mode == "add" else -1) * d[3].astype(int)) % q
                 got = np.asarray(M.to_dense())
                 assert np.array_equal(got, want), (fname, mode, device)
                 # padding lanes stay zero (F7 sub complements and re-masks)
