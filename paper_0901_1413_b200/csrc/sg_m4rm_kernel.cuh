@@ -293,7 +293,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   constexpr int CPT = COPIES / TPE;        // replicas written per thread
 
   uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][R][E][COPIES] uint4
-  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][16][R][4]
+  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][R][16][4]
   u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
   uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ROWS);  // [3] B-slot barriers
@@ -430,7 +430,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
           }
         }
 #pragma unroll
-        for (int d = 0; d < R; ++d) th[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
+        for (int d = 0; d < R; ++d) th[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
       }
     }
   };
@@ -440,12 +440,13 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   auto phase2_compute = [&](int s, V<F> (&v)[4]) {
     const u32* th = thalf + (s & 1) * 2 * HALF;
     if (g_own < E) {
-      const uint4* lo = reinterpret_cast<const uint4*>(th + (g_own & ((1 << KLO) - 1)) * R * 4);
-      const uint4* hi = reinterpret_cast<const uint4*>(th + HALF + (g_own >> KLO) * R * 4);
+      // half tables are [half][plane][16 entries][4 words]: plane d of entry e at (half R + d) 16 + e
+      const uint4* lo = reinterpret_cast<const uint4*>(th) + (g_own & ((1 << KLO) - 1));
+      const uint4* hi = reinterpret_cast<const uint4*>(th + HALF) + (g_own >> KLO);
       V<F> hv[4];
 #pragma unroll
       for (int d = 0; d < R; ++d) {
-        const uint4 L = lo[d], H = hi[d];
+        const uint4 L = lo[d * 16], H = hi[d * 16];
         v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
         hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
       }
@@ -594,7 +595,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
                 }
               }
 #pragma unroll
-              for (int d = 0; d < R; ++d) thalf[((h * 16 + e) * R + d) * 4 + w] = acc.p[d];
+              for (int d = 0; d < R; ++d) thalf[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
             }
           }
         }
@@ -604,12 +605,12 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 #pragma unroll
         for (int it = 0; it < E / NBT; ++it) {
           const int g = bt + NBT * it;
-          const uint4* lo = reinterpret_cast<const uint4*>(thalf + (g & ((1 << KLO) - 1)) * R * 4);
-          const uint4* hi = reinterpret_cast<const uint4*>(thalf + HALF + (g >> KLO) * R * 4);
+          const uint4* lo = reinterpret_cast<const uint4*>(thalf) + (g & ((1 << KLO) - 1));
+          const uint4* hi = reinterpret_cast<const uint4*>(thalf + HALF) + (g >> KLO);
           V<F> v[4], hv[4];
 #pragma unroll
           for (int d = 0; d < R; ++d) {
-            const uint4 L = lo[d], H = hi[d];
+            const uint4 L = lo[d * 16], H = hi[d * 16];
             v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
             hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
           }

@@ -21,6 +21,6 @@ for C in 1 2 3 4 0; do
   ncu -i /tmp/${TAG}_cfg$C.ncu-rep --page details --csv > gpurun_out/${TAG}_ncu_cfg${C}_details.csv 2>/dev/null
 done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_e2e_launches.csv \
-    python tools/e2e_trace_streamed.py > gpurun_out/${TAG}_e2e_launches.log 2>&1
+    python tools/e2e_probe.py 1 > gpurun_out/${TAG}_e2e_launches.log 2>&1
 echo "e2e launch list rc=$?"
 ls -la gpurun_out | grep ${TAG}

@@ -14,6 +14,13 @@ M = {
     "smem_wavefront_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smem_wavefronts_ld": "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "smem_wavefronts_st": "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+    "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "smem_bank_conflicts_ld": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "smem_bank_conflicts_st": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "alu_inst_executed": "smsp__inst_executed_pipe_alu.sum",
+    "duration_us": "gpu__time_duration.sum",
 }
 tag = sys.argv[1]
 out = {"_source": f"profiles/{tag}_pipes.json from ncu --set full captures of the M4RM kernel"}
@@ -23,7 +30,7 @@ for arg in sys.argv[2:]:
            subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
     rows = list(csv.reader(io.StringIO(raw)))
     d = dict(zip(rows[0], rows[2]))
-    out[name] = {k: float(d[v]) for k, v in M.items() if v in d and d[v]}
+    out[name] = {k: float(d[v].replace(",", "")) for k, v in M.items() if v in d and d[v]}
     out[name]["kernel"] = d.get("Kernel Name", "")[:80]
 with open(f"profiles/{tag}_pipes.json", "w") as f:
     json.dump(out, f, indent=1)
