@@ -68,6 +68,9 @@ UNIT = "mul-adds/s"
 # Algorithmic shared-memory bytes per field mul-add: the table lookups, NI lookups x
 # R planes x 16 B per (row, k-block of 8, 128-column slab) -- F3 / GF(4) 2 x 2, F5 / F7 3 x 3, F2 1 x 1.
 SMEM_PER_MULADD = {"f2": 4 / 256, "f3": 16 / 256, "f5": 36 / 256, "f7": 36 / 256, "gf4": 16 / 256}
+# ... and what this kernel's lookups move: GF(4) at k = 8 reads Karatsuba tables (T0[g0], T1[g1],
+# T0^T1[g0^g1]: three one-plane lookups instead of two two-plane ones), 12 / 256 B per mul-add
+KERNEL_SMEM_PER_MULADD = dict(SMEM_PER_MULADD, gf4=12 / 256)
 # Integer-pipe work per (row, k-block, slab): counted from this kernel's compiled SASS -- the lookup
 # warps' main loop / RT (profiles/*_sass_mix.json, tools/sass_mix.py; LOP3 + PRMT + LEA + ... on the
 # ALU pipe, IMAD on the FMA pipe, LDS).  The table build runs on the builder warps and is not counted
@@ -184,8 +187,10 @@ def m4rm_roofline(name, field, m, l, n, k_ms, plan, peaks, device):
     mix = SASS_MIX.get(key)
     nblocks, slabs = -(-l // 8), -(-n // 128)
     smem_bytes = work * SMEM_PER_MULADD[field]
+    own_bytes = work * KERNEL_SMEM_PER_MULADD[field]
     r = {"smem": {"achieved": smem_bytes / t / 1e12, "peak": p_smem / 1e12, "unit": "TB/s",
-                  "frac": smem_bytes / t / p_smem, "algorithmic_bytes_per_launch": smem_bytes}}
+                  "frac": smem_bytes / t / p_smem, "algorithmic_bytes_per_launch": smem_bytes,
+                  "kernel_lookup_bytes_per_launch": own_bytes, "kernel_lookup_frac": own_bytes / t / p_smem}}
     if mix:
         units = float(m) * nblocks * slabs
         alu = units * mix["alu_per_row_block"]

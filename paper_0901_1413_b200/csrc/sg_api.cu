@@ -50,14 +50,15 @@ DevState& dev_state(int device) {
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device);
     for (int i = 0; i < m4rm_kernel_count(); ++i) {
       KernelInfo* k = m4rm_kernel_at(i);
-      cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
+      const void* fn = k->fn ? (const void*)k->fn : (const void*)k->fn_fused;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_bytes);
       if (k->fn_stream &&
           cudaFuncSetAttribute(k->fn_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem_stream) != cudaSuccess)
         k->fn_stream = nullptr;  // does not fit this device: no streamed variant
       cudaFuncAttributes fa;
-      if (cudaFuncGetAttributes(&fa, k->fn) == cudaSuccess) k->regs = fa.numRegs;
+      if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) k->regs = fa.numRegs;
       int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->launch_threads, k->smem_bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k->launch_threads, k->smem_bytes);
       k->occupancy = occ;
     }
     cudaGetLastError();
@@ -94,6 +95,27 @@ StatusFlag* flag_for(int device, cudaStream_t st, cudaError_t* err) {
     }
   }
   return &f;
+}
+
+// Split-K arrival / departure counters of the fused small-product kernel, per (device, stream):
+// zeroed once, and every fused launch leaves them zero (M4rmFusedArgs).
+std::map<std::pair<int, cudaStream_t>, Buf> g_cnt;
+unsigned* fused_counters(int device, cudaStream_t st, int ntiles, cudaError_t* err) {
+  Buf& b = g_cnt[{device, st}];
+  *err = cudaSuccess;
+  const size_t bytes = (size_t)2 * std::max(ntiles, 4096) * sizeof(unsigned);
+  if (b.bytes < bytes) {
+    if (b.p) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.p);
+    }
+    b.p = nullptr;
+    b.bytes = 0;
+    if ((*err = cudaMalloc(&b.p, bytes)) != cudaSuccess) return nullptr;
+    if ((*err = cudaMemsetAsync(b.p, 0, bytes, st)) != cudaSuccess) return nullptr;
+    b.bytes = bytes;
+  }
+  return (unsigned*)b.p;
 }
 
 void* workspace_for(int device, cudaStream_t st, size_t bytes, cudaError_t* err) {
@@ -172,6 +194,50 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
   uint32_t* AT = (uint32_t*)ws;
   int64_t at_bytes = ((int64_t)p.at_planes * p.at_words * p.mpad * 4 + 255) / 256 * 256;
   uint32_t* partial = (p.splits > 1 || p.streamk) ? (uint32_t*)(ws + at_bytes) : nullptr;
+  if (p.ki->fn_fused) {
+    // one cooperative launch: A's words staged directly, split-K summed in the kernel
+    if (sin) return fail(SG_EINVAL, "product is not prepared for streamed B");
+    M4rmFusedArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.B = (const uint32_t*)B;
+    fa.AT = nullptr;
+    fa.A = (const uint32_t*)A;
+    fa.C = (uint32_t*)C;  // splits == 1: C directly; else compact slots in P2, summed into Cout
+    fa.P2 = p.splits > 1 ? partial : nullptr;
+    fa.Cout = (uint32_t*)C;
+    fa.m = m;
+    fa.l = l;
+    fa.mpad = p.mpad;
+    fa.wa32 = p.wa32;
+    fa.wc32 = p.wc32;
+    fa.nblocks = p.nblocks;
+    fa.bps = p.bps;
+    fa.partial = p.splits > 1;
+    fa.ntiles = (int)(p.grid.x * p.grid.y);
+    cudaError_t e;
+    fa.cnt = fa.partial ? fused_counters(dev, st, fa.ntiles, &e) : nullptr;
+    if (fa.partial && !fa.cnt) return cuda_fail(e, "sg_m4rm fused counters");
+    CUtensorMap tmB;
+    memset(&tmB, 0, sizeof(tmB));
+    cudaEvent_t ev[2];
+    if (g_timing) {
+      for (int i = 0; i < 2; ++i) cudaEventCreate(&ev[i]);
+      cudaEventRecord(ev[0], st);
+    }
+    SG_CUDA(launch_m4rm_fused(*p.ki, fa, tmB, p.grid, st), "sg_m4rm fused kernel");
+    g_launches++;
+    if (g_timing) {
+      cudaEventRecord(ev[1], st);
+      cudaEventSynchronize(ev[1]);
+      float t1 = 0;
+      cudaEventElapsedTime(&t1, ev[0], ev[1]);
+      g_last_ms[0] = 0;
+      g_last_ms[1] = t1;
+      g_last_ms[2] = 0;
+      for (int i = 0; i < 2; ++i) cudaEventDestroy(ev[i]);
+    }
+    return SG_OK;
+  }
 
   cudaEvent_t ev[4];
   if (g_timing)
@@ -206,9 +272,10 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
     }();
     a.tma_b = tma_env != 0 && p.ki->sched == 2 && p.K == 8 && p.wc32 % 4 == 0 && ((uintptr_t)B % 16) == 0 &&
               encode_b_map(&tmB, B, field, l, p.wc32);
-    // A's index words by TMA too, except under stream-K (measured: F3 32768^3 -1 %, F7 -1.4 %,
-    // GF(4) 8192^3 stream-K +2.6 %; SG_TMA=2 forces it, for experiments)
-    a.tma_a = a.tma_b && (tma_env == 2 || !p.streamk);
+    // A's index words by TMA too, except under stream-K for F3 / F5 / F7 (measured: F3 32768^3
+    // -1 %, F7 -1.4 %); GF(4)'s Karatsuba kernel, whose builder warps are its critical path
+    // (three replicated table planes), gains 3.9 % (1.349 -> 1.297 ms).  SG_TMA=2 forces it.
+    a.tma_a = a.tma_b && (tma_env == 2 || !p.streamk || field == SG_GF4);
   }
   if (sin && !a.tma_b) return fail(SG_EINVAL, "streamed B needs the TMA staging path");
   a.streamk = p.streamk;
@@ -287,7 +354,7 @@ int sg_kernel_info(int index, int device, int* field, int* k, int* rows_per_thre
   if (k) *k = ki->k;
   if (rows_per_thread) *rows_per_thread = ki->rt;
   if (threads) *threads = ki->threads;
-  if (schedule) *schedule = ki->sched;
+  if (schedule) *schedule = ki->sched + (ki->fn_fused ? SCHED_FUSED : 0);
   if (occupancy) *occupancy = ki->occupancy;
   if (regs) *regs = ki->regs;
   if (smem_bytes) *smem_bytes = ki->smem_bytes;
@@ -463,7 +530,7 @@ int sg_plan(int field, int64_t m, int64_t l, int64_t n, int k, int* rows_per_cta
   if (splits) *splits = p.streamk ? -1 : p.splits;
   if (ctas) *ctas = (int)(p.grid.x * p.grid.y * p.grid.z);
   if (kernel_index) *kernel_index = p.kernel_index;
-  if (pipelined) *pipelined = p.ki->sched;
+  if (pipelined) *pipelined = p.ki->sched + (p.ki->fn_fused ? SCHED_FUSED : 0);
   if (threads) *threads = p.ki->threads;
   return SG_OK;
 }

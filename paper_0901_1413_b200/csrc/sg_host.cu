@@ -70,7 +70,25 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   const auto t_entry = std::chrono::steady_clock::now();
   const int R = planes(field);
   const int64_t wa = w64_of(l), wc = w64_of(n);
-  auto rcut = [&](int r) { return m * r / Pr; };
+  // row pieces: Pr equal pieces, or (SG_HOST_PIECES=w0,w1,..., experiments) up to 8 pieces with
+  // relative weights -- e.g. a small first piece starts the product sooner, a small last piece
+  // shortens the download after the last product
+  std::vector<int64_t> cuts{0};
+  if (const char* e = getenv("SG_HOST_PIECES")) {
+    std::vector<int64_t> w;
+    for (const char* q = e; *q && w.size() < 8;) {
+      w.push_back(std::max(1LL, atoll(q)));
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+    int64_t tot = 0, acc = 0;
+    for (int64_t x : w) tot += x;
+    for (int64_t x : w) cuts.push_back(m * (acc += x) / tot);
+  } else {
+    for (int r = 1; r <= Pr; ++r) cuts.push_back(m * r / Pr);
+  }
+  Pr = (int)cuts.size() - 1;
+  auto rcut = [&](int r) { return cuts[r]; };
   // everything that may allocate or synchronize happens before the first copy is queued
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -132,7 +150,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   char* cur = dbuf;
   uint64_t* dB = (uint64_t*)cur;
   cur += up(b_bytes);
-  uint64_t* dAp[4];
+  uint64_t* dAp[8];
   for (int r = 0; r < Pr; ++r) {
     dAp[r] = (uint64_t*)cur;
     cur += up((size_t)R * (rcut(r + 1) - rcut(r)) * wa * 8);
@@ -328,6 +346,27 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
       d->buf.bytes = need;
     }
     dbuf = (char*)d->buf.p;
+  }
+  // (an explicit SG_HOST_CHUNKS / SG_HOST_KCHUNKS request, experiments and tests, runs the pipelines)
+  if (Pk == 1 && Pr == 1 && Pc == 1 && !getenv("SG_HOST_NOSMALL") && !getenv("SG_HOST_CHUNKS") &&
+      !getenv("SG_HOST_KCHUNKS")) {
+    // a small product (C < 1 MB, inputs < 24 MB): nothing to overlap, so everything goes on one
+    // stream -- two contiguous uploads, the product, one download, one synchronization (no
+    // cross-stream events: each costs a few microseconds, a large share of a ~50 us call)
+    char* q = dbuf;
+    uint64_t* dA = (uint64_t*)q;
+    q += up(a_bytes);
+    uint64_t* dB = (uint64_t*)q;
+    q += up(b_bytes);
+    uint64_t* dC = (uint64_t*)q;
+    cudaStream_t st = d->comp;
+    if (a_bytes) SG_CUDA(cudaMemcpyAsync(dA, A, a_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D A");
+    if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D B");
+    rc = sg_m4rm(field, dA, dB, dC, m, l, n, k, nullptr, 0, st);
+    if (rc != SG_OK) return rc;
+    SG_CUDA(cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st), "sg_m4rm_host D2H C");
+    SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
+    return SG_OK;
   }
   const char* stream_e = getenv("SG_HOST_STREAM");  // experiments: 0 = upload B before the products
   if ((!stream_e || atoi(stream_e) != 0) && Pk == 1 && Pc == 1 && l > 0 && Pr <= 4) {

@@ -87,9 +87,25 @@ struct M4rmStreamArgs : M4rmArgs {
   unsigned* err;
 };
 constexpr int SK_SLOTS = 2;  // compact partial slots per stream-K CTA: its first and last segment
+// Fused small products (one launch, the *_fused instantiations of the serial / pipelined k = 8
+// variants): the CTAs stage A's own plane words (no index pre-pass; the bytes are extracted from
+// them, F3's "+1" index as A0 ^ A1), write split-K partials to C (= the partial planes), then the
+// splits of every tile meet at an arrival counter (a cooperative launch: all CTAs co-resident)
+// and each sums its 1/splits of the tile's rows into Cout.  cnt: 2 x tiles arrival / departure
+// counters, zero between launches (the last CTA to leave a tile resets them).
+struct M4rmFusedArgs : M4rmArgs {
+  const uint32_t* A;  // [R][m][wa32]  32-bit view of A's planes
+  uint32_t* Cout;     // final [R][m][wc32]
+  unsigned* cnt;
+  int ntiles;
+};
 
 typedef void (*KernelFn)(M4rmArgs, CUtensorMap);  // (args, B as a 3-D u32 tensor map for TMA staging)
 typedef void (*StreamKernelFn)(M4rmStreamArgs, CUtensorMap);
+typedef void (*FusedKernelFn)(M4rmFusedArgs, CUtensorMap);
+// schedule codes seen through the ABI (sg_kernel_info, sg_plan, sg_set_plan_override): a fused
+// variant reports its serial / pipelined schedule + SCHED_FUSED
+constexpr int SCHED_FUSED = 10;
 struct KernelInfo {
   KernelFn fn;
   int field, k, rt, threads;  // threads = lookup threads (rows = rt * threads)
@@ -101,6 +117,7 @@ struct KernelInfo {
   int ablation;        // experiments only: never planned unless sg_set_ablation selects it
   StreamKernelFn fn_stream;  // the same variant reading streamed B (M4rmStreamArgs), or nullptr
   int smem_stream;           // ... and its dynamic shared memory (+ the staged group order)
+  FusedKernelFn fn_fused;    // a fused small-product variant (fn == nullptr then), see M4rmFusedArgs
 };
 // streamed products stage their tile's group order in shared memory: at most this many groups
 constexpr int STRM_MAX_GROUPS = 2048;
@@ -116,6 +133,9 @@ cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorM
                         cudaStream_t st);
 cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, const CUtensorMap& tmB, dim3 grid,
                                  cudaStream_t st);
+// cooperative launch (every CTA co-resident: the split-K arrival counters spin)
+cudaError_t launch_m4rm_fused(const KernelInfo& ki, const M4rmFusedArgs& a, const CUtensorMap& tmB, dim3 grid,
+                              cudaStream_t st);
 // up to SLICES_MAX equally shaped R-plane row slices with their own plane strides (u32 words)
 constexpr int SLICES_MAX = 8;
 struct SliceSet {

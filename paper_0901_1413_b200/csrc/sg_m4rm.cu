@@ -355,6 +355,28 @@ cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, 
   return launch_pdl(ki.fn_stream, grid, dim3(ki.launch_threads), ki.smem_stream, st, a, tmB);
 }
 
+cudaError_t launch_m4rm_fused(const KernelInfo& ki, const M4rmFusedArgs& a, const CUtensorMap& tmB, dim3 grid,
+                              cudaStream_t st) {
+  if (!ki.fn_fused) return cudaErrorInvalidDeviceFunction;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(ki.launch_threads);
+  cfg.dynamicSmemBytes = ki.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  // co-residency matters only for the split-K meeting (SG_FUSED_COOP=0, experiments: a plain
+  // launch -- the planner keeps the grid within one wave either way)
+  static const bool coop = [] {
+    const char* e = getenv("SG_FUSED_COOP");
+    return !e || atoi(e) != 0;
+  }();
+  cfg.numAttrs = a.partial && coop ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, ki.fn_fused, a, tmB);
+}
+
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
                                int wa32, int nwords, cudaStream_t st) {
   if (k == 8) {

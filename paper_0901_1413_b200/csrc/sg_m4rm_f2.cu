@@ -7,6 +7,7 @@ namespace sg {
 static KernelInfo g_table[] = {
     SG_K(F2, 8, 16, 2, 256),
     SG_KSET8(F2),
+    SG_KFUSED(F2),
     SG_KSET8_2PLANE(F2),
     SG_KLOW(F2),
 };

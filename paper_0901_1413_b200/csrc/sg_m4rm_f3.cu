@@ -8,6 +8,7 @@ static KernelInfo g_table[] = {
     SG_K(F3, 8, 16, 2, 256),
     SG_K(F3, 8, 8, 2, 256),
     SG_KSET8(F3),
+    SG_KFUSED(F3),
     SG_KSET8_2PLANE(F3),
     SG_KLOW(F3),
 #ifdef SG_EXPERIMENTS  // ablation variants (tools/ablate.py): results are wrong by design

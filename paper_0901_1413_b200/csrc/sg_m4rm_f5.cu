@@ -8,6 +8,7 @@ static KernelInfo g_table[] = {
     SG_K(F5, 8, 8, 2, 256),
     SG_K(F5, 8, 4, 2, 256),
     SG_KSET8(F5),
+    SG_KFUSED(F5),
     SG_K(F5, 8, 8, 1, 256),
     SG_K(F5, 8, 4, 1, 512),
     SG_KLOW(F5),

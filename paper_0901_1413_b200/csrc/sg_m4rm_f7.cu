@@ -8,6 +8,7 @@ static KernelInfo g_table[] = {
     SG_K(F7, 8, 8, 2, 256),
     SG_K(F7, 8, 4, 2, 256),
     SG_KSET8(F7),
+    SG_KFUSED(F7),
     SG_K(F7, 8, 8, 1, 256),
     SG_K(F7, 8, 4, 1, 512),
     SG_KLOW(F7),

@@ -8,6 +8,7 @@ static KernelInfo g_table[] = {
     SG_K(GF4, 8, 16, 2, 256),
     SG_K(GF4, 8, 8, 2, 256),
     SG_KSET8(GF4),
+    SG_KFUSED(GF4),
     SG_KSET8_2PLANE(GF4),
     SG_KLOW(GF4),
 };

@@ -8,6 +8,7 @@ static KernelInfo g_table[] = {
     SG_K(GF8, 8, 8, 2, 256),
     SG_K(GF8, 8, 4, 2, 256),
     SG_KSET8(GF8),
+    SG_KFUSED(GF8),
     SG_K(GF8, 8, 8, 1, 256),
     SG_KLOW(GF8),
 };

@@ -37,9 +37,30 @@
 
 namespace sg {
 
+// Per-CTA phase timestamps (tools/small_timeline.cu builds with SG_TIMELINE; compiled out otherwise)
+#ifdef SG_TIMELINE
+__device__ unsigned long long g_tl[8192][8];
+#define SG_TL(i)                                                                                   \
+  do {                                                                                             \
+    if (threadIdx.x == 0) {                                                                        \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      g_tl[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x][i] = t_;               \
+    }                                                                                              \
+  } while (0)
+#else
+#define SG_TL(i) \
+  do {           \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(src), "r"(bytes));
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, int bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(dst);
@@ -136,6 +157,22 @@ template <int F> __device__ __forceinline__ V<F> vzero() {
   return v;
 }
 
+// GF(4), k = 8: Karatsuba tables.  Besides T0 (over B's plane 0) and T1 (plane 1) the table
+// holds T2 = T0 ^ T1 (over B0 ^ B1), and a row's update is C0 += T0[g0] + T1[g1],
+// C1 += T2[g0 ^ g1] + T0[g0]  ((a0 + a1 x)(b0 + b1 x) = (a0 b0 + a1 b1) + ((a0 + a1)(b0 + b1) + a0 b0) x
+// mod x^2 + x + 1): three one-plane lookups per (row, k-block) instead of two two-plane ones.
+template <int F, int K> __host__ __device__ constexpr bool karatsuba() { return F == GF4 && K == 8; }
+// table planes in shared memory
+template <int F, int K> __host__ __device__ constexpr int table_planes() { return karatsuba<F, K>() ? 3 : Traits<F>::R; }
+// staging slots of A's index words: Karatsuba GF(4) needs the room of the third table plane, and
+// with two k-blocks per index word two slots are enough (see issue_a)
+template <int F, int K, bool FUSED = false> __host__ __device__ constexpr int index_slots() {
+  return K == 8 && !FUSED ? (karatsuba<F, K>() ? 2 : 3) : 2;
+}
+// staged index source: k = 8 packed records from the pre-pass (one plane), else R planes of A
+// words (A^T from the transpose pre-pass, or A itself in the fused small-product kernels)
+template <int F, int K, bool FUSED = false> __host__ __device__ constexpr bool packed_index() { return K == 8 && !FUSED; }
+
 // Row accumulator of one lane: 4 words x RS planes.
 template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
 
@@ -143,8 +180,14 @@ template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
 template <int F> struct Rows { uint4 v[Traits<F>::NI][Traits<F>::R]; };
 
 // Load the table rows at byte offsets e[] (entry * ENTRY_BYTES) from this lane's replica base.
-template <int F, int TPL>
+template <int F, int TPL, bool KAR = false>
 __device__ __forceinline__ void load_rows(Rows<F>& r, const unsigned char* __restrict__ tl, const u32 (&e)[3]) {
+  if constexpr (KAR) {  // T0[g0], T1[g1], T2[g0 ^ g1] (entry offsets are g * ENTRY_BYTES: XOR them)
+    r.v[0][0] = *reinterpret_cast<const uint4*>(tl + e[0]);
+    r.v[1][0] = *reinterpret_cast<const uint4*>(tl + e[1] + TPL * 16);
+    r.v[0][1] = *reinterpret_cast<const uint4*>(tl + (e[0] ^ e[1]) + 2 * TPL * 16);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < Traits<F>::NI; ++i)
 #pragma unroll
@@ -155,8 +198,17 @@ __device__ __forceinline__ void load_rows(Rows<F>& r, const unsigned char* __res
 __device__ __forceinline__ u32 comp(const uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
 
 // One (row, k-block) update of the 4 C words a lane owns from its loaded table rows.
-template <int F>
+template <int F, bool KAR = false>
 __device__ __forceinline__ void accumulate(Acc<F>& c, const Rows<F>& r) {
+  if constexpr (KAR) {  // C0 += T0[g0] + T1[g1];  C1 += T2[g0 ^ g1] + T0[g0]   (2 LOP3 per word)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const u32 t0 = comp(r.v[0][0], w);
+      c.w[w][0] ^= t0 ^ comp(r.v[1][0], w);
+      c.w[w][1] ^= comp(r.v[0][1], w) ^ t0;
+    }
+    return;
+  }
   if constexpr (F == F5 || F == F7) {
     // carry-save networks issued adder by adder across the four words (ILP 4 per step)
     u32 in[4][9];
@@ -267,12 +319,15 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
                                              const int mode, const int slot) {
   constexpr bool PIPE = SCHED == 1;
   constexpr bool WS = SCHED >= 2;
+  constexpr bool FUSED = std::is_same_v<AT, M4rmFusedArgs>;
   static_assert(!WS || K == 8, "the warp-specialized schedules are k = 8 only");
   constexpr int R = Traits<F>::R;
   constexpr int E = 1 << K;
   constexpr int KLO = K < 4 ? K : 4;
   constexpr int KHI = K - KLO;
   constexpr int ROWS = RT * NT;
+  constexpr bool KAR = karatsuba<F, K>();
+  constexpr int TR = table_planes<F, K>();  // table planes (R, or 3 for Karatsuba GF(4))
   constexpr int TPLANE = E * ENTRY_BYTES;  // bytes per table plane
   constexpr int TPL = TPLANE / 16;         // uint4 per table plane
   constexpr int HALF = 16 * R * 4;         // u32 per half table
@@ -282,18 +337,18 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // k = 8: A's index bytes arrive pre-packed as one record of NIP bytes per k-block (the
   // index_words pre-pass), RPW records per 32-bit word, NSLOT staging slots of ROWS words.
   // k < 8: A^T bit planes, R planes x 2 slots.
-  constexpr bool IW = (K == 8);
+  constexpr bool IW = packed_index<F, K, FUSED>();
   constexpr int NI = Traits<F>::NI;
   constexpr int NIP = NI == 3 ? 4 : NI;
   constexpr int RPW = 4 / NIP;
-  constexpr int NSLOT = IW ? 3 : 2;       // A words in use + two blocks in flight
+  constexpr int NSLOT = index_slots<F, K, FUSED>();  // A words in use + blocks in flight
   constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
   constexpr int TPE_RAW = NT / E;
   constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
   constexpr int CPT = COPIES / TPE;        // replicas written per thread
 
-  uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][R][E][COPIES] uint4
-  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * R * TPLANE);   // [2 buf][2 half][R][16][4]
+  uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][TR][E][COPIES] uint4
+  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * TR * TPLANE);  // [2 buf][2 half][R][16][4]
   u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
   uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ROWS);  // [3] B-slot barriers
@@ -305,7 +360,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   if (s_begin >= s_end) return;
   // TMA staging of B is compiled into the warp-specialized schedule only (measured: no gain for
   // the others); there it is used when the host found B aligned for it (a.tma_b).
-  constexpr bool TMA_OK = WS && K == 8;
+  constexpr bool TMA_OK = WS && K == 8 && !FUSED;
   const bool tma_b = TMA_OK && a.tma_b;
   const bool tma_a = tma_b && a.tma_a;
 
@@ -386,6 +441,16 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
         u32* adst = ast + (next_word % NSLOT) * NAP * ROWS;
         const bool ok = next_word < a.wa32;
         const int rw = real_word(next_word);
+        if constexpr (FUSED) {
+          // A's own plane words, one per (plane, row): [slot][plane][row] like A^T
+          for (int q = t0; q < NAP * ROWS; q += nthr) {
+            const int d = q / ROWS, r = q % ROWS;
+            const bool ok2 = ok && row0 + r < a.m;
+            const u32* src = ok2 ? a.A + ((int64_t)d * a.m + row0 + r) * a.wa32 + rw : a.A;
+            cp_async4(adst + d * ROWS + r, src, ok2 ? 4 : 0);
+          }
+          continue;
+        }
         for (int q = t0; q < NAP * ROWS / 4; q += nthr) {
           const int d = q / (ROWS / 4), r4 = q % (ROWS / 4);
           const u32* src = ok ? a.AT + ((int64_t)d * a.wa32 + rw) * a.mpad + row0 + 4 * r4 : a.AT;
@@ -464,6 +529,9 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 #pragma unroll
       for (int d = 0; d < R; ++d)
         tb[d * TPL + g_own * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
+      if constexpr (KAR)
+        tb[2 * TPL + g_own * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[0] ^ v[0].p[1], v[1].p[0] ^ v[1].p[1],
+                                                                     v[2].p[0] ^ v[2].p[1], v[3].p[0] ^ v[3].p[1]);
     }
   };
 
@@ -499,6 +567,16 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       const int w0 = col0 >> 5, sh = col0 & 31;
       const u32* aw0 = ast + (w0 & 1) * R * ROWS;
       const u32* aw1 = ast + ((w0 + 1) & 1) * R * ROWS;
+      if constexpr (FUSED && K == 8) {
+        // A's plane words: byte s & 3 of each (F3: the "+1" index is A0 ^ A1, fields.py:98)
+        u32 x[R];
+#pragma unroll
+        for (int d = 0; d < R; ++d) x[d] = aw0[d * ROWS + lr];
+        if constexpr (F == F3) x[0] ^= x[1];
+#pragma unroll
+        for (int d = 0; d < R; ++d) e[d] = ((x[d] >> sh) & 255u) * ENTRY_BYTES;
+        return;
+      }
 #pragma unroll
       for (int d = 0; d < R; ++d) {
         u32 x = aw0[d * ROWS + lr];
@@ -521,20 +599,20 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       for (int t = 0; t < RT; ++t) between(t);
       return;
     }
-    const unsigned char* tl = tl0 + tb * R * TPLANE;
+    const unsigned char* tl = tl0 + tb * TR * TPLANE;
     Rows<F> ring[LA + 1];
 #pragma unroll
     for (int t = 0; t < LA && t < RT; ++t) {
       u32 e[3];
       entries(s, t, e);
-      load_rows<F, TPL>(ring[t], tl, e);
+      load_rows<F, TPL, KAR>(ring[t], tl, e);
     }
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
       if (t + LA < RT) {
         u32 e[3];
         entries(s, t + LA, e);
-        load_rows<F, TPL>(ring[(t + LA) % (LA + 1)], tl, e);
+        load_rows<F, TPL, KAR>(ring[(t + LA) % (LA + 1)], tl, e);
       }
       if constexpr (ABL & 2) {
 #pragma unroll
@@ -542,7 +620,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 #pragma unroll
           for (int d = 0; d < Traits<F>::R; ++d) c[t].w[w][d] ^= comp(ring[t % (LA + 1)].v[0][d], w) ^ comp(ring[t % (LA + 1)].v[Traits<F>::NI - 1][d], w);
       } else {
-        accumulate<F>(c[t], ring[t % (LA + 1)]);
+        accumulate<F, KAR>(c[t], ring[t % (LA + 1)]);
       }
       between(t);
     }
@@ -553,6 +631,13 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     constexpr int NB = NT + NBT;  // all threads take part in every FULL / EMPTY barrier
     auto FULL = [](int s) { return 1 + (s & 1); };
     auto EMPTY = [](int s) { return 3 + (s & 1); };
+    // LW2 (experiment, off): the builders publish block s's half tables (double-buffered,
+    // HALF(s)) and store table planes 0 and 1 of Karatsuba GF(4); the lookup warps derive plane
+    // 2 = T0 ^ T1 of block s+1 from the half tables halfway through block s's lookups.  Measured
+    // slower (GF(4) 8192^3 1.35 -> 1.63 ms): the extra barrier inside the lookup loop costs more
+    // than the builders' third-plane stores.
+    constexpr bool LW2 = false;
+    auto HALFB = [](int s) { return 6 + (s & 1); };
     if constexpr (ROLE == 1) {
       // ------------------------------------------------ builder warps
       const int bt = tid - NT;
@@ -594,23 +679,30 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
                   vadd<F>(acc, b);
                 }
               }
+              u32* th = LW2 ? thalf + (s & 1) * 2 * HALF : thalf;
 #pragma unroll
-              for (int d = 0; d < R; ++d) thalf[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
+              for (int d = 0; d < R; ++d) th[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
             }
           }
         }
         bsync();
-        // phase 2: 256 entries x 8 replicas
-        uint4* tb = tab + (s & 1) * R * TPL;
+        if constexpr (LW2) nbar_arrive(HALFB(s), NB);
+        // phase 2: 256 entries x 8 replicas.  A thread's entries g = bt + NBT it share the low
+        // half-table entry (NBT is a multiple of 16): it is read once.
+        uint4* tb = tab + (s & 1) * TR * TPL;
+        static_assert(NBT % 16 == 0, "phase 2 shares the low half entry across a thread's entries");
+        const u32* th2 = LW2 ? thalf + (s & 1) * 2 * HALF : thalf;
+        uint4 Lh[R];
+#pragma unroll
+        for (int d = 0; d < R; ++d) Lh[d] = reinterpret_cast<const uint4*>(th2)[(bt & ((1 << KLO) - 1)) + d * 16];
 #pragma unroll
         for (int it = 0; it < E / NBT; ++it) {
           const int g = bt + NBT * it;
-          const uint4* lo = reinterpret_cast<const uint4*>(thalf) + (g & ((1 << KLO) - 1));
-          const uint4* hi = reinterpret_cast<const uint4*>(thalf + HALF) + (g >> KLO);
+          const uint4* hi = reinterpret_cast<const uint4*>(th2 + HALF) + (g >> KLO);
           V<F> v[4], hv[4];
 #pragma unroll
           for (int d = 0; d < R; ++d) {
-            const uint4 L = lo[d * 16], H = hi[d * 16];
+            const uint4 L = Lh[d], H = hi[d * 16];
             v[0].p[d] = L.x; v[1].p[d] = L.y; v[2].p[d] = L.z; v[3].p[d] = L.w;
             hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
           }
@@ -623,6 +715,9 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 #pragma unroll
               for (int d = 0; d < R; ++d)
                 tb[d * TPL + g * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
+              if constexpr (KAR && !LW2)
+                tb[2 * TPL + g * (ENTRY_BYTES / 16) + copy] =
+                    make_uint4(v[0].p[0] ^ v[0].p[1], v[1].p[0] ^ v[1].p[1], v[2].p[0] ^ v[2].p[1], v[3].p[0] ^ v[3].p[1]);
             }
           }
         }
@@ -632,9 +727,27 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       return;
     }
     // ------------------------------------------------ lookup warps (ROLE 2)
+    // (LW2) plane 2 of block s's table: entry tid = T0 ^ T1 from the half tables, 8 replicas
+    auto plane2 = [&](int s) {
+      if constexpr (LW2) {
+        nbar_sync(HALFB(s), NB);
+        const uint4* th = reinterpret_cast<const uint4*>(thalf + (s & 1) * 2 * HALF);
+        const int g = tid;  // NT == E: one entry per lookup thread
+        const uint4 l0 = th[g & 15], l1 = th[16 + (g & 15)], h0 = th[2 * 16 + (g >> 4)], h1 = th[3 * 16 + (g >> 4)];
+        const uint4 v = make_uint4(l0.x ^ l1.x ^ h0.x ^ h1.x, l0.y ^ l1.y ^ h0.y ^ h1.y, l0.z ^ l1.z ^ h0.z ^ h1.z,
+                                   l0.w ^ l1.w ^ h0.w ^ h1.w);
+        uint4* tb = tab + (s & 1) * TR * TPL + 2 * TPL + g * (ENTRY_BYTES / 16);
+#pragma unroll
+        for (int cc = 0; cc < COPIES; ++cc) tb[(cc + g) & (COPIES - 1)] = v;
+      }
+    };
+    if constexpr (LW2) static_assert(NT == E && R == 2, "plane-2 split: one entry per lookup thread");
+    plane2(s_begin);
     for (int s = s_begin; s < s_end; ++s) {
       nbar_sync(FULL(s), NB);
-      lookups(s, s & 1, [](int) {});
+      lookups(s, s & 1, [&](int t) {
+        if (t == RT / 2 - 1 && s + 1 < s_end) plane2(s + 1);
+      });
       if (s + 2 < s_end) nbar_arrive(EMPTY(s), NB);
     }
   } else if constexpr (!PIPE) {
@@ -646,6 +759,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     }
     cp_async_wait<PD - 1>();
     __syncthreads();
+    SG_TL(1);
     for (int s = s_begin; s < s_end; ++s) {
       phase1(s);
       __syncthreads();
@@ -675,10 +789,11 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       V<F> v[4];
       phase2_compute(s_begin, v);
 #pragma unroll
-      for (int cc = 0; cc < CPT; ++cc) phase2_store(tab + (s_begin & 1) * R * TPL, v, cc);
+      for (int cc = 0; cc < CPT; ++cc) phase2_store(tab + (s_begin & 1) * TR * TPL, v, cc);
     }
     if (s_begin + 1 < s_end) phase1(s_begin + 1);
     __syncthreads();
+    SG_TL(1);
     for (int s = s_begin; s < s_end; ++s) {
       issue_b(s + PD);
       issue_a(s + PDA);
@@ -686,7 +801,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       const bool nxt = s + 1 < s_end;
       V<F> v[4];
       if (nxt) phase2_compute(s + 1, v);
-      uint4* tnext = tab + ((s + 1) & 1) * R * TPL;
+      uint4* tnext = tab + ((s + 1) & 1) * TR * TPL;
       // spread the next table's replica stores over the row-slot loop
       lookups(s, s & 1, [&](int t) {
         if (nxt) {
@@ -703,6 +818,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   }
 
   // ---- epilogue
+  SG_TL(2);
   if (mode == 2) {  // stream-K: compact slot [R][ROWS][4 words], canonical (summed by the reduce)
     u32* out = a.P2 + (int64_t)slot * R * ROWS * 4;
 #pragma unroll
@@ -748,12 +864,16 @@ template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE, bool STRM,
 __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB, unsigned char* smem,
                                              uint64_t* mbar) {
   constexpr int ROWS = RT * NT;
+  constexpr bool FUSED = std::is_same_v<AT, M4rmFusedArgs>;
   constexpr bool TMA_OK = SCHED == 2 && K == 8;
   if (!a.streamk) {
     const int s_begin = blockIdx.z * a.bps;
     m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE, STRM>(a, tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS,
-                                                 s_begin, min(a.nblocks, s_begin + a.bps), a.partial ? 1 : 0,
-                                                 blockIdx.z);
+                                                 s_begin, min(a.nblocks, s_begin + a.bps),
+                                                 // fused split-K: compact canonical slots [split][tile] (mode 2)
+                                                 a.partial ? (FUSED ? 2 : 1) : 0,
+                                                 FUSED ? (int)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x)
+                                                       : (int)blockIdx.z);
     return;
   }
   const int64_t U = a.units, G = gridDim.x;
@@ -786,18 +906,92 @@ __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB
   }
 }
 
-template <int F, int K, int RT, int SCHED, int NT, int ABL = 0, bool STRM = false>
-__global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
-    m4rm_kernel(const std::conditional_t<STRM, M4rmStreamArgs, M4rmArgs> a, const __grid_constant__ CUtensorMap tmB) {
+// Fused small products: the split-K reduction inside the product kernel.  Every CTA of the tile
+// (blockIdx.x, blockIdx.y) has written its partial plane blockIdx.z; they meet at the tile's
+// arrival counter (all co-resident: cooperative launch), then CTA z sums rows
+// [z ROWS / S, (z+1) ROWS / S) of the tile over the S partials (L2 loads), canonicalizes them
+// into Cout, and the last CTA to leave resets the tile's counters for the next launch.
+template <int F, int ROWS>
+__device__ __forceinline__ void fused_reduce(const M4rmFusedArgs& a) {
+  constexpr int R = Traits<F>::R;
+  const unsigned S = gridDim.z;
+  const int ntiles = gridDim.x * gridDim.y;
+  const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+  unsigned* arrive = a.cnt + tile;
+  unsigned* depart = a.cnt + a.ntiles + tile;
+  __threadfence();  // this thread's partial stores, before the CTA's arrival
+  __syncthreads();
+  SG_TL(3);
+  if (threadIdx.x == 0) {
+    atomicAdd(arrive, 1u);
+    unsigned v;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(arrive) : "memory");
+      if (v >= S) break;
+      __nanosleep(32);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 4000000000ull) __trap();  // 4 s: a split never arrived (cannot happen co-resident)
+    }
+  }
+  __syncthreads();
+  SG_TL(4);
+  // slots [split][tile][plane][ROWS][4 words]: thread = (row, word) of rows [r_lo, r_hi)
+  const int64_t row0 = (int64_t)blockIdx.y * ROWS;
+  const int word0 = blockIdx.x * SLAB_WORDS;
+  const int r_lo = (int)(blockIdx.z * ROWS / S), r_hi = (int)((blockIdx.z + 1) * ROWS / S);
+  const int64_t sstride = (int64_t)ntiles * R * ROWS * 4;  // one split's slots
+  const u32* base = a.P2 + (int64_t)tile * R * ROWS * 4;
+  for (int it = threadIdx.x; it < (r_hi - r_lo) * SLAB_WORDS; it += blockDim.x) {
+    const int lr = r_lo + it / SLAB_WORDS, w = it % SLAB_WORDS;
+    const int64_t row = row0 + lr;
+    const u32* p = base + lr * 4 + w;
+    V<F> acc = vzero<F>();
+    // eight splits' loads in flight before their adds (L2 latency, not bandwidth, bound)
+    for (unsigned s0 = 0; s0 < S; s0 += 8) {
+      V<F> x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int d = 0; d < R; ++d) x[j].p[d] = s0 + j < S ? __ldcg(p + (s0 + j) * sstride + d * ROWS * 4) : 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vadd<F>(acc, x[j]);  // zero is the additive identity of every encoding
+    }
+    vcanon<F>(acc);
+    if (row < a.m && word0 + w < a.wc32) {
+#pragma unroll
+      for (int d = 0; d < R; ++d) a.Cout[((int64_t)d * a.m + row) * a.wc32 + word0 + w] = acc.p[d];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(depart, 1u) == S - 1) {  // every split has read its rows
+    *arrive = 0u;
+    *depart = 0u;
+  }
+  SG_TL(5);
+}
+
+// fused small-product kernels with few accumulator registers run two CTAs per SM (more warps to
+// hide the per-k-block latency of a short split)
+template <int F, int RT, bool FUSED> __host__ __device__ constexpr int min_ctas_per_sm() {
+  return FUSED && RT * Traits<F>::RS * 4 <= 32 ? 2 : 1;
+}
+
+template <int F, int K, int RT, int SCHED, int NT, int ABL = 0, bool STRM = false, bool FUSED = false>
+__global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, RT, FUSED>()))
+    m4rm_kernel(const std::conditional_t<STRM, M4rmStreamArgs, std::conditional_t<FUSED, M4rmFusedArgs, M4rmArgs>> a,
+                const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ROWS = RT * NT;
+  SG_TL(0);
   if (a.early_trigger) pdl_trigger();
   // launched with PDL behind the index pre-pass: each schedule waits for it (pdl_wait) just
   // before its first read of A's index words, so the B staging overlaps the pre-pass's tail
   constexpr int R = Traits<F>::R;
-  constexpr int NSLOT = K == 8 ? 3 : 2;
-  constexpr int NAP = K == 8 ? 1 : R;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES +
+  constexpr int NSLOT = index_slots<F, K, FUSED>();
+  constexpr int NAP = packed_index<F, K, FUSED>() ? 1 : R;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES +
                                                (2 * 2 * 16 * R * 4 + 3 * K * R * 4 + NSLOT * NAP * ROWS) * 4);
   constexpr bool TMA_OK = SCHED == 2 && K == 8;
   if (TMA_OK && a.tma_b) {
@@ -823,16 +1017,19 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), 1)
     }
   } else {
     run_segments<F, K, RT, SCHED, NT, ABL, 0, STRM>(a, &tmB, smem, mbar);
+    if constexpr (FUSED) {
+      if (a.partial) fused_reduce<F, ROWS>(a);
+    }
   }
 }
 
 // ------------------------------------------------------------------ registry helpers
-template <int F, int K, int RT, int SCHED, int NT>
+template <int F, int K, int RT, int SCHED, int NT, bool FUSED = false>
 constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
-  constexpr int NSLOT = K == 8 ? 3 : 2;
-  constexpr int NAP = K == 8 ? 1 : R;
-  return (SCHED >= 1 ? 2 : 1) * R * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
+  constexpr int NSLOT = index_slots<F, K, FUSED>();
+  constexpr int NAP = packed_index<F, K, FUSED>() ? 1 : R;
+  return (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
          NSLOT * NAP * RT * NT * 4 + 6 * 8;  // + the B- and A-slot mbarriers
 }
 
@@ -845,9 +1042,13 @@ constexpr StreamKernelFn stream_variant() {
 
 #define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \
                                smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0, stream_variant<F, K, RT, P, NT>(), \
-                               smem_bytes_for<F, K, RT, P, NT>() + 2 * STRM_MAX_GROUPS}
+                               smem_bytes_for<F, K, RT, P, NT>() + 2 * STRM_MAX_GROUPS, nullptr}
 #define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (NT) + ws_builders(P), P, \
-                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr, 0}
+                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr, 0, nullptr}
+// fused small-product variants (k = 8, serial / pipelined; see M4rmFusedArgs)
+#define SG_KF(F, RT, P) {nullptr, F, 8, RT, 256, 256, P, smem_bytes_for<F, 8, RT, P, 256, true>(), 0, 0, 0, nullptr, 0, \
+                         m4rm_kernel<F, 8, RT, P, 256, 0, false, true>}
+#define SG_KFUSED(F) SG_KF(F, 1, 0), SG_KF(F, 2, 0), SG_KF(F, 4, 0), SG_KF(F, 2, 1), SG_KF(F, 4, 1)
 // k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
 #define SG_KSET8(F)                                                                                 \
   SG_K(F, 8, 1, 0, 256), SG_K(F, 8, 2, 0, 256), SG_K(F, 8, 4, 0, 256), SG_K(F, 8, 8, 0, 256), \

@@ -8,6 +8,7 @@ static KernelInfo g_table[] = {
     SG_K(Z4, 8, 16, 2, 256),
     SG_K(Z4, 8, 8, 2, 256),
     SG_KSET8(Z4),
+    SG_KFUSED(Z4),
     SG_KSET8_2PLANE(Z4),
     SG_KLOW(Z4),
 };

@@ -84,12 +84,38 @@ const Calib g_calib[] = {
     {4, 16, 256, 0, 3598, 26686},  // max err 1%, 12 runs
     {4, 16, 256, 1, 3547, 27403},  // max err 2%, 12 runs
     {4, 16, 256, 2, 3107, 27836},  // max err 3%, 12 runs
+    // fused one-launch variants (schedule + 10), from bench-style step times on small shapes
+    // (tools/step_probe.py --grid, profiles/r02n_step_grid.jsonl; fit: tools/fit_calib.py)
+    {1, 1, 256, 10, 1329, 0},  // max err 36%, 20 runs
+    {1, 2, 256, 10, 1666, 2563},  // max err 16%, 19 runs
+    {1, 2, 256, 11, 1661, 4742},  // max err 10%, 14 runs
+    {1, 4, 256, 10, 2051, 4472},  // max err 19%, 19 runs
+    {1, 4, 256, 11, 2264, 6335},  // max err 19%, 16 runs
+    {2, 1, 256, 10, 2492, 2328},  // max err 14%, 17 runs
+    {2, 2, 256, 10, 3004, 5534},  // max err 18%, 20 runs
+    {2, 2, 256, 11, 3011, 6862},  // max err 9%, 14 runs
+    {2, 4, 256, 10, 3893, 7254},  // max err 12%, 16 runs
+    {2, 4, 256, 11, 3797, 8881},  // max err 20%, 16 runs
+    {3, 1, 256, 10, 2466, 1696},  // max err 12%, 17 runs
+    {3, 2, 256, 10, 3033, 5415},  // max err 19%, 20 runs
+    {3, 2, 256, 11, 3054, 6702},  // max err 9%, 14 runs
+    {3, 4, 256, 10, 3729, 7411},  // max err 11%, 16 runs
+    {3, 4, 256, 11, 3778, 9369},  // max err 19%, 16 runs
+    {4, 1, 256, 10, 1682, 2093},  // max err 9%, 17 runs
+    {4, 2, 256, 10, 1886, 2951},  // max err 14%, 19 runs
+    {4, 2, 256, 11, 1903, 5482},  // max err 9%, 14 runs
+    {4, 4, 256, 10, 2248, 4848},  // max err 12%, 16 runs
+    {4, 4, 256, 11, 2386, 7073},  // max err 18%, 17 runs
 };
 
 const Calib* calib_for(const KernelInfo* ki) {
   if (ki->k != 8) return nullptr;
+  const int sched = ki->sched + (ki->fn_fused ? SCHED_FUSED : 0);
   for (const Calib& c : g_calib)
-    if (c.field == ki->field && c.rt == ki->rt && c.threads == ki->threads && c.sched == ki->sched) return &c;
+    if (c.field == ki->field && c.rt == ki->rt && c.threads == ki->threads && c.sched == sched) return &c;
+  if (ki->fn_fused)  // uncalibrated fused variant: its unfused twin's constants
+    for (const Calib& c : g_calib)
+      if (c.field == ki->field && c.rt == ki->rt && c.threads == ki->threads && c.sched == ki->sched) return &c;
   return nullptr;
 }
 
@@ -141,13 +167,25 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
   double lane_alu, lane_smem, entry_alu;
   field_costs(field, &lane_alu, &lane_smem, &entry_alu);
   const int R = planes(field);
+  const bool small0 = K == 8 && (double)m * (double)l * (double)n <= 2.0e9;
   Plan best;
   best.est_clk = 1e300;
+  // pass 0: fused plans for small products only; pass 1 (no plan fits, e.g. > 65535 row groups):
+  // every variant
+  for (int pass = 0; pass < 2 && !best.ki; ++pass)
   for (int i = 0; i < m4rm_kernel_count(); ++i) {
+    // (pass 1: `small` equals the variant's own kind, so the size filter below keeps everything)
+    const bool small = pass == 0 ? small0 : m4rm_kernel_at(i)->fn_fused != nullptr;
     KernelInfo* ki = m4rm_kernel_at(i);
     if (ki->field != field || ki->k != K) continue;
     if (g_override_rt && ki->rt != g_override_rt) continue;
-    if (g_override_pipe >= 0 && ki->sched != g_override_pipe) continue;
+    const bool fused = ki->fn_fused != nullptr;
+    if (g_override_pipe >= 0 && ki->sched + (fused ? SCHED_FUSED : 0) != g_override_pipe) continue;
+    // Products up to ~2e9 mul-adds run the fused one-launch kernel, larger ones the unfused
+    // variants (bench-style steps, profiles/r02n_step_grid.jsonl: the best fused plan beat the best
+    // unfused one on every shape up to 1.07e9 mul-adds, by 10-40 %, and lost on every shape from
+    // 4.3e9 up).  A forced schedule (sg_set_plan_override) overrides the split.
+    if (g_override_pipe < 0 && fused != small) continue;
     if (g_override_threads && ki->threads != g_override_threads) continue;
     if (ki->ablation != g_ablation) continue;
     if (ki->occupancy < 1) continue;  // does not fit this device
@@ -165,7 +203,7 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
     const int max_splits = std::max(1, std::min(nblocks, 64));
     const int64_t tiles = slabs * rgroups;
     const int64_t units = tiles * nblocks;
-    {
+    if (!fused) {
       // stream-K candidate: one wave of SMs x occupancy CTAs, each owning U / G consecutive
       // (tile, k-block) units, then a compact reduction of the partially covered tiles
       const int64_t G = (int64_t)ds.sms * occ;
@@ -208,15 +246,20 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       if (splits != sp) continue;
       if (rgroups > 65535 || splits > 65535) continue;  // grid.y / grid.z limits (stream-K has none)
       const double ctas = (double)slabs * rgroups * splits;
+      // a fused plan's split-K CTAs meet in the kernel: all of them co-resident (one wave)
+      if (fused && splits > 1 && ctas > (double)ds.sms * occ) continue;
       // calibrated variants: measured per-block and per-CTA clocks; others: the analytic
       // model with a 25 % penalty, so a measured variant wins unless clearly worse
+      // (fused variants use their unfused twin's calibration)
       const double t_cta = cal ? bps * cal->blk + cal->cta : 1.25 * (bps * t_block + 3000.0);
       const double waves = std::ceil(ctas / (ds.sms * occ));
       double est = waves * t_cta * std::min<double>(occ, ctas / ds.sms > 1 ? occ : 1);
       if (splits > 1) {
         const double bytes = (splits + 1.0) * R * (double)m * wc32 * 4.0;
-        est += bytes / 3000.0 + 8000.0;  // ~3 KB/clk HBM + one extra launch
+        // ~3 KB/clk HBM + one extra launch (fused: the meeting inside the kernel instead)
+        est += bytes / 3000.0 + (fused ? 1500.0 : 8000.0);
       }
+      if (fused) est -= 6000.0;  // no index pre-pass launch
       if (est < best.est_clk) {
         best.est_clk = est;
         best.ki = ki;
@@ -236,7 +279,10 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
   best.nblocks = nblocks;
   best.wa32 = (int)wa32;
   best.wc32 = (int)wc32;
-  if (K == 8) {
+  if (best.ki->fn_fused) {  // A's words are staged by the kernel itself
+    best.at_words = 0;
+    best.at_planes = 0;
+  } else if (K == 8) {
     const int rpw = field == SG_F2 ? 4 : planes(field) == 3 ? 1 : 2;
     best.at_words = (nblocks + rpw - 1) / rpw;
     best.at_planes = 1;
@@ -276,6 +322,8 @@ int64_t workspace_bytes_for(const Plan& p, int field) {
   int64_t b = (int64_t)p.at_planes * p.at_words * p.mpad * 4;
   b = (b + 255) / 256 * 256;
   if (p.streamk) b += (int64_t)p.grid.x * SK_SLOTS * R * p.rows * SLAB_WORDS * 4;
+  else if (p.splits > 1 && p.ki->fn_fused)  // compact slots [split][tile][R][rows][4 words]
+    b += (int64_t)p.splits * R * p.mpad * ((p.wc32 + SLAB_WORDS - 1) / SLAB_WORDS) * SLAB_WORDS * 4;
   else if (p.splits > 1) b += (int64_t)p.splits * R * p.mpad * p.wc32 * 4;
   return std::max<int64_t>(b, 256);
 }

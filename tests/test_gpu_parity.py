@@ -143,6 +143,45 @@ def test_every_compiled_plan(fname):  # noqa: F811
 
 
 @pytest.mark.parametrize("fname", list(FIELDS))
+def test_fused_small_plans(fname):
+    """The fused one-launch variants (A's words staged by the kernel, split-K summed inside it at
+    per-tile arrival counters): every rows-per-thread variant, both schedules, split counts up to
+    the co-resident limit, ragged shapes; repeated calls (the counters must come back to zero)
+    and a second stream (its own counters); bit-identical to the oracle."""
+    ran = 0
+    for (m, l, n) in [(700, 1001, 777), (700, 1001, 768), (1024, 1024, 1024), (1, 5, 3), (257, 64, 129),
+                      (100, 2000, 40)]:
+        A = oracle.random_dense(fname, m, l, m + 5)
+        B = oracle.random_dense(fname, l, n, n + 6)
+        want = expect(fname, A, B)
+        for rt in (1, 2, 4):
+            for pipe in (m4rm_mod.FUSED_SERIAL, m4rm_mod.FUSED_PIPELINED):
+                for splits in (1, 2, 5, 16, 37):
+                    m4rm_mod.set_plan_override(rt, splits, pipe, 256)
+                    try:
+                        p = m4rm_mod.plan(fname, m, l, n)
+                    except RuntimeError as e:
+                        assert "no compiled" in str(e)
+                        continue
+                    assert p["schedule"].startswith("fused")
+                    for _ in range(2):
+                        C = gpu_multiply(fname, A, B)
+                        assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, rt, pipe, splits)
+                    ran += 1
+        s2 = torch.cuda.Stream()
+        with torch.cuda.stream(s2):
+            m4rm_mod.set_plan_override(4, 5, m4rm_mod.FUSED_PIPELINED, 256)
+            try:
+                C = gpu_multiply(fname, A, B)
+                s2.synchronize()
+                assert np.array_equal(C.planes_numpy(), want)
+            except RuntimeError as e:
+                assert "no compiled" in str(e)
+    m4rm_mod.set_plan_override()
+    assert ran >= 30
+
+
+@pytest.mark.parametrize("fname", list(FIELDS))
 def test_streamk_forced(fname):
     """Stream-K (splits = -1): CTA ranges that start and end mid-tile, span several whole tiles
     (written straight to C) or lie inside one tile, every schedule and CTA shape, ragged m / l / n;

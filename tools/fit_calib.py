@@ -10,8 +10,10 @@ row groups = ceil(m / rows), k-blocks nb = ceil(l / 8), and SMs = 148,
             nseg = min(2, per) + floor(per / nb) segments per CTA,
             G = SMs * occ, U = slabs * row groups * nb
 plus FIX = 20000 clocks per product (pre-pass, launches; the same for every variant, so it does not
-steer the planner).  T in SM clocks at 1965 MHz; (blk, cta) by least squares on the relative error."""
+steer the planner).  Fused variants (pipe 10 / 11, one launch): no pre-pass (FIX - 6000) and the
+split-K meeting inside the kernel (1500 instead of a reduction launch's 8000).  T in SM clocks at 1965 MHz; (blk, cta) by least squares on the relative error."""
 FIX = 20000.0
+FUSED_CREDIT = 6000.0  # fused variants (pipe 10 / 11): one launch instead of pre-pass + product (+ reduce)
 import json
 import math
 import sys
@@ -56,7 +58,11 @@ for key in sorted(groups, key=lambda k: (CODE[k[0]], k[1], k[2], k[3])):
             waves = math.ceil(ctas / (SMS * occ))
             mult = occ if ctas / SMS > 1 else 1
             x, y = waves * mult * bps, waves * mult
-            red = ((spl + 1) * R[field] * m * wc32 * 4 / 3000 + 8000) if spl > 1 else 0.0
+            if pipe >= 10:  # fused: the split-K meeting inside the kernel, no pre-pass launch
+                red = ((spl + 1) * R[field] * m * wc32 * 4 / 3000 + 1500) if spl > 1 else 0.0
+                red -= FUSED_CREDIT
+            else:
+                red = ((spl + 1) * R[field] * m * wc32 * 4 / 3000 + 8000) if spl > 1 else 0.0
         red += FIX
         rows_x.append([x / T, y / T])
         rhs.append((T - red) / T)

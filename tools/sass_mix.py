@@ -32,7 +32,9 @@ def mix_of(fname, ins, field_code, rt, sched, nt):
         c = Counter(opcode(t).split(".")[0] for t in body)
         # the lookup loop: RT row-slots of NI x R table loads, with the field arithmetic; in the
         # warp-specialized schedule it holds no table stores (those are the builder warps')
-        if c["LDS"] >= rt * NI * R and c["LOP3"] >= rt and (sched != 2 or c["STS"] == 0):
+        # (GF(4), k = 8: Karatsuba tables, three one-plane lookups per row)
+        nl = 3 if name == "gf4" else NI * R
+        if c["LDS"] >= rt * nl and c["LOP3"] >= rt and (sched != 2 or c["STS"] == 0):
             best = (a, b, c)
             break  # loops() is sorted by size: the smallest qualifying loop
     if best is None:
@@ -59,7 +61,8 @@ def main():
         if not os.path.exists(obj):
             continue
         for fname, ins in functions(obj):
-            m = re.search(rf"m4rm_kernelILi{code}ELi8ELi(\d+)ELi(\d)ELi(\d+)ELi0ELb0E", fname)
+            # the resident-B, unfused instantiations (STRM = FUSED = false)
+            m = re.search(rf"m4rm_kernelILi{code}ELi8ELi(\d+)ELi(\d)ELi(\d+)ELi0ELb0ELb0E", fname)
             if not m:
                 continue
             rt, sched, nt = (int(x) for x in m.groups())

@@ -14,14 +14,16 @@ from paper_0901_1413_b200 import m4rm as M  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="f3:1024:1024:1024")
+ap.add_argument("--fused-only", action="store_true")
 a = ap.parse_args()
 fld, m, l, n = a.shape.split(":")
 m, l, n = int(m), int(l), int(n)
 dev = torch.device("cuda", 0)
 f, A, B = bench.make_inputs(fld, m, l, n, 0, dev, True)
 C = sg.BitslicedMatrix.zero(f, m, n, device=dev)
-plans = [(0, 0, -1, 0)] + [(rt, sp, pipe, nt) for rt in (1, 2, 4, 8) for nt in (256,) for pipe in (0, 1, 2)
-                           for sp in (4, 8, 16, 32, -1)]
+pipes = (10, 11) if a.fused_only else (0, 1, 2, 10, 11)
+plans = [(0, 0, -1, 0)] + [(rt, sp, pipe, nt) for rt in (1, 2, 4, 8) for nt in (256,) for pipe in pipes
+                           for sp in (4, 8, 16, 18, 32, 37, -1)]
 for ov in plans:
     M.set_plan_override(*ov)
     try:

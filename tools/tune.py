@@ -19,6 +19,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--shapes", default="", help="extra field:m:l:n shapes")
 ap.add_argument("--rts", default="1,2,4,8,16")
 ap.add_argument("--splits", default="-1,1,2,4,8,16")  # -1 = stream-K
+ap.add_argument("--pipes", default="0,1,2")  # schedules; 10 / 11 = fused serial / pipelined
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 KINFO = M.kernel_info(0)
@@ -38,7 +39,7 @@ for name, field, m, l, n in jobs:
     best = None
     for rt in [int(x) for x in a.rts.split(",")]:
         for nt in (256, 512):
-            for pipe in (0, 1, 2):
+            for pipe in [int(x) for x in a.pipes.split(",")]:
                 for sp in [int(x) for x in a.splits.split(",")]:
                     M.set_plan_override(rt, sp, pipe, nt)
                     try:
