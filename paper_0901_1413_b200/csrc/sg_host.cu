@@ -8,6 +8,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -32,6 +33,12 @@ struct Io {
   cudaEvent_t ev_chunk[64];
   std::map<int, bool> preloaded;  // fields whose auxiliary kernels are loaded
   int stream_ops = 0;  // cuStreamWriteValue32 on this device: 0 untested, 1 works, -1 unsupported
+  // small calls (sg_m4rm_host's one-stream path) repeated on the same buffers replay a CUDA
+  // graph of (H2D A, H2D B, product, D2H C): one launch instead of four plus the planner.
+  // Keyed on everything the captured work depends on; dropped when the staging buffer moves.
+  typedef std::tuple<int, const void*, const void*, void*, int64_t, int64_t, int64_t, int, std::vector<int>> GraphKey;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int> graph_seen;  // calls so far (the first runs uncaptured: it allocates)
 };
 
 // After a failed call, wait for every copy already queued on the device's pipeline streams: the
@@ -340,12 +347,20 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
         cudaDeviceSynchronize();
         cudaFree(d->buf.p);
       }
+      for (auto& g : d->graphs) cudaGraphExecDestroy(g.second);  // they captured the old buffer
+      d->graphs.clear();
+      d->graph_seen.clear();
       d->buf.p = nullptr;
       d->buf.bytes = 0;
       SG_CUDA(cudaMalloc(&d->buf.p, need), "sg_m4rm_host alloc");
       d->buf.bytes = need;
     }
     dbuf = (char*)d->buf.p;
+  }
+  const char* stream_e = getenv("SG_HOST_STREAM");  // experiments: 0 = upload B before the products
+  if ((!stream_e || atoi(stream_e) != 0) && Pk == 1 && Pc == 1 && l > 0 && Pr <= 4) {
+    rc = host_streamed(d, dbuf, field, A, B, C, m, l, n, k, device, Pr);
+    if (rc != SG_EUNSUPPORTED) return rc;
   }
   // (an explicit SG_HOST_CHUNKS / SG_HOST_KCHUNKS request, experiments and tests, runs the pipelines)
   if (Pk == 1 && Pr == 1 && Pc == 1 && !getenv("SG_HOST_NOSMALL") && !getenv("SG_HOST_CHUNKS") &&
@@ -360,18 +375,69 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
     q += up(b_bytes);
     uint64_t* dC = (uint64_t*)q;
     cudaStream_t st = d->comp;
-    if (a_bytes) SG_CUDA(cudaMemcpyAsync(dA, A, a_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D A");
-    if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D B");
-    rc = sg_m4rm(field, dA, dB, dC, m, l, n, k, nullptr, 0, st);
-    if (rc != SG_OK) return rc;
-    SG_CUDA(cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st), "sg_m4rm_host D2H C");
+    auto enqueue = [&]() -> int {
+      if (a_bytes) SG_CUDA(cudaMemcpyAsync(dA, A, a_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D A");
+      if (b_bytes) SG_CUDA(cudaMemcpyAsync(dB, B, b_bytes, cudaMemcpyHostToDevice, st), "sg_m4rm_host H2D B");
+      int r = sg_m4rm(field, dA, dB, dC, m, l, n, k, nullptr, 0, st);
+      if (r != SG_OK) return r;
+      SG_CUDA(cudaMemcpyAsync(C, dC, c_bytes, cudaMemcpyDeviceToHost, st), "sg_m4rm_host D2H C");
+      return SG_OK;
+    };
+    // graph replay of a repeated call: page-locked host buffers only (a pageable copy is staged
+    // by the driver at call time), not under per-launch timing (experiments), SG_HOST_GRAPH=0 off
+    cudaPointerAttributes pa, pb, pc;
+    const bool pinned = cudaPointerGetAttributes(&pa, A) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        cudaPointerGetAttributes(&pb, B) == cudaSuccess && pb.type == cudaMemoryTypeHost &&
+                        cudaPointerGetAttributes(&pc, C) == cudaSuccess && pc.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    static const bool graphs_on = [] {
+      const char* e = getenv("SG_HOST_GRAPH");
+      return !e || atoi(e) != 0;
+    }();
+    if (!pinned || !graphs_on || g_timing) {
+      if ((rc = enqueue()) != SG_OK) return rc;
+      SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
+      return SG_OK;
+    }
+    Io::GraphKey key;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);  // the plan depends on the overrides and the SM reserve
+      key = Io::GraphKey{field, A, B, C, m, l, n, k,
+                         {g_override_rt, g_override_splits, g_override_pipe, g_override_threads, g_ablation,
+                          g_sm_reserve}};
+    }
+    auto it = d->graphs.find(key);
+    if (it == d->graphs.end()) {
+      if (d->graph_seen[key]++ == 0) {  // first call: uncaptured (plans, workspaces, counters)
+        if ((rc = enqueue()) != SG_OK) return rc;
+        SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
+        return SG_OK;
+      }
+      cudaGraphExec_t ex = nullptr;
+      if (d->graph_seen[key] == 2) {  // second call: capture (once; a failed capture is not retried)
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+          const int r = enqueue();
+          const cudaError_t ce = cudaStreamEndCapture(st, &g);
+          if (r != SG_OK || ce != cudaSuccess || cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) ex = nullptr;
+          if (g) cudaGraphDestroy(g);
+        }
+        cudaGetLastError();
+      }
+      if (!ex) {  // no graph for this call: the plain one-stream path
+        if ((rc = enqueue()) != SG_OK) return rc;
+        SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
+        return SG_OK;
+      }
+      if (d->graphs.size() >= 64) {
+        for (auto& x : d->graphs) cudaGraphExecDestroy(x.second);
+        d->graphs.clear();
+      }
+      it = d->graphs.emplace(key, ex).first;
+    }
+    SG_CUDA(cudaGraphLaunch(it->second, st), "sg_m4rm_host graph launch");
     SG_CUDA(cudaStreamSynchronize(st), "sg_m4rm_host sync");
     return SG_OK;
-  }
-  const char* stream_e = getenv("SG_HOST_STREAM");  // experiments: 0 = upload B before the products
-  if ((!stream_e || atoi(stream_e) != 0) && Pk == 1 && Pc == 1 && l > 0 && Pr <= 4) {
-    rc = host_streamed(d, dbuf, field, A, B, C, m, l, n, k, device, Pr);
-    if (rc != SG_EUNSUPPORTED) return rc;
   }
   if (Pc > 1) {
     // ---- Pr x Pc grid: uploads in order of first use, products row-major, pieces down as done

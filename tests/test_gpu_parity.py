@@ -268,6 +268,31 @@ def test_host_buffers_e2e_path():
         assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
 
 
+def test_host_small_calls_replay():
+    """Small host-buffer products (C < 1 MB) run on one stream, and a call repeated on the same
+    page-locked buffers replays a captured CUDA graph (from the third call on): the graph must
+    re-read the caller's buffers on every replay (new contents, same addresses) and a changed
+    plan override must not reuse a graph captured under another plan."""
+    for fname in ("f3", "f5", "gf4", "f7"):
+        m, l, n = 300, 520, 200
+        f = FIELDS[fname]
+        Ap = torch.empty((f.bits, m, (l + 63) // 64), dtype=torch.int64).pin_memory()
+        Bp = torch.empty((f.bits, l, (n + 63) // 64), dtype=torch.int64).pin_memory()
+        Cp = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64).pin_memory()
+        A_, B_, C_ = sg.BitslicedMatrix(f, m, l, Ap), sg.BitslicedMatrix(f, l, n, Bp), sg.BitslicedMatrix(f, m, n, Cp)
+        for i in range(5):
+            if i == 3:
+                m4rm_mod.set_plan_override(2, 4, m4rm_mod.FUSED_PIPELINED, 256)
+            A = oracle.random_dense(fname, m, l, 40 + i)
+            B = oracle.random_dense(fname, l, n, 50 + i)
+            Ap.copy_(torch.from_numpy(oracle.pack(fname, A).view(np.int64)))
+            Bp.copy_(torch.from_numpy(oracle.pack(fname, B).view(np.int64)))
+            Cp.fill_(-1)
+            C = sg.m4rm_multiply(A_, B_, sg.M4rmParams(8), out=C_)
+            assert C is C_ and np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, i)
+        m4rm_mod.set_plan_override()
+
+
 def test_host_buffers_pipelined_chunks():
     """sg_m4rm_host's pipeline: the default chunking at m >= 4096, and every (k-chunks, row
     pieces) pair forced through SG_HOST_KCHUNKS / SG_HOST_CHUNKS on ragged shapes."""
