@@ -243,7 +243,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
   if (g_timing)
     for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
   if (g_timing) cudaEventRecord(ev[0], st);
-  SG_CUDA(launch_transpose_a(field, p.K, (const uint32_t*)A, AT, m, p.mpad, p.wa32, p.at_words, st),
+  SG_CUDA(launch_transpose_a(field, p.K, (const uint32_t*)A, AT, m, p.mpad, p.wa32, p.at_words, p.ki->pair_nt, st),
           "sg_m4rm index pre-pass");
   g_launches++;
   if (g_timing) cudaEventRecord(ev[1], st);

@@ -118,6 +118,7 @@ struct KernelInfo {
   StreamKernelFn fn_stream;  // the same variant reading streamed B (M4rmStreamArgs), or nullptr
   int smem_stream;           // ... and its dynamic shared memory (+ the staged group order)
   FusedKernelFn fn_fused;    // a fused small-product variant (fn == nullptr then), see M4rmFusedArgs
+  int pair_nt;               // k = 8 index records two rows per word (rows r, r + pair_nt), or 0
 };
 // streamed products stage their tile's group order in shared memory: at most this many groups
 constexpr int STRM_MAX_GROUPS = 2048;
@@ -128,7 +129,7 @@ KernelInfo* m4rm_kernel_at(int i);
 
 // k = 8: packed index words [nwords][mpad]; k < 8: A^T bit planes [R][wa32][mpad]
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
-                               int wa32, int nwords, cudaStream_t st);
+                               int wa32, int nwords, int pair_nt, cudaStream_t st);
 cudaError_t launch_m4rm(const KernelInfo& ki, const M4rmArgs& a, const CUtensorMap& tmB, dim3 grid,
                         cudaStream_t st);
 cudaError_t launch_m4rm_streamed(const KernelInfo& ki, const M4rmStreamArgs& a, const CUtensorMap& tmB, dim3 grid,

@@ -94,6 +94,56 @@ __global__ void index_words_kernel(const u32* __restrict__ A, u32* __restrict__ 
   }
 }
 
+// Two-row records (paired_index, sg_m4rm_kernel.cuh): IW [nblocks][mpad / 2], word
+// (g NT + j) of k-block s = the 2-byte records of rows g 2NT + j (low half) and g 2NT + NT + j
+// (high half).  A block stages a 32-word x 32-row tile of each plane for both rows of 32 pairs.
+template <int F>
+__global__ void index_pairs_kernel(const u32* __restrict__ A, u32* __restrict__ IW, int64_t m, int64_t mpad,
+                                   int wa32, int nblocks, int nt) {
+  constexpr int R = Traits<F>::R;
+  __shared__ u32 tile[2][R][32][33];
+  pdl_trigger();  // the product kernel may launch now; it waits for this grid before reading IW
+  const int wbase = blockIdx.x * 32;  // A words wbase.. (= k-blocks 4*wbase ..)
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t half = mpad / 2;
+  const int per_group = nt / 32;      // 32-pair tiles per 2 NT-row group
+  for (int64_t pt = blockIdx.y; pt < half / 32; pt += gridDim.y) {
+    const int64_t g = pt / per_group;
+    const int64_t lo0 = g * 2 * nt + (pt % per_group) * 32;  // first low row; high rows + nt
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int d = 0; d < R; ++d)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = lo0 + h * nt + ty + 8 * i;
+          const int w = wbase + tx;
+          tile[h][d][ty + 8 * i][tx] = (row < m && w < wa32) ? A[((int64_t)d * m + row) * wa32 + w] : 0u;
+        }
+    __syncthreads();
+    for (int sl = ty; sl < 128; sl += 8) {
+      const int s = wbase * 4 + sl;
+      if (s >= nblocks) continue;
+      const int aw = sl >> 2, sh = 8 * (sl & 3);
+      u32 v = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        u32 b0, b1;
+        if constexpr (F == F3) {  // "+1" index from A0 ^ A1, "-1" from A1 (fields.py:98-99)
+          b0 = (tile[h][0][tx][aw] ^ tile[h][1][tx][aw]) >> sh;
+          b1 = tile[h][1][tx][aw] >> sh;
+        } else {
+          b0 = tile[h][0][tx][aw] >> sh;
+          b1 = tile[h][1][tx][aw] >> sh;
+        }
+        v |= ((b0 & 0xFFu) | (b1 & 0xFFu) << 8) << (16 * h);
+      }
+      IW[(int64_t)s * half + g * nt + (pt % per_group) * 32 + tx] = v;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ split-K reduction
 __device__ __forceinline__ u32 comp4(const uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
 __device__ __forceinline__ void set4(uint4& v, int w, u32 x) {
@@ -378,7 +428,17 @@ cudaError_t launch_m4rm_fused(const KernelInfo& ki, const M4rmFusedArgs& a, cons
 }
 
 cudaError_t launch_transpose_a(int field, int k, const uint32_t* A, uint32_t* AT, int64_t m, int64_t mpad,
-                               int wa32, int nwords, cudaStream_t st) {
+                               int wa32, int nwords, int pair_nt, cudaStream_t st) {
+  if (k == 8 && pair_nt) {
+    const int nblocks = (int)std::min<int64_t>((int64_t)nwords * 2, ((int64_t)wa32 * 32 + 7) / 8);
+    dim3 grid((wa32 + 31) / 32, (unsigned)std::min<int64_t>(std::max<int64_t>(1, mpad / 64), 65535), 1);
+    // (two-index fields only: F3, GF(4), Z4)
+    if (field == F3) index_pairs_kernel<F3><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nblocks, pair_nt);
+    else if (field == GF4) index_pairs_kernel<GF4><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nblocks, pair_nt);
+    else if (field == Z4) index_pairs_kernel<Z4><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nblocks, pair_nt);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+  }
   if (k == 8) {
     dim3 grid((wa32 + 31) / 32, (unsigned)std::min<int64_t>((mpad + 31) / 32, 65535), 1);
 #define SG_IW(FF) index_words_kernel<FF><<<grid, dim3(32, 8), 0, st>>>(A, AT, m, mpad, wa32, nwords)
@@ -404,6 +464,9 @@ cudaError_t preload_aux_kernels(int field) {
   SG_FOR_EACH_FIELD_CASE(field, SG_PL)
 #undef SG_PL
   cudaFuncGetAttributes(&fa, transpose_a_kernel);
+  if (field == F3) cudaFuncGetAttributes(&fa, index_pairs_kernel<F3>);
+  if (field == GF4) cudaFuncGetAttributes(&fa, index_pairs_kernel<GF4>);
+  if (field == Z4) cudaFuncGetAttributes(&fa, index_pairs_kernel<Z4>);
   return cudaGetLastError();
 }
 

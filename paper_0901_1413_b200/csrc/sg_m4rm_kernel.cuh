@@ -166,12 +166,24 @@ template <int F, int K> __host__ __device__ constexpr bool karatsuba() { return 
 template <int F, int K> __host__ __device__ constexpr int table_planes() { return karatsuba<F, K>() ? 3 : Traits<F>::R; }
 // staging slots of A's index words: Karatsuba GF(4) needs the room of the third table plane, and
 // with two k-blocks per index word two slots are enough (see issue_a)
-template <int F, int K, bool FUSED = false> __host__ __device__ constexpr int index_slots() {
-  return K == 8 && !FUSED ? (karatsuba<F, K>() ? 2 : 3) : 2;
-}
 // staged index source: k = 8 packed records from the pre-pass (one plane), else R planes of A
 // words (A^T from the transpose pre-pass, or A itself in the fused small-product kernels)
 template <int F, int K, bool FUSED = false> __host__ __device__ constexpr bool packed_index() { return K == 8 && !FUSED; }
+// k = 8 records of two-index fields (F3, GF(4), Z4: 2 bytes per row and k-block) are packed two
+// ROWS per 32-bit word -- rows r and r + NT of each 2 NT-row group, one k-block -- when the
+// variant's row-slots come in pairs (RT even): a lane's LDS.32 then serves two of its rows, half
+// the index wavefronts of one row per word (the pre-pass writes [k-block][mpad / 2] words).
+template <int F, int K, int RT, bool FUSED = false> __host__ __device__ constexpr bool paired_index() {
+  return packed_index<F, K, FUSED>() && Traits<F>::NI == 2 && RT % 2 == 0;
+}
+template <int F, int K, int RT, bool FUSED = false> __host__ __device__ constexpr int index_slots() {
+  return paired_index<F, K, RT, FUSED>() ? 3 : K == 8 && !FUSED ? (karatsuba<F, K>() ? 2 : 3) : 2;
+}
+// u32 of shared memory staging A's index words / planes (NSLOT slots)
+template <int F, int K, int RT, int NT, bool FUSED = false> __host__ __device__ constexpr int index_stage_words() {
+  return index_slots<F, K, RT, FUSED>() * (packed_index<F, K, FUSED>() ? 1 : Traits<F>::R) *
+         (paired_index<F, K, RT, FUSED>() ? RT * NT / 2 : RT * NT);
+}
 
 // Row accumulator of one lane: 4 words x RS planes.
 template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
@@ -341,7 +353,10 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   constexpr int NI = Traits<F>::NI;
   constexpr int NIP = NI == 3 ? 4 : NI;
   constexpr int RPW = 4 / NIP;
-  constexpr int NSLOT = index_slots<F, K, FUSED>();  // A words in use + blocks in flight
+  constexpr bool PAIR = paired_index<F, K, RT, FUSED>();  // two rows per record word (see there)
+  constexpr int BPU = PAIR ? 1 : RPW;      // (IW) k-blocks per staged unit of index words
+  constexpr int ASZ = PAIR ? ROWS / 2 : ROWS;  // u32 per staged unit and plane
+  constexpr int NSLOT = index_slots<F, K, RT, FUSED>();  // A words in use + blocks in flight
   constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
   constexpr int TPE_RAW = NT / E;
   constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
@@ -350,8 +365,8 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][TR][E][COPIES] uint4
   u32* thalf = reinterpret_cast<u32*>(smem + NTAB * TR * TPLANE);  // [2 buf][2 half][R][16][4]
   u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
-  u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ROWS]
-  uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ROWS);  // [3] B-slot barriers
+  u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ASZ]
+  uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ASZ);  // [3] B-slot barriers
   uint64_t* mbar_a = mbar_b + 3;                                               // [3] A-slot barriers
   // STRM only: this segment's tile's group order, staged by the builder warps ([ngroups] u16)
   unsigned short* perm_s = reinterpret_cast<unsigned short*>(mbar_a + 3);
@@ -364,7 +379,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   const bool tma_b = TMA_OK && a.tma_b;
   const bool tma_a = tma_b && a.tma_a;
 
-  int next_word = IW ? s_begin / RPW : (s_begin * K) >> 5;
+  int next_word = IW ? s_begin / BPU : (s_begin * K) >> 5;
   // Streamed products (a.perm, k = 8 only): virtual k-block s of this tile is real block
   // real_block(s); the 4-block groups are permuted, blocks inside a group keep their order, so
   // an index record word (RPW blocks) maps to one real record word.  Staging slots, barrier
@@ -380,7 +395,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   int ready_groups = 0;
   auto real_word = [&](int w) -> int {
     if constexpr (!STRM || !IW) return w;
-    return real_block(w * RPW) / RPW;
+    return real_block(w * BPU) / BPU;
   };
   // Stage block s's B rows (K x R x 16 B) into bst[s % 3].
   auto issue_b = [&](int s, int t0 = -1, int nthr = NT) {
@@ -423,12 +438,13 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       if (tma_a) {
         // TMA: the CTA's ROWS index records of each new word as ONE 1-D bulk copy
         if (s < s_end) {
-          for (const int whi = s / RPW; next_word <= whi; ++next_word) {
+          for (const int whi = s / BPU; next_word <= whi; ++next_word) {
             if (t0 == 0) {
               const int sl = next_word % NSLOT;
-              mbar_expect_tx(&mbar_a[sl], ROWS * 4);
-              tma_load_1d(ast + sl * ROWS, a.AT + (int64_t)real_word(next_word) * a.mpad + row0, ROWS * 4,
-                         &mbar_a[sl]);
+              mbar_expect_tx(&mbar_a[sl], ASZ * 4);
+              tma_load_1d(ast + sl * ASZ, a.AT + (int64_t)real_word(next_word) * (PAIR ? a.mpad / 2 : a.mpad) +
+                                             (PAIR ? row0 / 2 : row0),
+                          ASZ * 4, &mbar_a[sl]);
             }
           }
         }
@@ -436,10 +452,10 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       }
     }
     if (s < s_end) {
-      const int whi = IW ? s / RPW : (s * K + K - 1) >> 5;
+      const int whi = IW ? s / BPU : (s * K + K - 1) >> 5;
       for (; next_word <= whi; ++next_word) {
-        u32* adst = ast + (next_word % NSLOT) * NAP * ROWS;
-        const bool ok = next_word < a.wa32;
+        u32* adst = ast + (next_word % NSLOT) * NAP * ASZ;
+        const bool ok = next_word < (PAIR ? a.nblocks : a.wa32);
         const int rw = real_word(next_word);
         if constexpr (FUSED) {
           // A's own plane words, one per (plane, row): [slot][plane][row] like A^T
@@ -448,6 +464,13 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
             const bool ok2 = ok && row0 + r < a.m;
             const u32* src = ok2 ? a.A + ((int64_t)d * a.m + row0 + r) * a.wa32 + rw : a.A;
             cp_async4(adst + d * ROWS + r, src, ok2 ? 4 : 0);
+          }
+          continue;
+        }
+        if constexpr (PAIR) {
+          for (int q = t0; q < ASZ / 4; q += nthr) {
+            const u32* src = ok ? a.AT + (int64_t)rw * (a.mpad / 2) + row0 / 2 + 4 * q : a.AT;
+            cp_async16(adst + 4 * q, src, ok ? 16 : 0);
           }
           continue;
         }
@@ -470,7 +493,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // ... and block s's index word (slot w % NSLOT, used once per NSLOT words of the segment)
   auto wait_a = [&](int s) {
     if (TMA_OK && tma_a) {
-      const int w = s / RPW, w0 = s_begin / RPW;
+      const int w = s / BPU, w0 = s_begin / BPU;
       mbar_wait(&mbar_a[w % NSLOT], (unsigned)(((w - w0) / NSLOT) & 1));
     }
   };
@@ -553,11 +576,19 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 
   const unsigned char* tl0 = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
 
-  // Byte offsets of row-slot t's table entries for block s.
+  // Byte offsets of row-slot t's table entries for block s.  PAIR: row-slots 2j and 2j+1 share
+  // one record word -- it is loaded for the even slot and kept in xw (the callers go through the
+  // slots in order, each slot right after the one before it).
+  u32 xw = 0u;
   auto entries = [&](int s, int t, u32 (&e)[3]) {
     const int lr = t * NT + tid;
     e[0] = e[1] = e[2] = 0u;
-    if constexpr (IW) {
+    if constexpr (PAIR) {
+      if ((t & 1) == 0) xw = ast[(s % NSLOT) * ASZ + (t >> 1) * NT + tid];
+      const int b0 = (t & 1) * NIP;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) e[i] = __byte_perm(xw, 0u, 0x4440u | (u32)(b0 + i)) * ENTRY_BYTES;
+    } else if constexpr (IW) {
       const u32 x = ast[((s / RPW) % NSLOT) * ROWS + lr];
       const int b0 = (s % RPW) * NIP;
 #pragma unroll
@@ -989,10 +1020,9 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
   // launched with PDL behind the index pre-pass: each schedule waits for it (pdl_wait) just
   // before its first read of A's index words, so the B staging overlaps the pre-pass's tail
   constexpr int R = Traits<F>::R;
-  constexpr int NSLOT = index_slots<F, K, FUSED>();
-  constexpr int NAP = packed_index<F, K, FUSED>() ? 1 : R;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES +
-                                               (2 * 2 * 16 * R * 4 + 3 * K * R * 4 + NSLOT * NAP * ROWS) * 4);
+                                               (2 * 2 * 16 * R * 4 + 3 * K * R * 4 +
+                                                index_stage_words<F, K, RT, NT, FUSED>()) * 4);
   constexpr bool TMA_OK = SCHED == 2 && K == 8;
   if (TMA_OK && a.tma_b) {
     if (threadIdx.x == 0) {
@@ -1027,10 +1057,8 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
 template <int F, int K, int RT, int SCHED, int NT, bool FUSED = false>
 constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
-  constexpr int NSLOT = index_slots<F, K, FUSED>();
-  constexpr int NAP = packed_index<F, K, FUSED>() ? 1 : R;
   return (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
-         NSLOT * NAP * RT * NT * 4 + 6 * 8;  // + the B- and A-slot mbarriers
+         index_stage_words<F, K, RT, NT, FUSED>() * 4 + 6 * 8;  // + the B- and A-slot mbarriers
 }
 
 // the streamed-B instantiation of a warp-specialized k = 8 variant (nullptr for the others)
@@ -1042,12 +1070,14 @@ constexpr StreamKernelFn stream_variant() {
 
 #define SG_K(F, K, RT, P, NT) {m4rm_kernel<F, K, RT, P, NT>, F, K, RT, NT, (NT) + ws_builders(P), P, \
                                smem_bytes_for<F, K, RT, P, NT>(), 0, 0, 0, stream_variant<F, K, RT, P, NT>(), \
-                               smem_bytes_for<F, K, RT, P, NT>() + 2 * STRM_MAX_GROUPS, nullptr}
+                               smem_bytes_for<F, K, RT, P, NT>() + 2 * STRM_MAX_GROUPS, nullptr, \
+                               paired_index<F, K, RT>() ? (NT) : 0}
 #define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (NT) + ws_builders(P), P, \
-                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr, 0, nullptr}
+                                   smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr, 0, nullptr, \
+                                   paired_index<F, K, RT>() ? (NT) : 0}
 // fused small-product variants (k = 8, serial / pipelined; see M4rmFusedArgs)
 #define SG_KF(F, RT, P) {nullptr, F, 8, RT, 256, 256, P, smem_bytes_for<F, 8, RT, P, 256, true>(), 0, 0, 0, nullptr, 0, \
-                         m4rm_kernel<F, 8, RT, P, 256, 0, false, true>}
+                         m4rm_kernel<F, 8, RT, P, 256, 0, false, true>, 0}
 #define SG_KFUSED(F) SG_KF(F, 1, 0), SG_KF(F, 2, 0), SG_KF(F, 4, 0), SG_KF(F, 2, 1), SG_KF(F, 4, 1)
 // k = 8: 256-thread CTAs (RT 1..8, both schedules) and 512-thread CTAs (16 warps per SM)
 #define SG_KSET8(F)                                                                                 \
