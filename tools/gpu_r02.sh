@@ -43,6 +43,11 @@ pieces)  # streamed host pipeline: row-piece weight variants (SG_HOST_PIECES), t
   for rep in 1 2; do for P in 1,1 1,2,1 1,3 1,2,2,1 1,1,1,1 2,3,1 1,2,1,1 1,4,2,1; do
     SG_HOST_PIECES=$P timeout 120 python tools/e2e_probe.py 1 2>&1 | sed "s/^/pieces=$P /" >> gpurun_out/${T}_e2e_pieces.txt
   done; done ;;
+launches)  # ncu launch list of the bench command (per-kernel durations, cold-cache, serialised)
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv \
+      python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/${T}_launches_bench.json 2>&1 ;;
+trace)  # event trace of one streamed host call of config ARG (default 1), three processes
+  for i in 1 2 3; do TRACE=1 timeout 120 python tools/e2e_probe.py ${ARG:-1} >> gpurun_out/${T}_e2e_trace.txt 2>&1; done ;;
 suite)
   timeout 2400 python -m pytest tests -m gpu -x -q --durations=15 -p no:cacheprovider > gpurun_out/${T}_pytest_gpu.txt 2>&1
   echo "pytest exit $?" >> gpurun_out/${T}_pytest_gpu.txt ;;
