@@ -44,8 +44,8 @@ def _random(spec, m, n, seed):
     return BitslicedMatrix.random(spec, m, n, seed)
 
 
-def _multiply(spec, A, B):
-    return ext_multiply(A, B) if spec.name in EXT_FIELDS else m4rm_multiply(A, B, M4rmParams(8))
+def _multiply(spec, A, B, method="karatsuba"):
+    return ext_multiply(A, B, method=method) if spec.name in EXT_FIELDS else m4rm_multiply(A, B, M4rmParams(8))
 
 
 def _exact_dense(spec, A, B):
@@ -93,15 +93,15 @@ def cmd_verify(args) -> int:
     return 1 if failures else 0
 
 
-def _time_ms(spec, n, reps, seed):
+def _time_ms(spec, n, reps, seed, method="karatsuba"):
     A, B = _random(spec, n, n, seed), _random(spec, n, n, seed + 1)
-    _multiply(spec, A, B)
+    _multiply(spec, A, B, method)
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _multiply(spec, A, B)
+        _multiply(spec, A, B, method)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -121,8 +121,13 @@ def cmd_bench(args) -> int:
     for name in names:
         spec = ALL[name.lower()]
         for n in dims:
-            ms = _time_ms(spec, n, args.reps, _seed(args))
-            rows.append((spec.name, n, "m4rm" if spec.name not in EXT_FIELDS else "ext_multiply", ms,
+            # extension fields: ext_multiply's route (--ext-method: the reference's Karatsuba over
+            # the base field, or one direct power-basis product where the field has one: F4, F8)
+            method = args.ext_method
+            if spec.name in EXT_FIELDS and method == "auto":
+                method = "direct" if getattr(spec, "direct", None) is not None else "karatsuba"
+            ms = _time_ms(spec, n, args.reps, _seed(args), method)
+            rows.append((spec.name, n, "m4rm" if spec.name not in EXT_FIELDS else f"ext_multiply({method})", ms,
                          2.0 * n ** 3 / (ms * 1e-3) / 1e9))
     _header(args)
     if args.format == "csv":
@@ -160,6 +165,8 @@ def main(argv=None) -> int:
     b.add_argument("--dims", default="100,500,1000,2500")
     b.add_argument("--reps", type=int, default=5)
     b.add_argument("--format", choices=["csv", "table"], default="csv")
+    b.add_argument("--ext-method", choices=["auto", "karatsuba", "direct"], default="karatsuba",
+                   help="ext_multiply route for extension fields (default: the reference's Karatsuba)")
     b.add_argument("--seed", type=int, default=0)
     f = sub.add_parser("ffops")
     f.add_argument("--field", default="f3")
