@@ -270,7 +270,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
       const char* e = getenv("SG_TMA");
       return e ? atoi(e) : -1;
     }();
-    a.tma_b = tma_env != 0 && p.ki->sched == 2 && p.K == 8 && p.wc32 % 4 == 0 && ((uintptr_t)B % 16) == 0 &&
+    a.tma_b = tma_env != 0 && ws_tma(p.ki->sched) && p.K == 8 && p.wc32 % 4 == 0 && ((uintptr_t)B % 16) == 0 &&
               encode_b_map(&tmB, B, field, l, p.wc32);
     // A's index words by TMA too, except under stream-K for F3 / F5 / F7 (measured: F3 32768^3
     // -1 %, F7 -1.4 %); GF(4)'s Karatsuba kernel, whose builder warps are its critical path

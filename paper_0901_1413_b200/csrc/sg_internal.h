@@ -44,6 +44,10 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     default: X(Z8); break;               \
   }
 
+// the production warp-specialized schedules (TMA staging, setmaxnreg register split): 2 = four
+// builder warps, 5 = eight
+__host__ __device__ constexpr bool ws_tma(int sched) { return sched == 2 || sched == 5; }
+
 // Column slab per CTA (32-bit words); each lane owns one uint4 (4 words = 128 lanes) of a row.
 constexpr int SLAB_WORDS = 4;
 // Table replicas: the 8 lanes of one LDS.128 phase read 8 different C rows, so entry g is

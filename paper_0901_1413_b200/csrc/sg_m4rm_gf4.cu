@@ -6,6 +6,7 @@ namespace sg {
 
 static KernelInfo g_table[] = {
     SG_K(GF4, 8, 16, 2, 256),
+    SG_K(GF4, 8, 16, 5, 256),  // 8 builder warps: the three replicated Karatsuba planes
     SG_K(GF4, 8, 8, 2, 256),
     SG_KSET8(GF4),
     SG_KFUSED(GF4),

@@ -317,7 +317,13 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 // ABL (experiments only, 0 in production): bit 0 skips the table-replica stores, bit 1 replaces
 // the field update by a plain XOR of the looked-up rows, bit 2 skips the lookups.
 // builder threads of the warp-specialized schedules: SCHED 2 -> 4 warps, 3 -> 1 warp, 4 -> 2 warps
-__host__ __device__ constexpr int ws_builders(int sched) { return sched == 2 ? 128 : sched == 3 ? 32 : sched == 4 ? 64 : 0; }
+// SCHED 5: warp-specialized with 8 builder warps (512-thread CTAs: the lookup warps keep 192
+// registers, the builders 64) for kernels whose table build is their critical path (GF(4)'s three
+// replicated Karatsuba planes)
+__host__ __device__ constexpr int ws_builders(int sched) {
+  return sched == 2 ? 128 : sched == 3 ? 32 : sched == 4 ? 64 : sched == 5 ? 256 : 0;
+}
+
 
 // One segment: the CTA's slab (word0) x row group (row0) x k-blocks [s_begin, s_end), written to
 // C (mode 0), to split-K partial plane `slot` (mode 1) or to compact stream-K slot `slot` (mode 2).
@@ -896,7 +902,7 @@ __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB
                                              uint64_t* mbar) {
   constexpr int ROWS = RT * NT;
   constexpr bool FUSED = std::is_same_v<AT, M4rmFusedArgs>;
-  constexpr bool TMA_OK = SCHED == 2 && K == 8;
+  constexpr bool TMA_OK = ws_tma(SCHED) && K == 8;
   if (!a.streamk) {
     const int s_begin = blockIdx.z * a.bps;
     m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE, STRM>(a, tmB, smem, blockIdx.x * SLAB_WORDS, (int64_t)blockIdx.y * ROWS,
@@ -1023,7 +1029,7 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES +
                                                (2 * 2 * 16 * R * 4 + 3 * K * R * 4 +
                                                 index_stage_words<F, K, RT, NT, FUSED>()) * 4);
-  constexpr bool TMA_OK = SCHED == 2 && K == 8;
+  constexpr bool TMA_OK = ws_tma(SCHED) && K == 8;
   if (TMA_OK && a.tma_b) {
     if (threadIdx.x == 0) {
       for (int i = 0; i < 6; ++i) mbar_init(&mbar[i], 1);  // 3 B slots, 3 A slots
@@ -1031,13 +1037,16 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
     }
     __syncthreads();
   }
-  if constexpr (SCHED == 2) {
+  if constexpr (ws_tma(SCHED)) {
     // warp-specialized: the builder warpgroup hands registers to the two lookup warpgroups,
-    // whose row accumulators need them (384 x 168 = 128 x BREGS + 256 x LREGS)
+    // whose row accumulators need them (384 x 168 = 128 x BREGS + 256 x LREGS; SCHED 5:
+    // 512 x 128 = 256 x 64 + 256 x 192)
     // (F5: 72 / 216 measured ~1 % faster than 56 / 224 -- its builders' carry-save table adds
     // need the registers, its lookups fit in 216; F7 and GF(4) lost 1-2 % with the same split.
     // The streamed-B variant's builders also check chunk flags: at least 64 for them.)
-    constexpr int BREGS = F == F5 ? 72 : STRM ? 64 : 56, LREGS = (168 * (NT + 128) - BREGS * 128) / NT / 8 * 8;
+    constexpr int NBT = ws_builders(SCHED), PER = 65536 / (NT + NBT) / 8 * 8;
+    constexpr int BREGS = SCHED == 5 ? 64 : F == F5 ? 72 : STRM ? 64 : 56;
+    constexpr int LREGS = (PER * (NT + NBT) - BREGS * NBT) / NT / 8 * 8;
     if (threadIdx.x >= NT) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(BREGS));
       run_segments<F, K, RT, SCHED, NT, ABL, 1, STRM>(a, &tmB, smem, mbar);
@@ -1064,7 +1073,7 @@ constexpr int smem_bytes_for() {
 // the streamed-B instantiation of a warp-specialized k = 8 variant (nullptr for the others)
 template <int F, int K, int RT, int P, int NT>
 constexpr StreamKernelFn stream_variant() {
-  if constexpr (P == 2 && K == 8) return m4rm_kernel<F, K, RT, P, NT, 0, true>;
+  if constexpr (ws_tma(P) && K == 8) return m4rm_kernel<F, K, RT, P, NT, 0, true>;
   else return nullptr;
 }
 

@@ -84,6 +84,9 @@ const Calib g_calib[] = {
     {4, 16, 256, 0, 3598, 26686},  // max err 1%, 12 runs
     {4, 16, 256, 1, 3547, 27403},  // max err 2%, 12 runs
     {4, 16, 256, 2, 3107, 27836},  // max err 3%, 12 runs
+    // GF(4) RT 16 with 8 builder warps (schedule 5): the schedule-2 constants x 0.978, its measured
+    // ratio on 8192^3 (tools/step_probe.py, profiles/r02y_step_gf4.txt: 1.312 -> 1.283 ms)
+    {4, 16, 256, 5, 3038, 27836},
     // fused one-launch variants (schedule + 10), from bench-style step times on small shapes
     // (tools/step_probe.py --grid, profiles/r02n_step_grid.jsonl; fit: tools/fit_calib.py)
     {1, 1, 256, 10, 1329, 0},  // max err 36%, 20 runs
@@ -195,7 +198,7 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
     const double alu_l = rows * lane_alu / 64.0, alu_t = E * entry_alu / 64.0;
     const double smem_l = (rows * lane_smem + rows * R * 4.0) / 128.0, smem_t = E * R * ENTRY_BYTES / 128.0;
     // serial: table build then lookups; pipelined / warp-specialized: both share the pipes
-    const double t_block = ki->sched == 2   ? std::max(alu_l + alu_t, smem_l + smem_t) + 100.0
+    const double t_block = ws_tma(ki->sched) ? std::max(alu_l + alu_t, smem_l + smem_t) + 100.0
                            : ki->sched == 1 ? std::max(alu_l + alu_t, smem_l + smem_t) + 250.0
                                             : std::max(alu_l, smem_l) + std::max(alu_t, smem_t) + 400.0;
     const Calib* cal = calib_for(ki);
@@ -332,7 +335,7 @@ int64_t workspace_bytes_for(const Plan& p, int field) {
 // One stream-K wave of the warp-specialized kernel: its builder warps stage every k-block by
 // TMA, so they can wait for each block's chunk; the 4-block group order needs nblocks % 4 == 0.
 bool streamable(const Plan& p) {
-  return p.streamk && p.ki->sched == 2 && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 &&
+  return p.streamk && ws_tma(p.ki->sched) && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 &&
          p.tiles > 0 && p.nblocks / 4 <= STRM_MAX_GROUPS && (int64_t)p.tiles * (p.nblocks / 4) <= (int64_t)1 << 24;
 }
 

@@ -128,7 +128,7 @@ def test_every_compiled_plan(fname):  # noqa: F811
         B = oracle.random_dense(fname, 1001, n, 8)
         want = expect(fname, A, B)
         for rt in (1, 2, 4, 8, 16):
-            for pipe in (0, 1, 2):
+            for pipe in (0, 1, 2, 5):
                 for nt in (256, 512):
                     for splits in (1, 2, 5, 16):
                         m4rm_mod.set_plan_override(rt, splits, pipe, nt)
@@ -193,7 +193,7 @@ def test_streamk_forced(fname):
         B = oracle.random_dense(fname, l, n, n + 3)
         want = expect(fname, A, B)
         for rt in (1, 2, 4, 8, 16):
-            for pipe in (0, 1, 2):
+            for pipe in (0, 1, 2, 5):
                 for nt in (256, 512):
                     m4rm_mod.set_plan_override(rt, -1, pipe, nt)
                     try:
