@@ -164,7 +164,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   }
   uint64_t* dC = (uint64_t*)cur;  // pieces back to back, each [R][rows][wc]
   // SG_HOST_TRACE=1 (experiments): event timestamps of the pipeline steps on stderr
-  static const bool trace = getenv("SG_HOST_TRACE") != nullptr;
+  const bool trace = getenv("SG_HOST_TRACE") != nullptr;  // read per call (experiments)
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
   auto mark = [&](const std::string& what, cudaStream_t st) {
     if (!trace) return;
@@ -509,7 +509,7 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
   }
 
   // SG_HOST_TRACE=1 (experiments): event timestamps of every pipeline step on stderr
-  static const bool trace = getenv("SG_HOST_TRACE") != nullptr;
+  const bool trace = getenv("SG_HOST_TRACE") != nullptr;  // read per call (experiments)
   std::vector<std::pair<const char*, cudaEvent_t>> marks;
   cudaEvent_t t0 = nullptr;
   if (trace) {
