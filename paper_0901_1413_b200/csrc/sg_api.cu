@@ -24,6 +24,7 @@ namespace api {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_buffer_generation{0};
 std::atomic<int64_t> g_streamed{0};  // host-buffer products that streamed B (sg_host_streamed_count)
 int g_override_rt = 0, g_override_splits = 0, g_override_pipe = -1, g_override_threads = 0, g_ablation = 0;
 int g_sm_reserve = 0;  // SMs the planner leaves free (for a collective running concurrently)
@@ -111,6 +112,7 @@ unsigned* fused_counters(int device, cudaStream_t st, int ntiles, cudaError_t* e
     }
     b.p = nullptr;
     b.bytes = 0;
+    g_buffer_generation++;
     if ((*err = cudaMalloc(&b.p, bytes)) != cudaSuccess) return nullptr;
     if ((*err = cudaMemsetAsync(b.p, 0, bytes, st)) != cudaSuccess) return nullptr;
     b.bytes = bytes;
@@ -128,6 +130,7 @@ void* workspace_for(int device, cudaStream_t st, size_t bytes, cudaError_t* err)
     }
     b.p = nullptr;
     b.bytes = 0;
+    g_buffer_generation++;
     *err = cudaMalloc(&b.p, bytes);
     if (*err != cudaSuccess) return nullptr;
     b.bytes = bytes;

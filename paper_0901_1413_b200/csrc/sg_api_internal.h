@@ -19,6 +19,9 @@ namespace api {
 // ---- library state (sg_api.cu)
 extern thread_local std::string g_err;
 extern std::atomic<int64_t> g_launches;
+// bumped whenever a library-owned device buffer (workspace, fused counters) is reallocated:
+// captured graphs that baked the old pointer in must be dropped (sg_host.cu)
+extern std::atomic<int64_t> g_buffer_generation;
 extern std::atomic<int64_t> g_streamed;  // host-buffer products that streamed B (sg_host_streamed_count)
 extern int g_override_rt, g_override_splits, g_override_pipe, g_override_threads, g_ablation;
 extern int g_sm_reserve;  // SMs the planner leaves free (for a collective running concurrently)

@@ -39,6 +39,7 @@ struct Io {
   typedef std::tuple<int, const void*, const void*, void*, int64_t, int64_t, int64_t, int, std::vector<int>> GraphKey;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int> graph_seen;  // calls so far (the first runs uncaptured: it allocates)
+  int64_t graph_generation = -1;       // g_buffer_generation the graphs were captured under
 };
 
 // After a failed call, wait for every copy already queued on the device's pipeline streams: the
@@ -405,6 +406,13 @@ int sg_m4rm_host(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, i
       key = Io::GraphKey{field, A, B, C, m, l, n, k,
                          {g_override_rt, g_override_splits, g_override_pipe, g_override_threads, g_ablation,
                           g_sm_reserve}};
+    }
+    if (d->graph_generation != g_buffer_generation.load()) {
+      // a workspace or counter buffer the graphs point into was reallocated since: drop them all
+      for (auto& g : d->graphs) cudaGraphExecDestroy(g.second);
+      d->graphs.clear();
+      d->graph_seen.clear();
+      d->graph_generation = g_buffer_generation.load();
     }
     auto it = d->graphs.find(key);
     if (it == d->graphs.end()) {

@@ -291,6 +291,22 @@ def test_host_small_calls_replay():
             C = sg.m4rm_multiply(A_, B_, sg.M4rmParams(8), out=C_)
             assert C is C_ and np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, i)
         m4rm_mod.set_plan_override()
+        # a larger host product on the same device grows the library's buffers (workspace,
+        # staging): the graphs captured over the old ones must not be replayed
+        big = 6000 + 64 * "f3 f5 gf4 f7".split().index(fname)
+        Ab = oracle.random_dense(fname, big, 700, 61)
+        Bb = oracle.random_dense(fname, 700, 900, 62)
+        Cb = sg.m4rm_multiply(sg.BitslicedMatrix.from_planes(f, oracle.pack(fname, Ab), 700, device="cpu"),
+                              sg.BitslicedMatrix.from_planes(f, oracle.pack(fname, Bb), 900, device="cpu"))
+        assert np.array_equal(Cb.planes_numpy(), expect(fname, Ab, Bb))
+        for i in range(3):
+            A = oracle.random_dense(fname, m, l, 70 + i)
+            B = oracle.random_dense(fname, l, n, 80 + i)
+            Ap.copy_(torch.from_numpy(oracle.pack(fname, A).view(np.int64)))
+            Bp.copy_(torch.from_numpy(oracle.pack(fname, B).view(np.int64)))
+            Cp.fill_(-1)
+            C = sg.m4rm_multiply(A_, B_, sg.M4rmParams(8), out=C_)
+            assert np.array_equal(C.planes_numpy(), expect(fname, A, B)), (fname, "after growth", i)
 
 
 def test_host_buffers_pipelined_chunks():
