@@ -46,7 +46,10 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // the production warp-specialized schedules (TMA staging, setmaxnreg register split): 2 = four
 // builder warps, 5 = eight
-__host__ __device__ constexpr bool ws_tma(int sched) { return sched == 2 || sched == 5; }
+__host__ __device__ constexpr bool ws_tma(int sched) { return sched == 2 || sched == 5 || sched == 6; }
+// schedule 6: warp-specialized (4 builder warps) with a second set of RT row accumulators per
+// lookup thread in tensor memory -- each table serves 2 RT NT rows (half the replica-store share)
+__host__ __device__ constexpr int rows_of(int rt, int nt, int sched) { return rt * nt * (sched == 6 ? 2 : 1); }
 
 // Column slab per CTA (32-bit words); each lane owns one uint4 (4 words = 128 lanes) of a row.
 constexpr int SLAB_WORDS = 4;

@@ -6,6 +6,7 @@ namespace sg {
 
 static KernelInfo g_table[] = {
     SG_K(F3, 8, 16, 2, 256),
+    SG_KTM(F3, 16),  // 8192 rows per table: 16 row-slots in registers + 16 in tensor memory
     SG_K(F3, 8, 8, 2, 256),
     SG_KSET8(F3),
     SG_KFUSED(F3),

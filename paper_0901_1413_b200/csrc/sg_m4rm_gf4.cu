@@ -7,6 +7,7 @@ namespace sg {
 static KernelInfo g_table[] = {
     SG_K(GF4, 8, 16, 2, 256),
     SG_K(GF4, 8, 16, 5, 256),  // 8 builder warps: the three replicated Karatsuba planes
+    SG_KTM(GF4, 16),           // 8192 rows per table: 16 row-slots in registers + 16 in TMEM
     SG_K(GF4, 8, 8, 2, 256),
     SG_KSET8(GF4),
     SG_KFUSED(GF4),

@@ -176,14 +176,33 @@ template <int F, int K, bool FUSED = false> __host__ __device__ constexpr bool p
 template <int F, int K, int RT, bool FUSED = false> __host__ __device__ constexpr bool paired_index() {
   return packed_index<F, K, FUSED>() && Traits<F>::NI == 2 && RT % 2 == 0;
 }
-template <int F, int K, int RT, bool FUSED = false> __host__ __device__ constexpr int index_slots() {
-  return paired_index<F, K, RT, FUSED>() ? 3 : K == 8 && !FUSED ? (karatsuba<F, K>() ? 2 : 3) : 2;
+// (schedule 6 with Karatsuba GF(4): two slots -- the third table plane and the doubled rows leave
+// no room for a third; its builders then stage block s's index words just in time, see JIT_A)
+template <int F, int K, int RT, bool FUSED = false, int SCHED = 0> __host__ __device__ constexpr int index_slots() {
+  return paired_index<F, K, RT, FUSED>() ? (SCHED == 6 && karatsuba<F, K>() ? 2 : 3)
+                                         : K == 8 && !FUSED ? (karatsuba<F, K>() ? 2 : 3) : 2;
 }
 // u32 of shared memory staging A's index words / planes (NSLOT slots)
-template <int F, int K, int RT, int NT, bool FUSED = false> __host__ __device__ constexpr int index_stage_words() {
-  return index_slots<F, K, RT, FUSED>() * (packed_index<F, K, FUSED>() ? 1 : Traits<F>::R) *
-         (paired_index<F, K, RT, FUSED>() ? RT * NT / 2 : RT * NT);
+template <int F, int K, int RT, int NT, bool FUSED = false, int SCHED = 0>
+__host__ __device__ constexpr int index_stage_words() {
+  return index_slots<F, K, RT, FUSED, SCHED>() * (packed_index<F, K, FUSED>() ? 1 : Traits<F>::R) *
+         (paired_index<F, K, RT, FUSED>() ? rows_of(RT, NT, SCHED) / 2 : rows_of(RT, NT, SCHED));
 }
+
+// ---- tensor memory (schedule 6): a lookup thread's second set of row accumulators
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const u32 (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, u32 (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Row accumulator of one lane: 4 words x RS planes.
 template <int F> struct Acc { u32 w[4][Traits<F>::RS]; };
@@ -321,7 +340,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) { asm volatile("bar.a
 // registers, the builders 64) for kernels whose table build is their critical path (GF(4)'s three
 // replicated Karatsuba planes)
 __host__ __device__ constexpr int ws_builders(int sched) {
-  return sched == 2 ? 128 : sched == 3 ? 32 : sched == 4 ? 64 : sched == 5 ? 256 : 0;
+  return sched == 2 || sched == 6 ? 128 : sched == 3 ? 32 : sched == 4 ? 64 : sched == 5 ? 256 : 0;
 }
 
 
@@ -337,13 +356,14 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
                                              const int mode, const int slot) {
   constexpr bool PIPE = SCHED == 1;
   constexpr bool WS = SCHED >= 2;
+  constexpr bool TM = SCHED == 6;  // second accumulator set in tensor memory (see rows_of)
   constexpr bool FUSED = std::is_same_v<AT, M4rmFusedArgs>;
   static_assert(!WS || K == 8, "the warp-specialized schedules are k = 8 only");
   constexpr int R = Traits<F>::R;
   constexpr int E = 1 << K;
   constexpr int KLO = K < 4 ? K : 4;
   constexpr int KHI = K - KLO;
-  constexpr int ROWS = RT * NT;
+  constexpr int ROWS = rows_of(RT, NT, SCHED);
   constexpr bool KAR = karatsuba<F, K>();
   constexpr int TR = table_planes<F, K>();  // table planes (R, or 3 for Karatsuba GF(4))
   constexpr int TPLANE = E * ENTRY_BYTES;  // bytes per table plane
@@ -362,7 +382,11 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   constexpr bool PAIR = paired_index<F, K, RT, FUSED>();  // two rows per record word (see there)
   constexpr int BPU = PAIR ? 1 : RPW;      // (IW) k-blocks per staged unit of index words
   constexpr int ASZ = PAIR ? ROWS / 2 : ROWS;  // u32 per staged unit and plane
-  constexpr int NSLOT = index_slots<F, K, RT, FUSED>();  // A words in use + blocks in flight
+  constexpr int NSLOT = index_slots<F, K, RT, FUSED, SCHED>();  // A words in use + blocks in flight
+  // two one-block slots (schedule 6, GF(4)): block s's records go up at the builders' iteration
+  // s (its slot held block s-2, whose lookups EMPTY(s) has seen end) and are waited for just
+  // before FULL(s)
+  constexpr bool JIT_A = PAIR && NSLOT == 2;
   constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
   constexpr int TPE_RAW = NT / E;
   constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
@@ -582,6 +606,18 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 
   const unsigned char* tl0 = reinterpret_cast<const unsigned char*>(tab + (tid & (COPIES - 1)));
 
+  // TM: tensor-memory home of row-slot t of accumulator set `region` for this lane: warp w uses
+  // lane quarter w & 3 and columns (w >> 2) 256 + region 128 + t 8 (8 words = one slot of a
+  // 2-plane field); tm_cur = the set currently in registers
+  int tm_cur = 0;
+  auto tm_addr = [&](int region, int t) -> uint32_t {
+    const uint32_t base = *reinterpret_cast<const uint32_t*>(mbar_a + 3);
+    const int w = tid >> 5;
+    return base + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * 256 + region * 128 + t * 8);
+  };
+  static_assert(!TM || Traits<F>::RS * 4 == 8, "schedule 6: 8 accumulator words per row-slot");
+  auto acc8 = [](Acc<F>& x) -> u32(&)[8] { return *reinterpret_cast<u32(*)[8]>(&x.w[0][0]); };
+
   // Byte offsets of row-slot t's table entries for block s.  PAIR: row-slots 2j and 2j+1 share
   // one record word -- it is loaded for the even slot and kept in xw (the callers go through the
   // slots in order, each slot right after the one before it).
@@ -630,25 +666,27 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // lookups for block s from table buffer tb, software-pipelined LA row-slots ahead (entries
   // and table rows of t+1..t+LA in flight while t accumulates); `between(t)` runs after t.
   constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4) ? 2 : 1;
-  auto lookups = [&](int s, int tb, auto&& between) {
+  // (TM: `set` selects the accumulator set in registers -- row-slots set * RT + t)
+  auto lookups = [&](int s, int tb, auto&& between, int set = 0) {
     if constexpr (ABL & 4) {
 #pragma unroll
       for (int t = 0; t < RT; ++t) between(t);
       return;
     }
+    const int so = set * RT;
     const unsigned char* tl = tl0 + tb * TR * TPLANE;
     Rows<F> ring[LA + 1];
 #pragma unroll
     for (int t = 0; t < LA && t < RT; ++t) {
       u32 e[3];
-      entries(s, t, e);
+      entries(s, so + t, e);
       load_rows<F, TPL, KAR>(ring[t], tl, e);
     }
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
       if (t + LA < RT) {
         u32 e[3];
-        entries(s, t + LA, e);
+        entries(s, so + t + LA, e);
         load_rows<F, TPL, KAR>(ring[(t + LA) % (LA + 1)], tl, e);
       }
       if constexpr (ABL & 2) {
@@ -693,11 +731,11 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       for (int s = s_begin; s < s_end; ++s) {
         if (s >= s_begin + 2) nbar_sync(EMPTY(s), NB);  // lookups of block s-2 left tab[s & 1]
         issue_b(s + 2, bt, NBT);
-        issue_a(s + 1, bt, NBT);
+        issue_a(JIT_A ? s : s + 1, bt, NBT);
         cp_async_commit();
         cp_async_wait<1>();  // B rows of s and A words of s have landed (this thread's copies)
         wait_b(s);           // TMA path: the block's B rows ...
-        wait_a(s);           // ... and index word (published to the lookup warps by FULL)
+        if constexpr (!JIT_A) wait_a(s);  // ... and index word (published to the lookup warps by FULL)
         bsync();
         // phase 1: 2 halves x 16 entries x 4 words = 128 items
         {
@@ -758,6 +796,10 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
             }
           }
         }
+        if constexpr (JIT_A) {  // block s's records, staged at this iteration
+          if (tma_a) wait_a(s);
+          else cp_async_wait<0>();
+        }
         nbar_arrive(FULL(s), NB);  // table of block s (and A words of s) ready
       }
       cp_async_wait<0>();
@@ -780,11 +822,30 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     };
     if constexpr (LW2) static_assert(NT == E && R == 2, "plane-2 split: one entry per lookup thread");
     plane2(s_begin);
+    if constexpr (TM) {
+      // set 1 starts from the initial values (set 0, in registers, holds them too)
+#pragma unroll
+      for (int t = 0; t < RT; ++t) tmem_st8(tm_addr(1, t), acc8(c[t]));
+      tmem_wait_st();
+    }
     for (int s = s_begin; s < s_end; ++s) {
       nbar_sync(FULL(s), NB);
-      lookups(s, s & 1, [&](int t) {
-        if (t == RT / 2 - 1 && s + 1 < s_end) plane2(s + 1);
-      });
+      if constexpr (TM) {
+        // the set in registers; after each of its row-slots: park it in its TMEM region and
+        // start loading the same slot of the other set (those loads land behind the remaining
+        // slots' lookups), then the other set's lookups from the same table
+        lookups(s, s & 1, [&](int t) {
+          tmem_st8(tm_addr(tm_cur, t), acc8(c[t]));
+          tmem_ld8(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
+        }, tm_cur);
+        tmem_wait_ld();
+        tm_cur ^= 1;
+        lookups(s, s & 1, [](int) {}, tm_cur);
+      } else {
+        lookups(s, s & 1, [&](int t) {
+          if (t == RT / 2 - 1 && s + 1 < s_end) plane2(s + 1);
+        });
+      }
       if (s + 2 < s_end) nbar_arrive(EMPTY(s), NB);
     }
   } else if constexpr (!PIPE) {
@@ -854,42 +915,54 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     }
   }
 
-  // ---- epilogue
+  // ---- epilogue (row-slots set * RT + t from the registers; TM: both sets, the parked one
+  // loaded back from tensor memory)
   SG_TL(2);
-  if (mode == 2) {  // stream-K: compact slot [R][ROWS][4 words], canonical (summed by the reduce)
-    u32* out = a.P2 + (int64_t)slot * R * ROWS * 4;
+  auto write_set = [&](int set) {
+    if (mode == 2) {  // stream-K: compact slot [R][ROWS][4 words], canonical (summed by the reduce)
+      u32* out = a.P2 + (int64_t)slot * R * ROWS * 4;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int lr = (set * RT + t) * NT + tid;
+        u32 o[4][R];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], true);
+#pragma unroll
+        for (int d = 0; d < R; ++d)
+          *reinterpret_cast<uint4*>(out + ((int64_t)d * ROWS + lr) * 4) = make_uint4(o[0][d], o[1][d], o[2][d], o[3][d]);
+      }
+      return;
+    }
+    u32* out = a.C;
+    int64_t rows_out = a.m;
+    if (mode == 1) {
+      out += (int64_t)slot * R * a.mpad * a.wc32;
+      rows_out = a.mpad;
+    }
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
-      const int lr = t * NT + tid;
-      u32 o[4][R];
+      const int64_t row = row0 + (set * RT + t) * NT + tid;
+      if (row < a.m) {
+        u32 o[4][R];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], true);
+        for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], mode == 0);
 #pragma unroll
-      for (int d = 0; d < R; ++d)
-        *reinterpret_cast<uint4*>(out + ((int64_t)d * ROWS + lr) * 4) = make_uint4(o[0][d], o[1][d], o[2][d], o[3][d]);
-    }
-    return;
-  }
-  u32* out = a.C;
-  int64_t rows_out = a.m;
-  if (mode == 1) {
-    out += (int64_t)slot * R * a.mpad * a.wc32;
-    rows_out = a.mpad;
-  }
-#pragma unroll
-  for (int t = 0; t < RT; ++t) {
-    const int64_t row = row0 + t * NT + tid;
-    if (row < a.m) {
-      u32 o[4][R];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], mode == 0);
-#pragma unroll
-      for (int d = 0; d < R; ++d) {
-        u32* dst = out + ((int64_t)d * rows_out + row) * a.wc32 + word0;
-        if (word0 < a.wc32) *reinterpret_cast<uint2*>(dst) = make_uint2(o[0][d], o[1][d]);
-        if (word0 + 2 < a.wc32) *reinterpret_cast<uint2*>(dst + 2) = make_uint2(o[2][d], o[3][d]);
+        for (int d = 0; d < R; ++d) {
+          u32* dst = out + ((int64_t)d * rows_out + row) * a.wc32 + word0;
+          if (word0 < a.wc32) *reinterpret_cast<uint2*>(dst) = make_uint2(o[0][d], o[1][d]);
+          if (word0 + 2 < a.wc32) *reinterpret_cast<uint2*>(dst + 2) = make_uint2(o[2][d], o[3][d]);
+        }
       }
     }
+  };
+  if constexpr (TM) {
+    write_set(tm_cur);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) tmem_ld8(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
+    tmem_wait_ld();
+    write_set(tm_cur ^ 1);
+  } else {
+    write_set(0);
   }
 }
 
@@ -900,7 +973,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE, bool STRM, typename AT>
 __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB, unsigned char* smem,
                                              uint64_t* mbar) {
-  constexpr int ROWS = RT * NT;
+  constexpr int ROWS = rows_of(RT, NT, SCHED);
   constexpr bool FUSED = std::is_same_v<AT, M4rmFusedArgs>;
   constexpr bool TMA_OK = ws_tma(SCHED) && K == 8;
   if (!a.streamk) {
@@ -1020,7 +1093,7 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
     m4rm_kernel(const std::conditional_t<STRM, M4rmStreamArgs, std::conditional_t<FUSED, M4rmFusedArgs, M4rmArgs>> a,
                 const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int ROWS = RT * NT;
+  constexpr int ROWS = rows_of(RT, NT, SCHED);
   SG_TL(0);
   if (a.early_trigger) pdl_trigger();
   // launched with PDL behind the index pre-pass: each schedule waits for it (pdl_wait) just
@@ -1028,7 +1101,7 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
   constexpr int R = Traits<F>::R;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES +
                                                (2 * 2 * 16 * R * 4 + 3 * K * R * 4 +
-                                                index_stage_words<F, K, RT, NT, FUSED>()) * 4);
+                                                index_stage_words<F, K, RT, NT, FUSED, SCHED>()) * 4);
   constexpr bool TMA_OK = ws_tma(SCHED) && K == 8;
   if (TMA_OK && a.tma_b) {
     if (threadIdx.x == 0) {
@@ -1047,12 +1120,31 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
     constexpr int NBT = ws_builders(SCHED), PER = 65536 / (NT + NBT) / 8 * 8;
     constexpr int BREGS = SCHED == 5 ? 64 : F == F5 ? 72 : STRM ? 64 : 56;
     constexpr int LREGS = (PER * (NT + NBT) - BREGS * NBT) / NT / 8 * 8;
+    // schedule 6: warp 0 allocates all 512 TMEM columns (one CTA per SM) for the lookup warps'
+    // second accumulator sets; its address goes to the word after the mbarriers
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 6);
+    if constexpr (SCHED == 6) {
+      if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
     if (threadIdx.x >= NT) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(BREGS));
       run_segments<F, K, RT, SCHED, NT, ABL, 1, STRM>(a, &tmB, smem, mbar);
     } else {
       asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LREGS));
       run_segments<F, K, RT, SCHED, NT, ABL, 2, STRM>(a, &tmB, smem, mbar);
+    }
+    if constexpr (SCHED == 6) {
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (threadIdx.x < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tslot));
     }
   } else {
     run_segments<F, K, RT, SCHED, NT, ABL, 0, STRM>(a, &tmB, smem, mbar);
@@ -1067,7 +1159,8 @@ template <int F, int K, int RT, int SCHED, int NT, bool FUSED = false>
 constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
   return (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
-         index_stage_words<F, K, RT, NT, FUSED>() * 4 + 6 * 8;  // + the B- and A-slot mbarriers
+         index_stage_words<F, K, RT, NT, FUSED, SCHED>() * 4 + 6 * 8 +  // + the B- and A-slot mbarriers
+         (SCHED == 6 ? 16 : 0);                                         // + the TMEM address (schedule 6)
 }
 
 // the streamed-B instantiation of a warp-specialized k = 8 variant (nullptr for the others)
@@ -1084,6 +1177,10 @@ constexpr StreamKernelFn stream_variant() {
 #define SG_KA(F, K, RT, P, NT, A) {m4rm_kernel<F, K, RT, P, NT, A>, F, K, RT, NT, (NT) + ws_builders(P), P, \
                                    smem_bytes_for<F, K, RT, P, NT>(), 0, 0, A, nullptr, 0, nullptr, \
                                    paired_index<F, K, RT>() ? (NT) : 0}
+// schedule 6 (second accumulator set in TMEM): KernelInfo.rt counts both sets' row-slots
+#define SG_KTM(F, RT) {m4rm_kernel<F, 8, RT, 6, 256>, F, 8, 2 * (RT), 256, 256 + ws_builders(6), 6, \
+                       smem_bytes_for<F, 8, RT, 6, 256>(), 0, 0, 0, nullptr, 0, nullptr, \
+                       paired_index<F, 8, RT>() ? 256 : 0}
 // fused small-product variants (k = 8, serial / pipelined; see M4rmFusedArgs)
 #define SG_KF(F, RT, P) {nullptr, F, 8, RT, 256, 256, P, smem_bytes_for<F, 8, RT, P, 256, true>(), 0, 0, 0, nullptr, 0, \
                          m4rm_kernel<F, 8, RT, P, 256, 0, false, true>, 0}

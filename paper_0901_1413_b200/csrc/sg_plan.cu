@@ -87,6 +87,12 @@ const Calib g_calib[] = {
     // GF(4) RT 16 with 8 builder warps (schedule 5): the schedule-2 constants x 0.978, its measured
     // ratio on 8192^3 (tools/step_probe.py, profiles/r02y_step_gf4.txt: 1.312 -> 1.283 ms)
     {4, 16, 256, 5, 3038, 27836},
+    // F3 with the second accumulator set in TMEM (schedule 6, 8192 rows per CTA): from the
+    // bench-style steps of 32768^3 split-K (76.8 ms) and 8192 x 32768^2 stream-K (19.5 ms)
+    // (tools/step_probe.py, profiles/r02af_step.txt, r02ag_step.txt)
+    {1, 32, 256, 6, 5300, 25000},
+    // GF(4), schedule 6: 8192^3 stream-K 1.036 ms (profiles/r02ah_step.txt)
+    {4, 32, 256, 6, 4370, 25000},
     // fused one-launch variants (schedule + 10), from bench-style step times on small shapes
     // (tools/step_probe.py --grid, profiles/r02n_step_grid.jsonl; fit: tools/fit_calib.py)
     {1, 1, 256, 10, 1329, 0},  // max err 36%, 20 runs
@@ -217,8 +223,10 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       const int rpw = field == SG_F2 ? 4 : planes(field) == 3 ? 1 : 2;
       const double l2_set = (double)((nblocks + rpw - 1) / rpw) * rgroups * rows * 4.0 + (double)R * l * wc32 * 4.0;
       const bool short_ranges = (units + G - 1) / G <= 2 * (int64_t)nblocks - 1;
+      // (schedule 6: ranges over at most two row groups are fine too -- F3 16384 x 32768^2
+      // stream-K 39.0 ms against 43.8 split-K; at four row groups split-K wins by 1.5 %)
       const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 && units >= G &&
-                      (short_ranges || l2_set <= 120e6 || g_override_splits == -1);
+                      (short_ranges || l2_set <= 120e6 || g_override_splits == -1 || (ki->sched == 6 && rgroups <= 2));
       if (ok) {
         const double per = (double)(units + G - 1) / G;
         const double nseg = std::min(2.0, per) + std::floor(per / nblocks);  // segments per CTA

@@ -153,6 +153,7 @@ def build_table(B: BitslicedMatrix, s: int, k: int) -> torch.Tensor:
 SCHEDULES = {0: "serial", 1: "pipelined", 2: "warp-specialized (4 builder warps)",
              3: "warp-specialized (1 builder warp)", 4: "warp-specialized (2 builder warps)",
              5: "warp-specialized (8 builder warps)",
+             6: "warp-specialized (4 builder warps, TMEM row-slots)",
              10: "fused serial (one launch)", 11: "fused pipelined (one launch)"}
 # schedule codes of the fused small-product variants (sg_set_plan_override's `pipe`)
 FUSED_SERIAL, FUSED_PIPELINED = 10, 11

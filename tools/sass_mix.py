@@ -34,7 +34,7 @@ def mix_of(fname, ins, field_code, rt, sched, nt):
         # warp-specialized schedule it holds no table stores (those are the builder warps')
         # (GF(4), k = 8: Karatsuba tables, three one-plane lookups per row)
         nl = 3 if name == "gf4" else NI * R
-        if c["LDS"] >= rt * nl and c["LOP3"] >= rt and (sched not in (2, 5) or c["STS"] == 0):
+        if c["LDS"] >= rt * nl and c["LOP3"] >= rt and (sched not in (2, 5, 6) or c["STS"] == 0):
             best = (a, b, c)
             break  # loops() is sorted by size: the smallest qualifying loop
     if best is None:
@@ -43,7 +43,7 @@ def mix_of(fname, ins, field_code, rt, sched, nt):
     per = {k: v / rt for k, v in sorted(c.items())}
     return {"field": name, "rt": rt, "sched": sched, "threads": nt, "loop": [hex(a), hex(b)],
             "loop_instructions": sum(c.values()),
-            "includes_table_build": sched not in (2, 5),
+            "includes_table_build": sched not in (2, 5, 6),
             "per_row_block": per,
             "alu_per_row_block": sum(v for k, v in per.items() if k in ALU),
             "lop3_per_row_block": per.get("LOP3", 0.0),
@@ -66,6 +66,8 @@ def main():
             if not m:
                 continue
             rt, sched, nt = (int(x) for x in m.groups())
+            if sched == 6:  # second accumulator set in TMEM: the loop covers 2 RT row-slots
+                rt *= 2
             mix = mix_of(fname, ins, code, rt, sched, nt)
             if mix:
                 out[f"{name}/{rt}/{sched}/{nt}"] = mix
