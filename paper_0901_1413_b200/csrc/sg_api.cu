@@ -278,7 +278,9 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
     // A's index words by TMA too, except under stream-K for F3 / F5 / F7 (measured: F3 32768^3
     // -1 %, F7 -1.4 %); GF(4)'s Karatsuba kernel, whose builder warps are its critical path
     // (three replicated table planes), gains 3.9 % (1.349 -> 1.297 ms).  SG_TMA=2 forces it.
-    a.tma_a = a.tma_b && (tma_env == 2 || !p.streamk || field == SG_GF4);
+    // (schedule 6 stages the index words just in time where it has two slots: TMA keeps the
+    // builders from waiting on their own cp.async group)
+    a.tma_a = a.tma_b && (tma_env == 2 || !p.streamk || field == SG_GF4 || p.ki->sched == 6);
   }
   if (sin && !a.tma_b) return fail(SG_EINVAL, "streamed B needs the TMA staging path");
   a.streamk = p.streamk;

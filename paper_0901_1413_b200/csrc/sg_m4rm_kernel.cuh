@@ -166,6 +166,10 @@ template <int F, int K> __host__ __device__ constexpr bool karatsuba() { return 
 template <int F, int K> __host__ __device__ constexpr int table_planes() { return karatsuba<F, K>() ? 3 : Traits<F>::R; }
 // staging slots of A's index words: Karatsuba GF(4) needs the room of the third table plane, and
 // with two k-blocks per index word two slots are enough (see issue_a)
+// half-table buffers: the serial / pipelined schedules build block s+1's (or s+2's) while block
+// s's are read; the warp-specialized builders finish with one before the next
+__host__ __device__ constexpr int half_bufs(int sched) { return sched >= 2 ? 1 : 2; }
+
 // staged index source: k = 8 packed records from the pre-pass (one plane), else R planes of A
 // words (A^T from the transpose pre-pass, or A itself in the fused small-product kernels)
 template <int F, int K, bool FUSED = false> __host__ __device__ constexpr bool packed_index() { return K == 8 && !FUSED; }
@@ -180,7 +184,7 @@ template <int F, int K, int RT, bool FUSED = false> __host__ __device__ constexp
 // no room for a third; its builders then stage block s's index words just in time, see JIT_A)
 template <int F, int K, int RT, bool FUSED = false, int SCHED = 0> __host__ __device__ constexpr int index_slots() {
   return paired_index<F, K, RT, FUSED>() ? (SCHED == 6 && karatsuba<F, K>() ? 2 : 3)
-                                         : K == 8 && !FUSED ? (karatsuba<F, K>() ? 2 : 3) : 2;
+                                         : K == 8 && !FUSED ? (karatsuba<F, K>() || SCHED == 6 ? 2 : 3) : 2;
 }
 // u32 of shared memory staging A's index words / planes (NSLOT slots)
 template <int F, int K, int RT, int NT, bool FUSED = false, int SCHED = 0>
@@ -200,6 +204,29 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, u32 (&r)[8]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr)
                : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const u32 (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, u32 (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+// one row-slot's accumulator words (4 x RS) to / from tensor memory
+template <int N> __device__ __forceinline__ void tmem_st(uint32_t taddr, u32 (&r)[N]) {
+  static_assert(N == 8 || N == 16, "8 or 16 accumulator words per row-slot");
+  if constexpr (N == 8) tmem_st8(taddr, r); else tmem_st16(taddr, r);
+}
+template <int N> __device__ __forceinline__ void tmem_ld(uint32_t taddr, u32 (&r)[N]) {
+  if constexpr (N == 8) tmem_ld8(taddr, r); else tmem_ld16(taddr, r);
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -386,15 +413,15 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // two one-block slots (schedule 6, GF(4)): block s's records go up at the builders' iteration
   // s (its slot held block s-2, whose lookups EMPTY(s) has seen end) and are waited for just
   // before FULL(s)
-  constexpr bool JIT_A = PAIR && NSLOT == 2;
+  constexpr bool JIT_A = TM && IW && NSLOT == 2;
   constexpr int NAP = IW ? 1 : R;          // staged A planes per slot
   constexpr int TPE_RAW = NT / E;
   constexpr int TPE = TPE_RAW < 1 ? 1 : (TPE_RAW > COPIES ? COPIES : TPE_RAW);  // threads per entry
   constexpr int CPT = COPIES / TPE;        // replicas written per thread
 
   uint4* tab = reinterpret_cast<uint4*>(smem);                     // [NTAB][TR][E][COPIES] uint4
-  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * TR * TPLANE);  // [2 buf][2 half][R][16][4]
-  u32* bst = thalf + 2 * 2 * HALF;                                 // [3 slot][K][R][4]
+  u32* thalf = reinterpret_cast<u32*>(smem + NTAB * TR * TPLANE);  // [bufs][2 half][R][16][4]
+  u32* bst = thalf + half_bufs(SCHED) * 2 * HALF;                  // [3 slot][K][R][4]
   u32* ast = bst + 3 * K * R * 4;                                  // [NSLOT][NAP][ASZ]
   uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ASZ);  // [3] B-slot barriers
   uint64_t* mbar_a = mbar_b + 3;                                               // [3] A-slot barriers
@@ -610,13 +637,14 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // lane quarter w & 3 and columns (w >> 2) 256 + region 128 + t 8 (8 words = one slot of a
   // 2-plane field); tm_cur = the set currently in registers
   int tm_cur = 0;
+  constexpr int SW = 4 * Traits<F>::RS;  // accumulator words (TMEM columns) per row-slot
   auto tm_addr = [&](int region, int t) -> uint32_t {
     const uint32_t base = *reinterpret_cast<const uint32_t*>(mbar_a + 3);
     const int w = tid >> 5;
-    return base + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * 256 + region * 128 + t * 8);
+    return base + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(((w >> 2) * 2 + region) * RT * SW + t * SW);
   };
-  static_assert(!TM || Traits<F>::RS * 4 == 8, "schedule 6: 8 accumulator words per row-slot");
-  auto acc8 = [](Acc<F>& x) -> u32(&)[8] { return *reinterpret_cast<u32(*)[8]>(&x.w[0][0]); };
+  static_assert(!TM || 4 * RT * SW <= 512, "schedule 6: two sets of two warps per lane quarter in 512 columns");
+  auto acc8 = [](Acc<F>& x) -> u32(&)[SW] { return *reinterpret_cast<u32(*)[SW]>(&x.w[0][0]); };
 
   // Byte offsets of row-slot t's table entries for block s.  PAIR: row-slots 2j and 2j+1 share
   // one record word -- it is loaded for the even slot and kept in xw (the callers go through the
@@ -706,13 +734,6 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     constexpr int NB = NT + NBT;  // all threads take part in every FULL / EMPTY barrier
     auto FULL = [](int s) { return 1 + (s & 1); };
     auto EMPTY = [](int s) { return 3 + (s & 1); };
-    // LW2 (experiment, off): the builders publish block s's half tables (double-buffered,
-    // HALF(s)) and store table planes 0 and 1 of Karatsuba GF(4); the lookup warps derive plane
-    // 2 = T0 ^ T1 of block s+1 from the half tables halfway through block s's lookups.  Measured
-    // slower (GF(4) 8192^3 1.35 -> 1.63 ms): the extra barrier inside the lookup loop costs more
-    // than the builders' third-plane stores.
-    constexpr bool LW2 = false;
-    auto HALFB = [](int s) { return 6 + (s & 1); };
     if constexpr (ROLE == 1) {
       // ------------------------------------------------ builder warps
       const int bt = tid - NT;
@@ -754,19 +775,17 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
                   vadd<F>(acc, b);
                 }
               }
-              u32* th = LW2 ? thalf + (s & 1) * 2 * HALF : thalf;
 #pragma unroll
-              for (int d = 0; d < R; ++d) th[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
+              for (int d = 0; d < R; ++d) thalf[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
             }
           }
         }
         bsync();
-        if constexpr (LW2) nbar_arrive(HALFB(s), NB);
         // phase 2: 256 entries x 8 replicas.  A thread's entries g = bt + NBT it share the low
         // half-table entry (NBT is a multiple of 16): it is read once.
         uint4* tb = tab + (s & 1) * TR * TPL;
         static_assert(NBT % 16 == 0, "phase 2 shares the low half entry across a thread's entries");
-        const u32* th2 = LW2 ? thalf + (s & 1) * 2 * HALF : thalf;
+        const u32* th2 = thalf;
         uint4 Lh[R];
 #pragma unroll
         for (int d = 0; d < R; ++d) Lh[d] = reinterpret_cast<const uint4*>(th2)[(bt & ((1 << KLO) - 1)) + d * 16];
@@ -790,7 +809,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 #pragma unroll
               for (int d = 0; d < R; ++d)
                 tb[d * TPL + g * (ENTRY_BYTES / 16) + copy] = make_uint4(v[0].p[d], v[1].p[d], v[2].p[d], v[3].p[d]);
-              if constexpr (KAR && !LW2)
+              if constexpr (KAR)
                 tb[2 * TPL + g * (ENTRY_BYTES / 16) + copy] =
                     make_uint4(v[0].p[0] ^ v[0].p[1], v[1].p[0] ^ v[1].p[1], v[2].p[0] ^ v[2].p[1], v[3].p[0] ^ v[3].p[1]);
             }
@@ -806,26 +825,10 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       return;
     }
     // ------------------------------------------------ lookup warps (ROLE 2)
-    // (LW2) plane 2 of block s's table: entry tid = T0 ^ T1 from the half tables, 8 replicas
-    auto plane2 = [&](int s) {
-      if constexpr (LW2) {
-        nbar_sync(HALFB(s), NB);
-        const uint4* th = reinterpret_cast<const uint4*>(thalf + (s & 1) * 2 * HALF);
-        const int g = tid;  // NT == E: one entry per lookup thread
-        const uint4 l0 = th[g & 15], l1 = th[16 + (g & 15)], h0 = th[2 * 16 + (g >> 4)], h1 = th[3 * 16 + (g >> 4)];
-        const uint4 v = make_uint4(l0.x ^ l1.x ^ h0.x ^ h1.x, l0.y ^ l1.y ^ h0.y ^ h1.y, l0.z ^ l1.z ^ h0.z ^ h1.z,
-                                   l0.w ^ l1.w ^ h0.w ^ h1.w);
-        uint4* tb = tab + (s & 1) * TR * TPL + 2 * TPL + g * (ENTRY_BYTES / 16);
-#pragma unroll
-        for (int cc = 0; cc < COPIES; ++cc) tb[(cc + g) & (COPIES - 1)] = v;
-      }
-    };
-    if constexpr (LW2) static_assert(NT == E && R == 2, "plane-2 split: one entry per lookup thread");
-    plane2(s_begin);
     if constexpr (TM) {
       // set 1 starts from the initial values (set 0, in registers, holds them too)
 #pragma unroll
-      for (int t = 0; t < RT; ++t) tmem_st8(tm_addr(1, t), acc8(c[t]));
+      for (int t = 0; t < RT; ++t) tmem_st(tm_addr(1, t), acc8(c[t]));
       tmem_wait_st();
     }
     for (int s = s_begin; s < s_end; ++s) {
@@ -835,16 +838,14 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
         // start loading the same slot of the other set (those loads land behind the remaining
         // slots' lookups), then the other set's lookups from the same table
         lookups(s, s & 1, [&](int t) {
-          tmem_st8(tm_addr(tm_cur, t), acc8(c[t]));
-          tmem_ld8(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
+          tmem_st(tm_addr(tm_cur, t), acc8(c[t]));
+          tmem_ld(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
         }, tm_cur);
         tmem_wait_ld();
         tm_cur ^= 1;
         lookups(s, s & 1, [](int) {}, tm_cur);
       } else {
-        lookups(s, s & 1, [&](int t) {
-          if (t == RT / 2 - 1 && s + 1 < s_end) plane2(s + 1);
-        });
+        lookups(s, s & 1, [](int) {});
       }
       if (s + 2 < s_end) nbar_arrive(EMPTY(s), NB);
     }
@@ -958,7 +959,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   if constexpr (TM) {
     write_set(tm_cur);
 #pragma unroll
-    for (int t = 0; t < RT; ++t) tmem_ld8(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
+    for (int t = 0; t < RT; ++t) tmem_ld(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
     tmem_wait_ld();
     write_set(tm_cur ^ 1);
   } else {
@@ -1100,7 +1101,7 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
   // before its first read of A's index words, so the B staging overlaps the pre-pass's tail
   constexpr int R = Traits<F>::R;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES +
-                                               (2 * 2 * 16 * R * 4 + 3 * K * R * 4 +
+                                               (half_bufs(SCHED) * 2 * 16 * R * 4 + 3 * K * R * 4 +
                                                 index_stage_words<F, K, RT, NT, FUSED, SCHED>()) * 4);
   constexpr bool TMA_OK = ws_tma(SCHED) && K == 8;
   if (TMA_OK && a.tma_b) {
@@ -1158,7 +1159,8 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
 template <int F, int K, int RT, int SCHED, int NT, bool FUSED = false>
 constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
-  return (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES + 2 * 2 * 16 * R * 4 * 4 + 3 * K * R * 4 * 4 +
+  return (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES + half_bufs(SCHED) * 2 * 16 * R * 4 * 4 +
+         3 * K * R * 4 * 4 +
          index_stage_words<F, K, RT, NT, FUSED, SCHED>() * 4 + 6 * 8 +  // + the B- and A-slot mbarriers
          (SCHED == 6 ? 16 : 0);                                         // + the TMEM address (schedule 6)
 }
