@@ -85,6 +85,19 @@ __device__ __forceinline__ void f5_add(u32& x0, u32& x1, u32& x2, u32 y0, u32 y1
   add3(x0, x1, x2, y0, y1, y2, s0, s1, s2, s3);
   fold5(s0, s1, s2, s3, x0, x1, x2);
 }
+// x + y for canonical F5 lanes (x, y <= 4): a 3-bit representative of the residue (0..7, not
+// canonical): the only carry out is x = y = 4, sum 8 == 3 (mod 5) -- OR it into bits 0 and 1.
+// 7 LOP3 against f5_add's ~13; the M4RM table entries may be redundant (the lookup networks are
+// exact mod 15 for every 3-bit input, tools/lop3/csa_gen.py), their half-table inputs canonical.
+__device__ __forceinline__ void f5_add_lazy(u32& x0, u32& x1, u32& x2, u32 y0, u32 y1, u32 y2) {
+  const u32 c0 = x0 & y0;
+  const u32 c1 = lop3<LOP_MAJ>(x1, y1, c0);
+  const u32 s3 = lop3<LOP_MAJ>(x2, y2, c1);
+  x2 = lop3<LOP_XOR3>(x2, y2, c1);
+  const u32 s1 = lop3<LOP_XOR3>(x1, y1, c0);
+  x0 = (x0 ^ y0) | s3;
+  x1 = s1 | s3;
+}
 // x += y mod 7 as a 3-bit one's-complement (end-around-carry) adder: 8 LOP3.  co = [x+y >= 8]
 // re-enters at bit 0 (8 == 1 mod 7); x + y + co never carries out again (<= 15 - 8).  Same
 // residues as the reference's 17-op adder chain + fold (_core_py.py:65-88), any of 0/7 for zero.

@@ -775,6 +775,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
                   vadd<F>(acc, b);
                 }
               }
+              if constexpr (F == F5) vcanon<F>(acc);  // canonical halves for the lazy phase-2 add
 #pragma unroll
               for (int d = 0; d < R; ++d) thalf[((h * R + d) * 16 + e) * 4 + w] = acc.p[d];
             }
@@ -801,7 +802,12 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
             hv[0].p[d] = H.x; hv[1].p[d] = H.y; hv[2].p[d] = H.z; hv[3].p[d] = H.w;
           }
 #pragma unroll
-          for (int w = 0; w < 4; ++w) vadd<F>(v[w], hv[w]);
+          for (int w = 0; w < 4; ++w) {
+            if constexpr (F == F5)  // canonical halves: a redundant 3-bit sum is enough
+              f5_add_lazy(v[w].p[0], v[w].p[1], v[w].p[2], hv[w].p[0], hv[w].p[1], hv[w].p[2]);
+            else
+              vadd<F>(v[w], hv[w]);
+          }
           if constexpr (!(ABL & 1)) {
 #pragma unroll
             for (int cc = 0; cc < COPIES; ++cc) {
