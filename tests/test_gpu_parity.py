@@ -799,19 +799,20 @@ def test_sm_reserve_plans_fewer_ctas():
 
 def test_fuzz_plans_shapes_fields():
     """Seeded fuzz: random field, shape (incl. word-boundary and tiny / skinny ones), k, and a
-    random forced plan (rows per thread, schedule, split count or stream-K, CTA width, F3 SM
-    reserve); every product bit-identical to the oracle."""
+    random forced plan (rows per thread, schedule incl. the 8-builder, TMEM-accumulator and fused
+    one-launch ones, split count or stream-K, CTA width, SM reserve); every product bit-identical
+    to the oracle."""
     rng = np.random.default_rng(2026)
     names = list(FIELDS)
     ran = 0
-    for it in range(120):
+    for it in range(200):
         fname = names[it % len(names)]
         m = int(rng.choice([1, 7, 63, 64, 65, 200, 513, 1500, 3000]))
         l = int(rng.choice([1, 8, 31, 64, 100, 257, 1000, 2049]))
         n = int(rng.choice([1, 32, 63, 64, 65, 128, 129, 700, 1024]))
         k = int(rng.choice([8, 8, 8, 5, 3, 1, 12]))
-        rt = int(rng.choice([0, 1, 2, 4, 8, 16]))
-        pipe = int(rng.choice([-1, 0, 1, 2]))
+        rt = int(rng.choice([0, 1, 2, 4, 8, 16, 32]))
+        pipe = int(rng.choice([-1, 0, 1, 2, 5, 6, m4rm_mod.FUSED_SERIAL, m4rm_mod.FUSED_PIPELINED]))
         nt = int(rng.choice([0, 256, 512]))
         splits = int(rng.choice([0, 0, 1, 3, 7, -1]))
         A = oracle.random_dense(fname, m, l, it)
