@@ -374,9 +374,11 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
 
     L = _lib.load()
     rank = dist.get_rank() if world > 1 else 0
-    Ah = A.planes.cpu().pin_memory()
-    Bh = B.planes.cpu().pin_memory()
-    Ch = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64).pin_memory()
+    # page-locked operands written by one thread on one CPU (BitslicedMatrix.pin_memory: on the
+    # B200 box, a VM, H2D from buffers written by several threads at once ran at 15-25 GB/s)
+    Ah = A.pin_memory().planes
+    Bh = B.pin_memory().planes
+    Ch = sg.BitslicedMatrix.pinned_zero(f, m, n).planes
     vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     dev = device.index or 0
     Bd = torch.empty_like(B.planes)
@@ -456,6 +458,8 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
                              "ms_per_step": 1e3 * statistics.mean(pts), "step_ms_min": 1e3 * min(pts),
                              "verified_vs_device_path": bool(np.array_equal(Cn, Ch.numpy().view(np.uint64))),
                              "path": "m4rm_multiply(BitslicedMatrix over pageable numpy planes) -> sg_m4rm_host"}
+    extra["host_buffers"] = ("page-locked, allocated and written by one thread on one CPU "
+                             "(BitslicedMatrix.pin_memory / pinned_zero)")
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(Ch.numel() * 8), **extra,
             "path": ("sg_m4rm_host (C ABI; pinned host planes; A and C in row pieces, the first piece's product "

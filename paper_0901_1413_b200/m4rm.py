@@ -61,9 +61,10 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
         a = A.planes.contiguous()
         b = B.planes.contiguous()
         if out is None:
-            C = BitslicedMatrix.zero(field, m, n, device="cpu")
-            if a.is_pinned() and b.is_pinned():
-                C.planes = C.planes.pin_memory()  # page-locked in, page-locked out: async copies
+            if a.is_pinned() and b.is_pinned():  # page-locked in, page-locked out: async copies
+                C = BitslicedMatrix.pinned_zero(field, m, n)
+            else:
+                C = BitslicedMatrix.zero(field, m, n, device="cpu")
         else:
             # sg_m4rm_host writes R*m*W words through this pointer: the same checks as on the
             # device, plus host residency (a device pointer is not a host buffer)

@@ -31,6 +31,32 @@ def _dev(device):
     return d
 
 
+class one_cpu_writer:
+    """Context: the calling thread on the CPU it is running on and torch's CPU ops single-threaded
+    (both restored on exit) -- host buffers written inside are written by one thread on one CPU."""
+
+    def __enter__(self):
+        self.threads = torch.get_num_threads()
+        self.mask = None
+        try:
+            cpu = ctypes.CDLL(None).sched_getcpu()
+            if cpu >= 0 and hasattr(__import__("os"), "sched_setaffinity"):
+                import os
+                self.mask = os.sched_getaffinity(0)
+                os.sched_setaffinity(0, {cpu})
+        except (OSError, AttributeError):
+            self.mask = None
+        torch.set_num_threads(1)
+        return self
+
+    def __exit__(self, *exc):
+        torch.set_num_threads(self.threads)
+        if self.mask is not None:
+            import os
+            os.sched_setaffinity(0, self.mask)
+        return False
+
+
 def _require_cuda(device):
     if device.type != "cuda":
         raise ValueError("this operation runs on a CUDA device (no CPU fallback)")
@@ -149,6 +175,27 @@ class BitslicedMatrix:
 
     def copy(self) -> "BitslicedMatrix":
         return BitslicedMatrix(self.field, self.nrows, self.ncols, self.planes.clone())
+
+    def pin_memory(self) -> "BitslicedMatrix":
+        """A copy in page-locked host memory, the operand form of the host-buffer path (copied
+        asynchronously, overlapped with the products).  The buffer is allocated and filled by
+        the calling thread alone, kept on one CPU while it does: on the B200 box (a 16-vCPU VM)
+        host-to-device DMA from page-locked buffers written by several threads at once ran at
+        15-25 GB/s instead of ~52 in most processes (profiles/r02_experiments.txt)."""
+        with one_cpu_writer():
+            t = torch.empty(tuple(self.planes.shape), dtype=torch.int64, pin_memory=True)
+            t.copy_(self.planes)
+        return BitslicedMatrix(self.field, self.nrows, self.ncols, t)
+
+    @classmethod
+    def pinned_zero(cls, field, m: int, n: int) -> "BitslicedMatrix":
+        """An all-zero page-locked host matrix (an `out` for the host-buffer path), written as
+        pin_memory's buffers are."""
+        if isinstance(field, str):
+            field = by_name(field)
+        with one_cpu_writer():
+            t = torch.zeros((field.bits, m, _words(n)), dtype=torch.int64, pin_memory=True)
+        return cls(field, m, n, t)
 
     def planes_numpy(self) -> np.ndarray:
         """The reference-layout planes as a host uint64 array of shape (R, m, W)."""
