@@ -20,8 +20,8 @@ L = _lib.load()
 dev = torch.device("cuda", 0)
 name, field, m, l, n = bench.CONFIGS[ci]
 f, A, B = bench.make_inputs(field, m, l, n, 0, dev, True)
-Ah, Bh = A.planes.cpu().pin_memory(), B.planes.cpu().pin_memory()
-Ch = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64).pin_memory()
+Ah, Bh = A.pin_memory().planes, B.pin_memory().planes  # written by one thread on one CPU
+Ch = A.pinned_zero(f, m, n).planes
 vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
 

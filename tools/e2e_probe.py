@@ -12,6 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+import paper_0901_1413_b200 as sg  # noqa: E402
 from paper_0901_1413_b200 import _lib  # noqa: E402
 
 
@@ -22,8 +23,8 @@ def main():
     dev = torch.device("cuda", 0)
     name, field, m, l, n = bench.CONFIGS[ci]
     f, A, B = bench.make_inputs(field, m, l, n, 0, dev, True)
-    Ah, Bh = A.planes.cpu().pin_memory(), B.planes.cpu().pin_memory()
-    Ch = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64).pin_memory()
+    Ah, Bh = A.pin_memory().planes, B.pin_memory().planes
+    Ch = sg.BitslicedMatrix.pinned_zero(f, m, n).planes
     vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     for _ in range(5):
         _lib.check(L.sg_m4rm_host(f.code, vp(Ah), vp(Bh), vp(Ch), m, l, n, 8, 0))
@@ -62,8 +63,8 @@ if __name__ == "__main__":
         dev = torch.device("cuda", 0)
         name, field, m, l, n = bench.CONFIGS[int(sys.argv[1])]
         f, A, B = bench.make_inputs(field, m, l, n, 0, dev, True)
-        Ah, Bh = A.planes.cpu().pin_memory(), B.planes.cpu().pin_memory()
-        Ch = torch.empty((f.bits, m, (n + 63) // 64), dtype=torch.int64).pin_memory()
+        Ah, Bh = A.pin_memory().planes, B.pin_memory().planes
+        Ch = sg.BitslicedMatrix.pinned_zero(f, m, n).planes
         vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
         os.environ.pop("SG_HOST_TRACE")
         for _ in range(5):
