@@ -108,3 +108,21 @@ def test_exports_cover_the_reference_hot_path_names():
                  "F7", "F8", "F9", "F25", "F27", "Z4", "Z8", "FIELDS", "EXT_FIELDS", "backend_name", "build_table",
                  "choose_k", "classical_multiply", "ext_multiply", "m4rm_multiply", "row_accumulate"):
         assert hasattr(sg, name), name
+
+
+def test_one_cpu_writer_restores_affinity_and_threads():
+    """BitslicedMatrix.pin_memory's writer context (CPU side): inside, the calling thread is on
+    one CPU and torch's CPU ops are single-threaded; both are restored on exit, also on error."""
+    import torch
+    from paper_0901_1413_b200.matrix import one_cpu_writer
+    if not hasattr(os, "sched_getaffinity"):
+        pytest.skip("no sched_getaffinity on this platform")
+    mask, threads = os.sched_getaffinity(0), torch.get_num_threads()
+    with one_cpu_writer():
+        assert len(os.sched_getaffinity(0)) == 1 and os.sched_getaffinity(0) <= mask
+        assert torch.get_num_threads() == 1
+    assert os.sched_getaffinity(0) == mask and torch.get_num_threads() == threads
+    with pytest.raises(RuntimeError):
+        with one_cpu_writer():
+            raise RuntimeError("boom")
+    assert os.sched_getaffinity(0) == mask and torch.get_num_threads() == threads
