@@ -7,6 +7,7 @@ namespace sg {
 static KernelInfo g_table[] = {
     SG_K(F5, 8, 8, 2, 256),
     SG_K(F5, 8, 4, 2, 256),
+    SG_KTM(F5, 8),  // 4096 rows per table: 8 row-slots in registers + 8 rotating through TMEM
     SG_KSET8(F5),
     SG_KFUSED(F5),
     SG_K(F5, 8, 8, 1, 256),

@@ -220,13 +220,38 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, u32 (&r)[16]) {
       : "r"(taddr)
       : "memory");
 }
-// one row-slot's accumulator words (4 x RS) to / from tensor memory
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const u32* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, u32* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr)
+               : "memory");
+}
+// one row-slot's accumulator words (4 x RS: 8, 16 or 20) to / from tensor memory
 template <int N> __device__ __forceinline__ void tmem_st(uint32_t taddr, u32 (&r)[N]) {
-  static_assert(N == 8 || N == 16, "8 or 16 accumulator words per row-slot");
-  if constexpr (N == 8) tmem_st8(taddr, r); else tmem_st16(taddr, r);
+  static_assert(N == 8 || N == 16 || N == 20, "8, 16 or 20 accumulator words per row-slot");
+  if constexpr (N == 8) {
+    tmem_st8(taddr, r);
+  } else if constexpr (N == 16) {
+    tmem_st16(taddr, r);
+  } else {
+    tmem_st16(taddr, *reinterpret_cast<u32(*)[16]>(&r[0]));
+    tmem_st4(taddr + 16, &r[16]);
+  }
 }
 template <int N> __device__ __forceinline__ void tmem_ld(uint32_t taddr, u32 (&r)[N]) {
-  if constexpr (N == 8) tmem_ld8(taddr, r); else tmem_ld16(taddr, r);
+  if constexpr (N == 8) {
+    tmem_ld8(taddr, r);
+  } else if constexpr (N == 16) {
+    tmem_ld16(taddr, r);
+  } else {
+    tmem_ld16(taddr, *reinterpret_cast<u32(*)[16]>(&r[0]));
+    tmem_ld4(taddr + 16, &r[16]);
+  }
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -638,12 +663,29 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // 2-plane field); tm_cur = the set currently in registers
   int tm_cur = 0;
   constexpr int SW = 4 * Traits<F>::RS;  // accumulator words (TMEM columns) per row-slot
+  // Two sets of RT slots (registers + one TMEM region each way) when two warps' two regions fit
+  // the 512 columns; otherwise (F5: 20-word slots) the rotation: row-slots in 4 groups of RT / 2,
+  // two groups in registers, two parked in 3 TMEM regions of RT / 2 slots (one free).
+  constexpr bool TM_ROT = TM && 4 * RT * SW > 512;
+  constexpr int TG = TM_ROT ? RT / 2 : RT;  // slots per TMEM region
   auto tm_addr = [&](int region, int t) -> uint32_t {
     const uint32_t base = *reinterpret_cast<const uint32_t*>(mbar_a + 3);
     const int w = tid >> 5;
-    return base + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(((w >> 2) * 2 + region) * RT * SW + t * SW);
+    return base + ((uint32_t)(32 * (w & 3)) << 16) +
+           (uint32_t)(((w >> 2) * (TM_ROT ? 3 : 2) + region) * TG * SW + t * SW);
   };
-  static_assert(!TM || 4 * RT * SW <= 512, "schedule 6: two sets of two warps per lane quarter in 512 columns");
+  static_assert(!TM || 2 * (TM_ROT ? 3 : 2) * TG * SW <= 512, "schedule 6: two warps' regions per lane quarter");
+  static_assert(!TM_ROT || RT % 2 == 0, "schedule 6 rotation: two register groups");
+  // TM_ROT state after k blocks: register groups A (c[0, TG)) and B (c[TG, RT)) hold logical
+  // groups gA, gB = 2 (k & 1) + 0, 1; groups gZ, gW = the other two are parked in TMEM regions
+  // rZ = -k mod 3, rW = rZ + 1 mod 3; region rF = rZ + 2 mod 3 is free (warp-uniform, from k)
+  struct Rot {
+    int gA, gB, gZ, gW, rZ, rW, rF;
+  };
+  auto rot = [](int k) {
+    const int par = k & 1, rz = (3 - k % 3) % 3;
+    return Rot{2 * par, 2 * par + 1, 2 - 2 * par, 3 - 2 * par, rz, (rz + 1) % 3, (rz + 2) % 3};
+  };
   auto acc8 = [](Acc<F>& x) -> u32(&)[SW] { return *reinterpret_cast<u32(*)[SW]>(&x.w[0][0]); };
 
   // Byte offsets of row-slot t's table entries for block s.  PAIR: row-slots 2j and 2j+1 share
@@ -693,26 +735,27 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 
   // lookups for block s from table buffer tb, software-pipelined LA row-slots ahead (entries
   // and table rows of t+1..t+LA in flight while t accumulates); `between(t)` runs after t.
-  constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4) ? 2 : 1;
-  // (TM: `set` selects the accumulator set in registers -- row-slots set * RT + t)
-  auto lookups = [&](int s, int tb, auto&& between, int set = 0) {
+  constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4 && !TM_ROT) ? 2 : 1;
+  // (general form: registers c[CB .. CB + N) hold row-slots so .. so + N; TM: `set` selects the
+  // accumulator set in registers -- row-slots set * RT + t)
+  auto lookups_part = [&](int s, int tb, auto&& between, int so, auto cb_ic, auto n_ic) {
+    constexpr int CB = decltype(cb_ic)::value, N = decltype(n_ic)::value;
     if constexpr (ABL & 4) {
 #pragma unroll
-      for (int t = 0; t < RT; ++t) between(t);
+      for (int t = 0; t < N; ++t) between(t);
       return;
     }
-    const int so = set * RT;
     const unsigned char* tl = tl0 + tb * TR * TPLANE;
     Rows<F> ring[LA + 1];
 #pragma unroll
-    for (int t = 0; t < LA && t < RT; ++t) {
+    for (int t = 0; t < LA && t < N; ++t) {
       u32 e[3];
       entries(s, so + t, e);
       load_rows<F, TPL, KAR>(ring[t], tl, e);
     }
 #pragma unroll
-    for (int t = 0; t < RT; ++t) {
-      if (t + LA < RT) {
+    for (int t = 0; t < N; ++t) {
+      if (t + LA < N) {
         u32 e[3];
         entries(s, so + t + LA, e);
         load_rows<F, TPL, KAR>(ring[(t + LA) % (LA + 1)], tl, e);
@@ -721,12 +764,15 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 #pragma unroll
         for (int w = 0; w < 4; ++w)
 #pragma unroll
-          for (int d = 0; d < Traits<F>::R; ++d) c[t].w[w][d] ^= comp(ring[t % (LA + 1)].v[0][d], w) ^ comp(ring[t % (LA + 1)].v[Traits<F>::NI - 1][d], w);
+          for (int d = 0; d < Traits<F>::R; ++d) c[CB + t].w[w][d] ^= comp(ring[t % (LA + 1)].v[0][d], w) ^ comp(ring[t % (LA + 1)].v[Traits<F>::NI - 1][d], w);
       } else {
-        accumulate<F, KAR>(c[t], ring[t % (LA + 1)]);
+        accumulate<F, KAR>(c[CB + t], ring[t % (LA + 1)]);
       }
       between(t);
     }
+  };
+  auto lookups = [&](int s, int tb, auto&& between, int set = 0) {
+    lookups_part(s, tb, between, set * RT, std::integral_constant<int, 0>{}, std::integral_constant<int, RT>{});
   };
 
   if constexpr (WS) {
@@ -831,7 +877,16 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       return;
     }
     // ------------------------------------------------ lookup warps (ROLE 2)
-    if constexpr (TM) {
+    using IC0 = std::integral_constant<int, 0>;
+    using ICG = std::integral_constant<int, TG>;
+    if constexpr (TM_ROT) {
+#pragma unroll
+      for (int t = 0; t < TG; ++t) {
+        tmem_st(tm_addr(0, t), acc8(c[t]));
+        tmem_st(tm_addr(1, t), acc8(c[t]));
+      }
+      tmem_wait_st();
+    } else if constexpr (TM) {
       // set 1 starts from the initial values (set 0, in registers, holds them too)
 #pragma unroll
       for (int t = 0; t < RT; ++t) tmem_st(tm_addr(1, t), acc8(c[t]));
@@ -839,7 +894,27 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     }
     for (int s = s_begin; s < s_end; ++s) {
       nbar_sync(FULL(s), NB);
-      if constexpr (TM) {
+      if constexpr (TM_ROT) {
+        const Rot r = rot(s - s_begin);
+        const int gA = r.gA, gB = r.gB, gZ = r.gZ, gW = r.gW, rZ = r.rZ, rW = r.rW, rF = r.rF;
+        // group A: park each slot in the free region, load Z's slot in its place; group B: park
+        // in Z's (now read) region, load W's; then Z and W from registers.  Z's region's loads
+        // were waited for before B's stores reuse it.
+        lookups_part(s, s & 1, [&](int t) {
+          tmem_st(tm_addr(rF, t), acc8(c[t]));
+          tmem_ld(tm_addr(rZ, t), acc8(c[t]));
+        }, gA * TG, IC0{}, ICG{});
+        tmem_wait_ld();
+        lookups_part(s, s & 1, [&](int t) {
+          tmem_st(tm_addr(rZ, t), acc8(c[TG + t]));
+          tmem_ld(tm_addr(rW, t), acc8(c[TG + t]));
+        }, gB * TG, ICG{}, ICG{});
+        tmem_wait_ld();
+        lookups_part(s, s & 1, [](int) {}, gZ * TG, IC0{}, ICG{});
+        lookups_part(s, s & 1, [](int) {}, gW * TG, ICG{}, ICG{});
+        // (now A, B hold gZ, gW; gA sits in rF, gB in rZ; rW is free: rot(k + 1))
+        tmem_wait_st();  // the next block's loads read what these stores wrote
+      } else if constexpr (TM) {
         // the set in registers; after each of its row-slots: park it in its TMEM region and
         // start loading the same slot of the other set (those loads land behind the remaining
         // slots' lookups), then the other set's lookups from the same table
@@ -925,15 +1000,17 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // ---- epilogue (row-slots set * RT + t from the registers; TM: both sets, the parked one
   // loaded back from tensor memory)
   SG_TL(2);
-  auto write_set = [&](int set) {
+  // registers c[CB .. CB + N) hold row-slots so .. so + N
+  auto write_part = [&](int so, auto cb_ic, auto n_ic) {
+    constexpr int CB = decltype(cb_ic)::value, N = decltype(n_ic)::value;
     if (mode == 2) {  // stream-K: compact slot [R][ROWS][4 words], canonical (summed by the reduce)
       u32* out = a.P2 + (int64_t)slot * R * ROWS * 4;
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int lr = (set * RT + t) * NT + tid;
+      for (int t = 0; t < N; ++t) {
+        const int lr = (so + t) * NT + tid;
         u32 o[4][R];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], true);
+        for (int w = 0; w < 4; ++w) finish<F>(c[CB + t].w[w], o[w], true);
 #pragma unroll
         for (int d = 0; d < R; ++d)
           *reinterpret_cast<uint4*>(out + ((int64_t)d * ROWS + lr) * 4) = make_uint4(o[0][d], o[1][d], o[2][d], o[3][d]);
@@ -947,12 +1024,12 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       rows_out = a.mpad;
     }
 #pragma unroll
-    for (int t = 0; t < RT; ++t) {
-      const int64_t row = row0 + (set * RT + t) * NT + tid;
+    for (int t = 0; t < N; ++t) {
+      const int64_t row = row0 + (so + t) * NT + tid;
       if (row < a.m) {
         u32 o[4][R];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) finish<F>(c[t].w[w], o[w], mode == 0);
+        for (int w = 0; w < 4; ++w) finish<F>(c[CB + t].w[w], o[w], mode == 0);
 #pragma unroll
         for (int d = 0; d < R; ++d) {
           u32* dst = out + ((int64_t)d * rows_out + row) * a.wc32 + word0;
@@ -962,7 +1039,26 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       }
     }
   };
-  if constexpr (TM) {
+  auto write_set = [&](int set) {
+    write_part(set * RT, std::integral_constant<int, 0>{}, std::integral_constant<int, RT>{});
+  };
+  if constexpr (TM_ROT) {
+    // (only the lookup warps get here in a WS kernel; the rotation state is theirs)
+    using IC0 = std::integral_constant<int, 0>;
+    using ICG = std::integral_constant<int, TG>;
+    const Rot r = rot(s_end - s_begin);
+    const int gA = r.gA, gB = r.gB, gZ = r.gZ, gW = r.gW, rZ = r.rZ, rW = r.rW;
+    write_part(gA * TG, IC0{}, ICG{});
+    write_part(gB * TG, ICG{}, ICG{});
+#pragma unroll
+    for (int t = 0; t < TG; ++t) {
+      tmem_ld(tm_addr(rZ, t), acc8(c[t]));
+      tmem_ld(tm_addr(rW, t), acc8(c[TG + t]));
+    }
+    tmem_wait_ld();
+    write_part(gZ * TG, IC0{}, ICG{});
+    write_part(gW * TG, ICG{}, ICG{});
+  } else if constexpr (TM) {
     write_set(tm_cur);
 #pragma unroll
     for (int t = 0; t < RT; ++t) tmem_ld(tm_addr(tm_cur ^ 1, t), acc8(c[t]));

@@ -95,6 +95,9 @@ const Calib g_calib[] = {
     {4, 32, 256, 6, 4370, 25000},
     // F7, schedule 6 (4096 rows per CTA): 16384 x 8192 x 16384 stream-K 12.55 ms (r02aj_step.txt)
     {3, 16, 256, 6, 6930, 25000},
+    // F5, schedule 6 (4096 rows per CTA, row-slots rotating through three TMEM regions):
+    // 8192^3 stream-K 3.468 ms, 4096^3 0.470 ms (profiles/r02ba_step.txt)
+    {2, 16, 256, 6, 7550, 25000},
     // fused one-launch variants (schedule + 10), from bench-style step times on small shapes
     // (tools/step_probe.py --grid, profiles/r02n_step_grid.jsonl; fit: tools/fit_calib.py)
     {1, 1, 256, 10, 1329, 0},  // max err 36%, 20 runs
