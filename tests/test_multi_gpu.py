@@ -46,6 +46,27 @@ def test_nccl_sharded_product_bit_identical_to_one_gpu_and_oracle():
         assert all(v for k, v in c.items() if k.startswith("eq_")), c
 
 
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 1, reason="needs a GPU")
+def test_nccl_one_rank_path():
+    """The same worker as one NCCL rank on one GPU (torch.distributed.run, world size 1): the
+    NCCL communicator, the chunked broadcast queued as async collectives, the SM reserve around
+    the chunk products, the in-field sum of the chunk products and the row gather all run on the
+    GPU, bit-identical to the single-GPU product and the oracle.  (World size > 1 needs more GPUs:
+    test_nccl_sharded_product_bit_identical_to_one_gpu_and_oracle.)"""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "_nccl_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
+    assert line, r.stdout[-2000:]
+    res = json.loads(line[-1][len("RESULT "):])
+    assert res["world"] == 1 and res["backend"] == "nccl"
+    assert len(res["results"]) == 12
+    for c in res["results"]:
+        assert all(v for k, v in c.items() if k.startswith("eq_")), c
+
+
 def test_bench_relaunch_command_and_world_check():
     """bench.py --gpus N without a launcher re-runs itself under torch.distributed.run with N
     ranks; a WORLD_SIZE that disagrees with --gpus is an error (exit 2), never a silent 1-GPU
