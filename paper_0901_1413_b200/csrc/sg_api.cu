@@ -294,6 +294,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
     sa.ready = sin->ready;
     sa.epoch = sin->epoch;
     sa.first_groups = sin->first_groups;
+    sa.cap_log = sin->cap_log;
     sa.nchunks = sin->nchunks;
     sa.poll_ns = sin->poll_ns;
     sa.perm = perm;

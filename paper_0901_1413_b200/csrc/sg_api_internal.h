@@ -90,7 +90,8 @@ int64_t workspace_bytes_for(const Plan& p, int field);
 struct StreamIn {
   const unsigned* ready;
   unsigned epoch;
-  int first_groups;  // B's chunk j = 4-block groups [g0 (2^j - 1), g0 (2^(j+1) - 1)), g0 = first_groups
+  int first_groups;  // B's chunk j = 4-block groups [chunk_lo(j), chunk_lo(j + 1)) (sg_internal.h)
+  int cap_log;       // chunks double from first_groups up to first_groups 2^cap_log, then stay
   int nchunks;
   unsigned poll_ns;
   unsigned* err;

@@ -139,20 +139,24 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   }
   unsigned* err = d->ready + MAX_BCHUNKS;
   const unsigned epoch = ++d->epoch;
-  // B chunks: whole 4-block groups (32 rows) in geometrically growing chunks, g0, 2 g0, 4 g0, ...
-  // (chunk j = groups [g0 (2^j - 1), g0 (2^(j+1) - 1))): the first chunk is small so the product
-  // starts early, later ones large so fewer copies pay the per-copy setup, and each arrives
-  // before the product needs it (the product consumes B at a steady rate while the upload's
-  // lead grows).  g0 = groups / 32 by default (F5 4096^3, tools/e2e_sweep.py: 4 of 128 groups
-  // 0.716 ms, 2: 0.725, 8: 0.776; equal chunks of 8-16 groups: 0.72).
+  // B chunks: whole 4-block groups (32 rows): g0, then chunks of 2 g0 (chunk_lo in sg_internal.h:
+  // sizes double from g0 up to g0 2^q; q = 1 by default).  The first chunk is small so the
+  // product starts early; after it every chunk is small enough that the product never waits
+  // long for one (B arrives at ~0.7 groups / us against ~0.5 consumed), and few enough that the
+  // per-copy setup stays small.  g0 = groups / 32 by default.  F5 4096^3, in-process A/B
+  // (profiles/r02bl_e2e_bcap_ab.txt): q = 1 0.687 ms, q = 2 0.697, doubling to the end
+  // (q = 20, the round-1 layout whose last chunk is half of B) 0.704, q = 0 (all g0) 0.733.
   const int64_t groups = (l + 31) / 32;
   const size_t b_bytes = (size_t)R * l * wc * 8;
   const char* g0_e = getenv("SG_HOST_BFIRST");  // experiments: groups in the first chunk
   int64_t g0 = g0_e ? atoll(g0_e) : (groups + 31) / 32;
   g0 = std::max<int64_t>(1, std::min<int64_t>(g0, groups));
-  auto chunk_lo = [&](int j) { return std::min<int64_t>(groups, g0 * (((int64_t)1 << j) - 1)); };
+  // SG_HOST_BCAP=q (experiments): chunks stop doubling at g0 2^q groups
+  const char* cap_e = getenv("SG_HOST_BCAP");
+  const int q = cap_e ? std::max(0, std::min(20, atoi(cap_e))) : 1;
+  auto chunk_lo_h = [&](int j) { return std::min<int64_t>(groups, sg::chunk_lo(j, (int)g0, q)); };
   int nch = 1;
-  while (chunk_lo(nch) < groups) ++nch;
+  while (chunk_lo_h(nch) < groups) ++nch;
   if (nch > MAX_BCHUNKS) return SG_EUNSUPPORTED;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   char* cur = dbuf;
@@ -214,7 +218,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   if ((rc = upload_a(0)) != SG_OK) return rc;
   const auto t_first = std::chrono::steady_clock::now();
   for (int j = 0; j < nch; ++j) {
-    const int64_t r0 = chunk_lo(j) * 32, rows = std::min<int64_t>(l, chunk_lo(j + 1) * 32) - r0;
+    const int64_t r0 = chunk_lo_h(j) * 32, rows = std::min<int64_t>(l, chunk_lo_h(j + 1) * 32) - r0;
     // Each flag goes out on its own stream behind its copy's event.  (Measured on B200: B's
     // chunks still arrive at ~30 GB/s against ~50 GB/s for one large copy -- every chunk pays
     // the copy setup; alternating two upload streams made the arrival order worse.)
@@ -232,7 +236,7 @@ int host_streamed(Io* d, char* dbuf, int field, const uint64_t* A, const uint64_
   for (int r = 1; r < Pr; ++r)
     if ((rc = upload_a(r)) != SG_OK) return rc;
   const char* poll_e = getenv("SG_HOST_POLL_NS");  // experiments: flag polling interval
-  const StreamIn sin{d->ready, epoch, (int)g0, nch, poll_e ? (unsigned)atoi(poll_e) : 100u, err};
+  const StreamIn sin{d->ready, epoch, (int)g0, q, nch, poll_e ? (unsigned)atoi(poll_e) : 100u, err};
   // SG_HOST_STREAM=2 (experiments): the streamed kernel on fully uploaded inputs (its cost
   // without any waiting, in a warm L2)
   if (const char* e = getenv("SG_HOST_STREAM"))

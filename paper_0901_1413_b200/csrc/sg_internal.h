@@ -78,15 +78,31 @@ struct M4rmArgs {
   int tma_a;           // ... and A's index words with 1-D bulk copies (with tma_b only)
 };
 // Streamed B (sg_m4rm_host; stream-K warp-specialized TMA plans, the STRM kernel instantiations):
-// B's chunk c -- 4-block groups [g0 (2^c - 1), g0 (2^(c+1) - 1)), g0 = first_groups: chunks
-// double in size -- may be read once ready[c] - epoch >= 0 (written by the upload stream behind
+// B's chunk c -- 4-block groups [chunk_lo(c), chunk_lo(c + 1)): chunks double in size from
+// g0 = first_groups up to g0 2^cap_log, then stay at that size -- may be read once ready[c] - epoch >= 0 (written by the upload stream behind
 // chunk c's copy).  perm: per tile, the order of its 4-block groups (virtual group
 // -> real group) that lets each segment start on blocks that arrive first.  err: set (to the
 // chunk + 1) when a wait times out; the product is then garbage and reported failed.
+// First 4-block group of B chunk c (g0 = first groups, chunks double up to g0 2^q, then equal);
+// chunk_of(g) inverts it.
+__host__ __device__ inline int64_t chunk_lo(int c, int g0, int q) {
+  return c <= q ? (int64_t)g0 * ((1LL << c) - 1) : (int64_t)g0 * (((1LL << q) - 1) + (int64_t)(c - q) * (1LL << q));
+}
+__host__ __device__ inline int chunk_of(int g, int g0, int q) {
+  const int64_t lq = (int64_t)g0 * ((1LL << q) - 1);
+  if (g < lq) {
+    const unsigned x = (unsigned)(g / g0 + 1);
+    int c = 0;
+    while ((2u << c) <= x) ++c;  // floor(log2(x))
+    return c;
+  }
+  return q + (int)((g - lq) / ((int64_t)g0 << q));
+}
 struct M4rmStreamArgs : M4rmArgs {
   const unsigned* ready;
   unsigned epoch;
   int first_groups;
+  int cap_log;
   int nchunks;
   unsigned poll_ns;  // sleep between two polls of a flag that has not landed
   const int* perm;

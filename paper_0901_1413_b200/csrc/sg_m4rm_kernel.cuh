@@ -489,10 +489,10 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
         if (s < s_end && t0 == 0) {
           const int rs = real_block(s);
           if constexpr (STRM) {
-            if ((rs >> 2) >= ready_groups) {  // chunk c = groups [g0 (2^c - 1), g0 (2^(c+1) - 1))
-              const int c = wait_chunk(a.ready, 31 - __clz((rs >> 2) / a.first_groups + 1), a.nchunks, a.epoch, a.err,
-                                       a.poll_ns);
-              ready_groups = a.first_groups * ((2 << c) - 1);
+            if ((rs >> 2) >= ready_groups) {  // chunk c = groups [chunk_lo(c), chunk_lo(c + 1))
+              const int c = wait_chunk(a.ready, chunk_of(rs >> 2, a.first_groups, a.cap_log), a.nchunks, a.epoch,
+                                       a.err, a.poll_ns);
+              ready_groups = (int)chunk_lo(c + 1, a.first_groups, a.cap_log);
             }
           }
           mbar_expect_tx(&mbar_b[s % 3], (unsigned)(K * R * 16));
