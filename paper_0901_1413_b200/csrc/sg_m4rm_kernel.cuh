@@ -738,7 +738,8 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4 && !TM_ROT) ? 2 : 1;
   // (general form: registers c[CB .. CB + N) hold row-slots so .. so + N; TM: `set` selects the
   // accumulator set in registers -- row-slots set * RT + t)
-  auto lookups_part = [&](int s, int tb, auto&& between, int so, auto cb_ic, auto n_ic) {
+  // `pre` runs after the first LA row-slots' table rows are on their way, before any accumulate
+  auto lookups_part = [&](int s, int tb, auto&& between, int so, auto cb_ic, auto n_ic, auto&& pre) {
     constexpr int CB = decltype(cb_ic)::value, N = decltype(n_ic)::value;
     if constexpr (ABL & 4) {
 #pragma unroll
@@ -753,6 +754,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       entries(s, so + t, e);
       load_rows<F, TPL, KAR>(ring[t], tl, e);
     }
+    pre();
 #pragma unroll
     for (int t = 0; t < N; ++t) {
       if (t + LA < N) {
@@ -771,8 +773,9 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       between(t);
     }
   };
+  auto nop = [] {};
   auto lookups = [&](int s, int tb, auto&& between, int set = 0) {
-    lookups_part(s, tb, between, set * RT, std::integral_constant<int, 0>{}, std::integral_constant<int, RT>{});
+    lookups_part(s, tb, between, set * RT, std::integral_constant<int, 0>{}, std::integral_constant<int, RT>{}, nop);
   };
 
   if constexpr (WS) {
@@ -900,20 +903,22 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
         // group A: park each slot in the free region, load Z's slot in its place; group B: park
         // in Z's (now read) region, load W's; then Z and W from registers.  Z's region's loads
         // were waited for before B's stores reuse it.
+        // The waits sit one row-slot late so that the last load's latency hides behind work that
+        // does not touch the loaded registers: Z's loads are waited for after B's first slot
+        // has accumulated (before its store reuses Z's region), W's after Z's lookups.
         lookups_part(s, s & 1, [&](int t) {
+          if (t == 0) tmem_wait_st();  // this block's loads read what the last block's stores wrote
           tmem_st(tm_addr(rF, t), acc8(c[t]));
           tmem_ld(tm_addr(rZ, t), acc8(c[t]));
-        }, gA * TG, IC0{}, ICG{});
-        tmem_wait_ld();
+        }, gA * TG, IC0{}, ICG{}, nop);
         lookups_part(s, s & 1, [&](int t) {
+          if (t == 0) tmem_wait_ld();
           tmem_st(tm_addr(rZ, t), acc8(c[TG + t]));
           tmem_ld(tm_addr(rW, t), acc8(c[TG + t]));
-        }, gB * TG, ICG{}, ICG{});
-        tmem_wait_ld();
-        lookups_part(s, s & 1, [](int) {}, gZ * TG, IC0{}, ICG{});
-        lookups_part(s, s & 1, [](int) {}, gW * TG, ICG{}, ICG{});
+        }, gB * TG, ICG{}, ICG{}, nop);
+        lookups_part(s, s & 1, [](int) {}, gZ * TG, IC0{}, ICG{}, nop);
+        lookups_part(s, s & 1, [](int) {}, gW * TG, ICG{}, ICG{}, [] { tmem_wait_ld(); });
         // (now A, B hold gZ, gW; gA sits in rF, gB in rZ; rW is free: rot(k + 1))
-        tmem_wait_st();  // the next block's loads read what these stores wrote
       } else if constexpr (TM) {
         // the set in registers; after each of its row-slots: park it in its TMEM region and
         // start loading the same slot of the other set (those loads land behind the remaining
@@ -922,9 +927,10 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
           tmem_st(tm_addr(tm_cur, t), acc8(c[t]));
           tmem_ld(tm_addr(tm_cur ^ 1, t), acc8(c[t]));
         }, tm_cur);
-        tmem_wait_ld();
         tm_cur ^= 1;
-        lookups(s, s & 1, [](int) {}, tm_cur);
+        // (the wait sits behind the other set's first table-row loads)
+        lookups_part(s, s & 1, [](int) {}, tm_cur * RT, std::integral_constant<int, 0>{},
+                     std::integral_constant<int, RT>{}, [] { tmem_wait_ld(); });
       } else {
         lookups(s, s & 1, [](int) {});
       }
@@ -1050,6 +1056,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
     const int gA = r.gA, gB = r.gB, gZ = r.gZ, gW = r.gW, rZ = r.rZ, rW = r.rW;
     write_part(gA * TG, IC0{}, ICG{});
     write_part(gB * TG, ICG{}, ICG{});
+    tmem_wait_st();  // the last block's stores
 #pragma unroll
     for (int t = 0; t < TG; ++t) {
       tmem_ld(tm_addr(rZ, t), acc8(c[t]));
