@@ -82,6 +82,9 @@ __device__ __forceinline__ void mbar_inval(uint64_t* bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred P1;\n LAB_WAIT:\n"
@@ -451,7 +454,11 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   uint64_t* mbar_b = reinterpret_cast<uint64_t*>(ast + NSLOT * NAP * ASZ);  // [3] B-slot barriers
   uint64_t* mbar_a = mbar_b + 3;                                               // [3] A-slot barriers
   // STRM only: this segment's tile's group order, staged by the builder warps ([ngroups] u16)
-  unsigned short* perm_s = reinterpret_cast<unsigned short*>(mbar_a + 3);
+  // warp-specialized schedules: FULL(s) = mbar_full[s & 1], every builder thread arrives, each
+  // lookup warp waits on its own (no barrier among the lookup warps: they may drift apart by up
+  // to the double-buffered table's one block)
+  uint64_t* mbar_full = mbar_a + 3;                                            // [2]
+  unsigned short* perm_s = reinterpret_cast<unsigned short*>(mbar_a + 5);
 
   const int tid = threadIdx.x;
   if (s_begin >= s_end) return;
@@ -666,10 +673,16 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   // Two sets of RT slots (registers + one TMEM region each way) when two warps' two regions fit
   // the 512 columns; otherwise (F5: 20-word slots) the rotation: row-slots in 4 groups of RT / 2,
   // two groups in registers, two parked in 3 TMEM regions of RT / 2 slots (one free).
-  constexpr bool TM_ROT = TM && 4 * RT * SW > 512;
+#ifndef SG_X_MBAR_FULL
+#define SG_X_MBAR_FULL 1
+#endif
+#ifndef SG_X_ROT_ALL
+#define SG_X_ROT_ALL 0
+#endif
+  constexpr bool TM_ROT = TM && (4 * RT * SW > 512 || SG_X_ROT_ALL);
   constexpr int TG = TM_ROT ? RT / 2 : RT;  // slots per TMEM region
   auto tm_addr = [&](int region, int t) -> uint32_t {
-    const uint32_t base = *reinterpret_cast<const uint32_t*>(mbar_a + 3);
+    const uint32_t base = *reinterpret_cast<const uint32_t*>(mbar_a + 5);
     const int w = tid >> 5;
     return base + ((uint32_t)(32 * (w & 3)) << 16) +
            (uint32_t)(((w >> 2) * (TM_ROT ? 3 : 2) + region) * TG * SW + t * SW);
@@ -735,7 +748,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 
   // lookups for block s from table buffer tb, software-pipelined LA row-slots ahead (entries
   // and table rows of t+1..t+LA in flight while t accumulates); `between(t)` runs after t.
-  constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4 && !TM_ROT) ? 2 : 1;
+  constexpr int LA = (RT >= 4 && Traits<F>::R * Traits<F>::NI <= 4 && !(TM_ROT && F == F5)) ? 2 : 1;
   // (general form: registers c[CB .. CB + N) hold row-slots so .. so + N; TM: `set` selects the
   // accumulator set in registers -- row-slots set * RT + t)
   // `pre` runs after the first LA row-slots' table rows are on their way, before any accumulate
@@ -781,6 +794,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
   if constexpr (WS) {
     constexpr int NBT = ws_builders(SCHED);
     constexpr int NB = NT + NBT;  // all threads take part in every FULL / EMPTY barrier
+    constexpr bool MBF = SG_X_MBAR_FULL && ws_tma(SCHED);
     auto FULL = [](int s) { return 1 + (s & 1); };
     auto EMPTY = [](int s) { return 3 + (s & 1); };
     if constexpr (ROLE == 1) {
@@ -874,7 +888,9 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
           if (tma_a) wait_a(s);
           else cp_async_wait<0>();
         }
-        nbar_arrive(FULL(s), NB);  // table of block s (and A words of s) ready
+        // table of block s (and A words of s) ready
+        if constexpr (MBF) mbar_arrive(&mbar_full[s & 1]);
+        else nbar_arrive(FULL(s), NB);
       }
       cp_async_wait<0>();
       return;
@@ -896,7 +912,8 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
       tmem_wait_st();
     }
     for (int s = s_begin; s < s_end; ++s) {
-      nbar_sync(FULL(s), NB);
+      if constexpr (MBF) mbar_wait(&mbar_full[s & 1], (unsigned)((s - s_begin) >> 1) & 1u);
+      else nbar_sync(FULL(s), NB);
       if constexpr (TM_ROT) {
         const Rot r = rot(s - s_begin);
         const int gA = r.gA, gB = r.gB, gZ = r.gZ, gW = r.gW, rZ = r.rZ, rW = r.rW, rF = r.rF;
@@ -1113,11 +1130,17 @@ __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB
     u += s1 - s0;
     cp_async_wait<0>();
     __syncthreads();  // shared memory is reused by the next segment
-    if (TMA_OK && a.tma_b) {  // fresh barriers: the next segment counts its phases from zero
+    if constexpr (ws_tma(SCHED)) {  // fresh barriers: the next segment counts its phases from zero
       if (threadIdx.x == 0) {
-        for (int i = 0; i < 6; ++i) {
+        if (TMA_OK && a.tma_b) {
+          for (int i = 0; i < 6; ++i) {
+            mbar_inval(&mbar[i]);
+            mbar_init(&mbar[i], 1);
+          }
+        }
+        for (int i = 6; i < 8; ++i) {
           mbar_inval(&mbar[i]);
-          mbar_init(&mbar[i], 1);
+          mbar_init(&mbar[i], ws_builders(SCHED));
         }
         fence_mbar_init();
       }
@@ -1213,9 +1236,11 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
                                                (half_bufs(SCHED) * 2 * 16 * R * 4 + 3 * K * R * 4 +
                                                 index_stage_words<F, K, RT, NT, FUSED, SCHED>()) * 4);
   constexpr bool TMA_OK = ws_tma(SCHED) && K == 8;
-  if (TMA_OK && a.tma_b) {
+  if constexpr (ws_tma(SCHED)) {
     if (threadIdx.x == 0) {
-      for (int i = 0; i < 6; ++i) mbar_init(&mbar[i], 1);  // 3 B slots, 3 A slots
+      if (TMA_OK && a.tma_b)
+        for (int i = 0; i < 6; ++i) mbar_init(&mbar[i], 1);  // 3 B slots, 3 A slots
+      for (int i = 6; i < 8; ++i) mbar_init(&mbar[i], ws_builders(SCHED));  // FULL of the two table buffers
       fence_mbar_init();
     }
     __syncthreads();
@@ -1228,11 +1253,14 @@ __global__ void __launch_bounds__(NT + ws_builders(SCHED), (min_ctas_per_sm<F, R
     // need the registers, its lookups fit in 216; F7 and GF(4) lost 1-2 % with the same split.
     // The streamed-B variant's builders also check chunk flags: at least 64 for them.)
     constexpr int NBT = ws_builders(SCHED), PER = 65536 / (NT + NBT) / 8 * 8;
-    constexpr int BREGS = SCHED == 5 ? 64 : F == F5 ? 72 : STRM ? 64 : 56;
+#ifndef SG_X_F5_BREGS6
+#define SG_X_F5_BREGS6 64
+#endif
+    constexpr int BREGS = SCHED == 5 ? 64 : F == F5 ? (SCHED == 6 ? SG_X_F5_BREGS6 : 72) : STRM ? 64 : 56;
     constexpr int LREGS = (PER * (NT + NBT) - BREGS * NBT) / NT / 8 * 8;
     // schedule 6: warp 0 allocates all 512 TMEM columns (one CTA per SM) for the lookup warps'
     // second accumulator sets; its address goes to the word after the mbarriers
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 6);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 8);
     if constexpr (SCHED == 6) {
       if (threadIdx.x < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
@@ -1270,7 +1298,7 @@ constexpr int smem_bytes_for() {
   constexpr int R = Traits<F>::R;
   return (SCHED >= 1 ? 2 : 1) * table_planes<F, K>() * (1 << K) * ENTRY_BYTES + half_bufs(SCHED) * 2 * 16 * R * 4 * 4 +
          3 * K * R * 4 * 4 +
-         index_stage_words<F, K, RT, NT, FUSED, SCHED>() * 4 + 6 * 8 +  // + the B- and A-slot mbarriers
+         index_stage_words<F, K, RT, NT, FUSED, SCHED>() * 4 + 8 * 8 +  // + the B- / A-slot and FULL mbarriers
          (SCHED == 6 ? 16 : 0);                                         // + the TMEM address (schedule 6)
 }
 
