@@ -228,10 +228,12 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       const int rpw = field == SG_F2 ? 4 : planes(field) == 3 ? 1 : 2;
       const double l2_set = (double)((nblocks + rpw - 1) / rpw) * rgroups * rows * 4.0 + (double)R * l * wc32 * 4.0;
       const bool short_ranges = (units + G - 1) / G <= 2 * (int64_t)nblocks - 1;
-      // (schedule 6: ranges over at most two row groups are fine too -- F3 16384 x 32768^2
-      // stream-K 39.0 ms against 43.8 split-K; at four row groups split-K wins by 1.5 %)
+      // (schedule 6: ranges over up to four row groups are fine too -- F3 16384 x 32768^2
+      // stream-K 39.0 ms against 43.8 split-K; at four row groups, 32768^3, stream-K 72.9 ms
+      // against 74.0 since the lookup warps wait on the FULL mbarrier warp by warp -- before that
+      // split-K won there by 1.5 %)
       const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 && units >= G &&
-                      (short_ranges || l2_set <= 120e6 || g_override_splits == -1 || (ki->sched == 6 && rgroups <= 2));
+                      (short_ranges || l2_set <= 120e6 || g_override_splits == -1 || (ki->sched == 6 && rgroups <= 4));
       if (ok) {
         const double per = (double)(units + G - 1) / G;
         const double nseg = std::min(2.0, per) + std::floor(per / nblocks);  // segments per CTA
