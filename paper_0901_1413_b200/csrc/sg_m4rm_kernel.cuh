@@ -234,11 +234,16 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, u32* r) {
                : "r"(taddr)
                : "memory");
 }
-// one row-slot's accumulator words (4 x RS: 8, 16 or 20) to / from tensor memory
+// one row-slot's accumulator words (4 x RS: 4, 8, 12, 16 or 20) to / from tensor memory
 template <int N> __device__ __forceinline__ void tmem_st(uint32_t taddr, u32 (&r)[N]) {
-  static_assert(N == 8 || N == 16 || N == 20, "8, 16 or 20 accumulator words per row-slot");
-  if constexpr (N == 8) {
+  static_assert(N == 4 || N == 8 || N == 12 || N == 16 || N == 20, "4, 8, 12, 16 or 20 accumulator words per row-slot");
+  if constexpr (N == 4) {
+    tmem_st4(taddr, &r[0]);
+  } else if constexpr (N == 8) {
     tmem_st8(taddr, r);
+  } else if constexpr (N == 12) {
+    tmem_st8(taddr, *reinterpret_cast<u32(*)[8]>(&r[0]));
+    tmem_st4(taddr + 8, &r[8]);
   } else if constexpr (N == 16) {
     tmem_st16(taddr, r);
   } else {
@@ -247,8 +252,13 @@ template <int N> __device__ __forceinline__ void tmem_st(uint32_t taddr, u32 (&r
   }
 }
 template <int N> __device__ __forceinline__ void tmem_ld(uint32_t taddr, u32 (&r)[N]) {
-  if constexpr (N == 8) {
+  if constexpr (N == 4) {
+    tmem_ld4(taddr, &r[0]);
+  } else if constexpr (N == 8) {
     tmem_ld8(taddr, r);
+  } else if constexpr (N == 12) {
+    tmem_ld8(taddr, *reinterpret_cast<u32(*)[8]>(&r[0]));
+    tmem_ld4(taddr + 8, &r[8]);
   } else if constexpr (N == 16) {
     tmem_ld16(taddr, r);
   } else {

@@ -5,6 +5,7 @@
 namespace sg {
 
 static KernelInfo g_table[] = {
+    SG_KTM(Z4, 16),  // 8192 rows per table: 16 row-slots in registers + 16 in tensor memory
     SG_K(Z4, 8, 16, 2, 256),
     SG_K(Z4, 8, 8, 2, 256),
     SG_KSET8(Z4),

@@ -5,6 +5,7 @@
 namespace sg {
 
 static KernelInfo g_table[] = {
+    SG_KTM(Z8, 8),  // 4096 rows per table: 8 row-slots in registers + 8 in tensor memory
     SG_K(Z8, 8, 8, 2, 256),
     SG_K(Z8, 8, 4, 2, 256),
     SG_KSET8(Z8),

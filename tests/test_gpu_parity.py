@@ -181,19 +181,20 @@ def test_fused_small_plans(fname):
     assert ran >= 30
 
 
-@pytest.mark.parametrize("fname", ["f3", "gf4", "f7", "f5"])
+@pytest.mark.parametrize("fname", ["f3", "gf4", "f7", "f5", "gf8", "z8", "z4", "f2"])
 def test_tmem_accumulator_variant(fname):
     """Schedule 6: a second set of row-slots per lookup thread parked in tensor memory (F3 /
-    GF(4) 16 + 16 = 8192 rows per table, F7 8 + 8 = 4096; F5 8 + 8 with the row-slots rotating
-    through three TMEM regions in groups of 4; GF(4), F7 and F5 with just-in-time index staging
-    in two slots); forced split-K and stream-K plans on ragged shapes, bit-identical."""
+    GF(4) / Z4 / F2 16 + 16 = 8192 rows per table, F7 / GF(8) / Z8 8 + 8 = 4096; F5 8 + 8 with the
+    row-slots rotating through three TMEM regions in groups of 4; the three-plane fields and
+    GF(4) with just-in-time index staging in two slots); forced split-K and stream-K plans on
+    ragged shapes, bit-identical."""
     ran = 0
     for (m, l, n) in [(700, 1001, 777), (8200, 1000, 768), (16384, 512, 512), (3000, 64, 1000), (9000, 40, 2000)]:
         A = oracle.random_dense(fname, m, l, m + 11)
         B = oracle.random_dense(fname, l, n, n + 12)
         want = expect(fname, A, B)
         for splits in (1, 2, 5, -1):
-            rt = 16 if fname in ("f7", "f5") else 32  # row-slots per thread, both sets
+            rt = 16 if fname in ("f7", "f5", "gf8", "z8") else 32  # row-slots per thread, both sets
             m4rm_mod.set_plan_override(rt, splits, 6, 256)
             try:
                 p = m4rm_mod.plan(fname, m, l, n)
