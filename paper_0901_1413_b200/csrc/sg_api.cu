@@ -285,6 +285,7 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
   if (sin && !a.tma_b) return fail(SG_EINVAL, "streamed B needs the TMA staging path");
   a.streamk = p.streamk;
   a.units = p.units;
+  a.dp_tiles = p.dp_tiles;
   a.slabs = p.slabs;
   a.P2 = p.streamk ? partial : nullptr;
   if (p.streamk) a.C = (uint32_t*)C;
@@ -307,8 +308,8 @@ int m4rm_device(int field, const uint64_t* A, const uint64_t* B, uint64_t* C, in
   g_launches++;
   if (g_timing) cudaEventRecord(ev[2], st);
   if (p.streamk) {
-    SG_CUDA(launch_reduce_streamk(field, partial, (uint32_t*)C, m, p.wc32, p.rows, p.slabs, p.tiles, p.nblocks,
-                                  p.units, (int)p.grid.x, st),
+    SG_CUDA(launch_reduce_streamk(field, partial, (uint32_t*)C, m, p.wc32, p.rows, p.slabs, p.tiles - p.dp_tiles,
+                                  p.dp_tiles, p.nblocks, p.units, (int)p.grid.x, st),
             "sg_m4rm stream-K reduce");
     g_launches++;
   } else if (p.splits > 1) {

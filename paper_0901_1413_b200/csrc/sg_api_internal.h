@@ -72,6 +72,7 @@ struct Plan {
   int at_words = 0, at_planes = 0;  // staged index array: k=8 packed words (1 plane), else A^T planes
   bool streamk = false;              // one wave of CTAs over tiles x k-blocks (see m4rm_kernel)
   int64_t units = 0, tiles = 0;
+  int64_t dp_tiles = 0;              // stream-K hybrid: leading tiles processed whole (units cover the rest)
   int slabs = 0, rows = 0;
   dim3 grid;
   double est_clk = 0;

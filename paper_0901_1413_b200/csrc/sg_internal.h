@@ -70,6 +70,8 @@ struct M4rmArgs {
   // stream-K (partial = 0): CTA c covers work units [c U / G, (c+1) U / G) of U = tiles x nblocks
   int streamk;
   int64_t units;
+  int64_t dp_tiles;    // stream-K hybrid: tiles [0, dp_tiles) go whole, CTA c takes c, c + G, ...; the
+                       // units cover tiles [dp_tiles, tiles) only
   int slabs;           // tiles = slabs x row groups, tile t -> slab t % slabs, row group t / slabs
   uint32_t* P2;        // compact stream-K partials [G * SK_SLOTS][R][ROWS][4]
   int early_trigger;   // experiments (SG_PDL=2): release the dependent reduction at kernel start
@@ -172,7 +174,8 @@ cudaError_t launch_sum_slices(int field, const SliceSet& s, uint32_t* out, int64
 cudaError_t launch_reduce_splits(int field, const uint32_t* P, uint32_t* C, int64_t m, int64_t mpad,
                                  int wc32, int splits, cudaStream_t st);
 cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,
-                                  int slabs, int64_t tiles, int nblocks, int64_t units, int ctas, cudaStream_t st);
+                                  int slabs, int64_t tiles, int64_t tile0, int nblocks, int64_t units, int ctas,
+                                  cudaStream_t st);
 
 // load every auxiliary kernel of `field` (index pre-pass, reductions) ahead of a streamed product
 cudaError_t preload_aux_kernels(int field);

@@ -221,15 +221,15 @@ cudaError_t launch_sum_slices(int field, const SliceSet& s, uint32_t* out, int64
 // Tiles with more than 64 contributors (forced stream-K plans with a few units per CTA).
 template <int F>
 __device__ __noinline__ void reduce_streamk_tile_slow(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m,
-                                                      int wc32, int rows_cta, int slabs, int64_t t, int nb,
-                                                      int64_t U, int G) {
+                                                      int wc32, int rows_cta, int slabs, int64_t t, int64_t tile0,
+                                                      int nb, int64_t U, int G) {
   constexpr int R = Traits<F>::R;
   const int64_t lo = t * nb, hi = lo + nb;
   int64_t c0 = lo * G / U;
   while (c0 > 0 && c0 * U / G > lo) --c0;
   while ((c0 + 1) * U / G <= lo) ++c0;
-  const int64_t row0 = (t / slabs) * rows_cta;
-  const int word0 = (int)(t % slabs) * SLAB_WORDS;
+  const int64_t row0 = ((tile0 + t) / slabs) * rows_cta;
+  const int word0 = (int)((tile0 + t) % slabs) * SLAB_WORDS;
   for (int lr = blockIdx.y * blockDim.x + threadIdx.x; lr < rows_cta; lr += gridDim.y * blockDim.x) {
     const int64_t row = row0 + lr;
     if (row >= m) break;
@@ -262,11 +262,12 @@ __device__ __noinline__ void reduce_streamk_tile_slow(const u32* __restrict__ P2
 
 template <int F>
 __global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restrict__ P2, u32* __restrict__ C, int64_t m,
-                                                             int wc32, int rows_cta, int slabs, int64_t tiles, int nb,
-                                                             int64_t U, int G) {
+                                                             int wc32, int rows_cta, int slabs, int64_t tiles,
+                                                             int64_t tile0, int nb, int64_t U, int G) {
   constexpr int R = Traits<F>::R;
   pdl_wait();  // launched with PDL behind the product kernel
-  // blockIdx.x = tile; the slots of the CTAs whose unit ranges touch it are listed once per block
+  // blockIdx.x = tile among the stream-K tiles (tile0 + blockIdx.x of the product: tiles below tile0
+  // were written whole by the product kernel); the slots of the CTAs whose unit ranges touch it are listed once per block
   constexpr int MAXS = 64;
   const int64_t t = blockIdx.x;
   __shared__ int slots[MAXS + 1];  // [0] = count (0: the tile was written by the product kernel)
@@ -291,11 +292,11 @@ __global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restri
   const int n = slots[0];
   if (n == 0) return;
   if (n > MAXS) {  // very short CTA ranges (forced plans): enumerate per thread
-    reduce_streamk_tile_slow<F>(P2, C, m, wc32, rows_cta, slabs, t, nb, U, G);
+    reduce_streamk_tile_slow<F>(P2, C, m, wc32, rows_cta, slabs, t, tile0, nb, U, G);
     return;
   }
-  const int64_t row0 = (t / slabs) * rows_cta;
-  const int word0 = (int)(t % slabs) * SLAB_WORDS;
+  const int64_t row0 = ((tile0 + t) / slabs) * rows_cta;
+  const int word0 = (int)((tile0 + t) % slabs) * SLAB_WORDS;
   for (int lr = blockIdx.y * blockDim.x + threadIdx.x; lr < rows_cta; lr += gridDim.y * blockDim.x) {
     const int64_t row = row0 + lr;
     if (row >= m) break;
@@ -352,11 +353,12 @@ __global__ void __launch_bounds__(256) reduce_streamk_kernel(const u32* __restri
 }
 
 cudaError_t launch_reduce_streamk(int field, const uint32_t* P2, uint32_t* C, int64_t m, int wc32, int rows_cta,
-                                  int slabs, int64_t tiles, int nblocks, int64_t units, int ctas, cudaStream_t st) {
+                                  int slabs, int64_t tiles, int64_t tile0, int nblocks, int64_t units, int ctas,
+                                  cudaStream_t st) {
   if (tiles <= 0) return cudaSuccess;
   const dim3 grid((unsigned)tiles, (unsigned)((rows_cta + 255) / 256));
 #define SG_RK(FF) return launch_pdl(reduce_streamk_kernel<FF>, grid, dim3(256), 0, st, P2, C, m, wc32, rows_cta, \
-                                 slabs, tiles, nblocks, units, ctas)
+                                 slabs, tiles, tile0, nblocks, units, ctas)
   SG_FOR_EACH_FIELD_CASE(field, SG_RK)
 #undef SG_RK
   return cudaGetLastError();

@@ -1104,7 +1104,7 @@ __device__ __forceinline__ void m4rm_segment(const AT& a, const CUtensorMap* tmB
 }
 
 // All of this CTA's segments.  Stream-K: CTA c owns work units [c U / G, (c+1) U / G) of
-// U = tiles x k-blocks: a partial tail of one tile, whole tiles, a partial head of another; the
+// U = (tiles - dp_tiles) x k-blocks (after its whole tiles c, c + G, ... < dp_tiles): a partial tail of one tile, whole tiles, a partial head of another; the
 // partial segments land in compact slots and reduce_streamk sums the slots of every tile.  Otherwise one segment
 // per CTA: (slab, row group, k-split) = blockIdx.
 template <int F, int K, int RT, int SCHED, int NT, int ABL, int ROLE, bool STRM, typename AT>
@@ -1123,23 +1123,10 @@ __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB
                                                        : (int)blockIdx.z);
     return;
   }
-  const int64_t U = a.units, G = gridDim.x;
-  const int64_t u0 = blockIdx.x * U / G;
-  const int64_t u1 = (blockIdx.x + 1) * U / G;
-  for (int64_t u = u0; u < u1;) {
-    const int64_t tile = u / a.nblocks;
-    const int s0 = (int)(u - tile * a.nblocks);
-    const int64_t room = u1 - u;
-    const int s1 = (int)(s0 + room < a.nblocks ? s0 + room : (int64_t)a.nblocks);
-    // a whole tile goes straight to C; a partial one (only the range's first or last segment can
-    // be partial) to compact slot 2c (first) or 2c + 1 (last), summed by reduce_streamk_kernel
-    const bool whole = s0 == 0 && s1 == a.nblocks;
-    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE, STRM>(a, tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS,
-                                                 (tile / a.slabs) * ROWS, s0, s1, whole ? 0 : 2,
-                                                 (int)(blockIdx.x * SK_SLOTS + (u == u0 ? 0 : 1)));
-    u += s1 - s0;
+  // shared memory and the barriers are reused by the next segment
+  auto next_segment = [&] {
     cp_async_wait<0>();
-    __syncthreads();  // shared memory is reused by the next segment
+    __syncthreads();
     if constexpr (ws_tma(SCHED)) {  // fresh barriers: the next segment counts its phases from zero
       if (threadIdx.x == 0) {
         if (TMA_OK && a.tma_b) {
@@ -1156,6 +1143,42 @@ __device__ __forceinline__ void run_segments(const AT& a, const CUtensorMap* tmB
       }
       __syncthreads();
     }
+  };
+  const int64_t U = a.units, G = gridDim.x;
+  // Hybrid: with at least one tile per CTA, tiles [0, dp_tiles) (a multiple of G) go whole, CTA c
+  // taking c, c + G, ...: every CTA then walks the k-blocks of neighbouring tiles at the same
+  // time, so B's rows and A's index words of a k-block are fetched once into L2 for the whole
+  // wave (pure stream-K scatters the CTAs over all of k: F3 32768^3 read 72 GB from HBM per
+  // launch against 2 GB).  Only the last, partial wave -- tiles [dp_tiles, tiles) -- is cut
+  // into unit ranges.
+  // (one call site for both kinds of segment: the segment code is inlined once)
+  const int64_t u0 = blockIdx.x * U / G;
+  const int64_t u1 = (blockIdx.x + 1) * U / G;
+  int64_t dpt = blockIdx.x, u = u0;
+  for (;;) {
+    int64_t tile;
+    int s0, s1, mode, slot;
+    if (dpt < a.dp_tiles) {  // a whole tile of the leading waves
+      tile = dpt;
+      dpt += G;
+      s0 = 0, s1 = a.nblocks, mode = 0, slot = 0;
+    } else if (u < u1) {
+      const int64_t tl = u / a.nblocks;  // among the stream-K tiles
+      tile = a.dp_tiles + tl;
+      s0 = (int)(u - tl * a.nblocks);
+      const int64_t room = u1 - u;
+      s1 = (int)(s0 + room < a.nblocks ? s0 + room : (int64_t)a.nblocks);
+      // a whole tile goes straight to C; a partial one (only the range's first or last segment
+      // can be partial) to compact slot 2c (first) or 2c + 1 (last), summed by reduce_streamk_kernel
+      mode = s0 == 0 && s1 == a.nblocks ? 0 : 2;
+      slot = (int)(blockIdx.x * SK_SLOTS + (u == u0 ? 0 : 1));
+      u += s1 - s0;
+    } else {
+      break;
+    }
+    m4rm_segment<F, K, RT, SCHED, NT, ABL, ROLE, STRM>(a, tmB, smem, (int)(tile % a.slabs) * SLAB_WORDS,
+                                                 (tile / a.slabs) * ROWS, s0, s1, mode, slot);
+    next_segment();
   }
 }
 

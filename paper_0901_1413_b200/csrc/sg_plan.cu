@@ -122,6 +122,12 @@ const Calib g_calib[] = {
     {4, 4, 256, 11, 2386, 7073},  // max err 18%, 17 runs
 };
 
+// experiments: SG_STREAMK_HYBRID=0 plans pure stream-K ranges (no whole-tile waves)
+static const bool g_streamk_hybrid = [] {
+  const char* e = getenv("SG_STREAMK_HYBRID");
+  return !e || atoi(e) != 0;
+}();
+
 const Calib* calib_for(const KernelInfo* ki) {
   if (ki->k != 8) return nullptr;
   const int sched = ki->sched + (ki->fn_fused ? SCHED_FUSED : 0);
@@ -221,22 +227,25 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
       // stream-K candidate: one wave of SMs x occupancy CTAs, each owning U / G consecutive
       // (tile, k-block) units, then a compact reduction of the partially covered tiles
       const int64_t G = (int64_t)ds.sms * occ;
+      // Hybrid: with at least one tile per CTA the leading tiles/G whole waves go tile by tile
+      // (CTA c: tiles c, c + G, ...), all CTAs walking the k-blocks of neighbouring tiles together,
+      // and only the last, partial wave is cut into unit ranges -- pure stream-K ranges of several
+      // tiles scatter the concurrent CTAs over all of k and the row groups, and B and A's index
+      // words then stream from HBM for every tile (F3 32768^3: 72 GB per launch against 2 GB).
+      const int64_t dp = g_streamk_hybrid && G > 0 && tiles >= G ? tiles / G * G : 0;
+      const int64_t units_sk = (tiles - dp) * nblocks;
       // a CTA's range: partial tail, whole tiles, partial head (one segment boundary each).  Ranges
-      // of more than ~2 tiles scatter the concurrent CTAs over row groups, so they are planned only
-      // when A's index words and B fit in L2 together (measured: F7 16384x8192x16384 -1.7 %,
-      // F3 32768^3 +1.7 % where they do not); forced plans (splits = -1) take any range.
+      // of more than ~2 tiles (no hybrid: fewer tiles than CTAs never have them) are planned only
+      // when A's index words and B fit in L2 together; forced plans (splits = -1) take any range.
       const int rpw = field == SG_F2 ? 4 : planes(field) == 3 ? 1 : 2;
       const double l2_set = (double)((nblocks + rpw - 1) / rpw) * rgroups * rows * 4.0 + (double)R * l * wc32 * 4.0;
-      const bool short_ranges = (units + G - 1) / G <= 2 * (int64_t)nblocks - 1;
-      // (schedule 6: ranges over up to four row groups are fine too -- F3 16384 x 32768^2
-      // stream-K 39.0 ms against 43.8 split-K; at four row groups, 32768^3, stream-K 72.9 ms
-      // against 74.0 since the lookup warps wait on the FULL mbarrier warp by warp -- before that
-      // split-K won there by 1.5 %)
+      const bool short_ranges = G > 0 && (units_sk + G - 1) / G <= 2 * (int64_t)nblocks - 1;
       const bool ok = K == 8 && (g_override_splits == 0 || g_override_splits == -1) && G > 0 && units >= G &&
                       (short_ranges || l2_set <= 120e6 || g_override_splits == -1 || (ki->sched == 6 && rgroups <= 4));
       if (ok) {
-        const double per = (double)(units + G - 1) / G;
-        const double nseg = std::min(2.0, per) + std::floor(per / nblocks);  // segments per CTA
+        const double per = (double)(units + G - 1) / G, per_sk = (double)(units_sk + G - 1) / G;
+        // segments per CTA: its whole tiles, then the ends of its unit range
+        const double nseg = (double)(dp / G) + (units_sk ? std::min(2.0, per_sk) + std::floor(per_sk / nblocks) : 0.0);
         const double t_cta = cal ? per * cal->blk + nseg * cal->cta : 1.25 * (per * t_block + 3000.0 * nseg);
         const double bytes = (double)G * 2.0 * R * rows * 16.0 + (double)R * m * wc32 * 4.0;
         // occ co-resident CTAs share the SM, as in the split-K estimate below
@@ -249,7 +258,8 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
           best.bps = nblocks;
           best.mpad = rgroups * rows;
           best.streamk = true;
-          best.units = units;
+          best.units = units_sk;
+          best.dp_tiles = dp;
           best.tiles = tiles;
           best.slabs = (int)slabs;
           best.rows = rows;
@@ -286,6 +296,7 @@ int make_plan_uncached(int field, int64_t m, int64_t l, int64_t n, int k, int de
         best.bps = bps;
         best.mpad = rgroups * rows;
         best.streamk = false;
+        best.dp_tiles = 0;
         best.grid = dim3((unsigned)slabs, (unsigned)rgroups, (unsigned)splits);
       }
     }
@@ -350,7 +361,7 @@ int64_t workspace_bytes_for(const Plan& p, int field) {
 // One stream-K wave of the warp-specialized kernel: its builder warps stage every k-block by
 // TMA, so they can wait for each block's chunk; the 4-block group order needs nblocks % 4 == 0.
 bool streamable(const Plan& p) {
-  return p.streamk && ws_tma(p.ki->sched) && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 &&
+  return p.streamk && p.dp_tiles == 0 && ws_tma(p.ki->sched) && p.ki->fn_stream && p.K == 8 && p.wc32 % 4 == 0 && p.nblocks % 4 == 0 &&
          p.tiles > 0 && p.nblocks / 4 <= STRM_MAX_GROUPS && (int64_t)p.tiles * (p.nblocks / 4) <= (int64_t)1 << 24;
 }
 
