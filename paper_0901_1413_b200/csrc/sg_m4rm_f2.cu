@@ -6,6 +6,7 @@ namespace sg {
 
 static KernelInfo g_table[] = {
     SG_KTM(F2, 16),  // 8192 rows per table: 16 row-slots in registers + 16 in tensor memory
+    SG_KTM(F2, 32),  // 16384 rows per table: 32 + 32 (one-plane slots: 4 words each)
     SG_K(F2, 8, 16, 2, 256),
     SG_KSET8(F2),
     SG_KFUSED(F2),

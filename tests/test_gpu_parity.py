@@ -189,12 +189,13 @@ def test_tmem_accumulator_variant(fname):
     GF(4) with just-in-time index staging in two slots); forced split-K and stream-K plans on
     ragged shapes, bit-identical."""
     ran = 0
-    for (m, l, n) in [(700, 1001, 777), (8200, 1000, 768), (16384, 512, 512), (3000, 64, 1000), (9000, 40, 2000)]:
+    for (m, l, n) in [(700, 1001, 777), (8200, 1000, 768), (16384, 512, 512), (3000, 64, 1000), (9000, 40, 2000), (20000, 300, 640)]:
         A = oracle.random_dense(fname, m, l, m + 11)
         B = oracle.random_dense(fname, l, n, n + 12)
         want = expect(fname, A, B)
-        for splits in (1, 2, 5, -1):
-            rt = 16 if fname in ("f7", "f5", "gf8", "z8") else 32  # row-slots per thread, both sets
+        # row-slots per thread, both sets (F2 also 32 + 32: 16384 rows per table)
+        rts = (16,) if fname in ("f7", "f5", "gf8", "z8") else (32, 64) if fname == "f2" else (32,)
+        for splits, rt in [(sp, r) for sp in (1, 2, 5, -1) for r in rts]:
             m4rm_mod.set_plan_override(rt, splits, 6, 256)
             try:
                 p = m4rm_mod.plan(fname, m, l, n)
@@ -203,7 +204,7 @@ def test_tmem_accumulator_variant(fname):
                 continue
             assert p["rows_per_cta"] == 256 * rt and p["schedule"].startswith("warp-specialized (4 builder warps, TMEM")
             C = gpu_multiply(fname, A, B)
-            assert np.array_equal(C.planes_numpy(), want), (m, l, n, splits)
+            assert np.array_equal(C.planes_numpy(), want), (m, l, n, splits, rt)
             ran += 1
     m4rm_mod.set_plan_override()
     assert ran >= 12
