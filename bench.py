@@ -297,6 +297,38 @@ def run_config(cfg, args, world, rank, device, peaks, e2e=False):
     return out
 
 
+def run_next_rows(args, device, n=8192):
+    """SURVEY.md 8(f) rows beside the BASELINE configs: the other rings of the same kernel family
+    (GF(8) direct, Z8, Z4, F2) at n^3, bench-style steps (L2 flushed, events per step)."""
+    import torch
+    import paper_0901_1413_b200 as sg
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    params = sg.M4rmParams(8)
+    steps = max(3, min(args.steps, 5))
+    for field in ("gf8", "z8", "z4", "f2"):
+        f, A, B = make_inputs(field, n, n, n, 0, device, True)
+        C = sg.BitslicedMatrix.zero(f, n, n, device=device)
+        for _ in range(3):
+            sg.m4rm_multiply(A, B, params, out=C)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record()
+            sg.m4rm_multiply(A, B, params, out=C)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+        p = sg.plan(f, n, n, n, 8)
+        out[f"{field} {n}x{n}x{n} k=8"] = {"value": float(n) ** 3 / (ms * 1e-3), "ms_per_step": ms, "steps": steps,
+                                          "plan": {k: p[k] for k in ("rows_per_cta", "splits", "ctas", "schedule")}}
+        del A, B, C
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_pack_unpack(device, field="f3", m=16384, n=32768, reps=5):
     """HBM roofline of the pack / unpack kernels (dense uint8 residues <-> bit planes) on a matrix
     larger than L2: algorithmic bytes = m n (1 + R/8) per call, against MEASURED_PEAKS.json."""
@@ -661,6 +693,7 @@ def main():
                                   "achieved_muladds_per_s": r["roofline"]["achieved_muladds_per_s"],
                                   "plan": r["plan"], "clocks": r["clocks"]}
     pack_unpack = run_pack_unpack(device) if not args.no_per_config else None
+    next_rows = run_next_rows(args, device) if (world == 1 and not args.no_per_config) else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -701,7 +734,8 @@ def main():
                 "step_breakdown_ms": {"index_prepass": res["transpose_ms"], "m4rm": res["roofline"]["kernel_ms"],
                                       "reduce": res["reduce_ms"],
                                       "note": "events around each launch (serialised, sg_set_timing)"},
-                "peaks_probe": peaks, "per_config": per_config, "pack_unpack": pack_unpack}
+                "peaks_probe": peaks, "per_config": per_config, "pack_unpack": pack_unpack,
+                "next_rows": next_rows}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
