@@ -39,13 +39,29 @@ __device__ __forceinline__ u32 spread_nibble(u32 nib) { return (nib * 0x00204081
 // Pack / unpack: thread (blockIdx.x * 256 + threadIdx.x) owns 32-bit plane word w of every
 // row blockIdx.y, blockIdx.y + gridDim.y, ... (2-D grid: no 64-bit index division), two rows per
 // iteration with both rows' loads issued first.  Field-templated (constant plane count).
+// 256-bit streaming global accesses (sm_100: ld / st .v8.b32): a lane's 32 dense bytes in one
+// request, so a warp's load covers 1024 contiguous bytes with every 32-byte sector asked for once
+// (two LDG.128 per lane ask for each sector twice).  The address must be 32-byte aligned.
+__device__ __forceinline__ void ldcs256(const void* p, u32 (&x)[8]) {
+  asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void stcs256(void* p, const u32 (&x)[8]) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(x[0]), "r"(x[1]), "r"(x[2]),
+               "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7])
+               : "memory");
+}
+
 template <int F>
 __device__ __forceinline__ void pack_word(const uint8_t* __restrict__ src, bool full, int64_t c0, int64_t n,
                                           u32 (&p)[3], bool& bad) {
   constexpr int R = F == F2 ? 1 : (F == F5 || F == F7 || F == GF8 || F == Z8) ? 3 : 2;
   constexpr u32 order = F == F2 ? 2 : F == F3 ? 3 : F == F5 ? 5 : F == F7 ? 7 : (F == GF4 || F == Z4) ? 4 : 8;
   u32 x[8];
-  if (full) {
+  if (full && (reinterpret_cast<uintptr_t>(src) & 31) == 0) {
+    ldcs256(src, x);
+  } else if (full) {
     const uint4 a = __ldcs(reinterpret_cast<const uint4*>(src)), b = __ldcs(reinterpret_cast<const uint4*>(src) + 1);
     x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
   } else {
@@ -150,7 +166,9 @@ __global__ void __launch_bounds__(256) unpack_kernel(const u32* __restrict__ pla
       u32 x[8];
       unpack_word<F>(h ? p2 : p1, x, bad);
       uint8_t* dst = dense + r * ld + c0;
-      if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 31) == 0)) {
+        stcs256(dst, x);
+      } else if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
         __stcs(reinterpret_cast<uint4*>(dst), make_uint4(x[0], x[1], x[2], x[3]));
         __stcs(reinterpret_cast<uint4*>(dst) + 1, make_uint4(x[4], x[5], x[6], x[7]));
       } else {
