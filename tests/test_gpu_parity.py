@@ -237,6 +237,42 @@ def test_streamk_forced(fname):
     assert ran >= 12
 
 
+@pytest.mark.parametrize("fname", ["f3", "f5", "gf4", "f2"])
+def test_streamk_hybrid_whole_tile_waves(fname):
+    """Stream-K with at least one tile per CTA: the leading whole waves go tile by tile (CTA c:
+    tiles c, c + G, ...) and only the last partial wave is cut into unit ranges, with the
+    reduction kernel offset to the first stream-K tile.  Tile counts just above G, far above it,
+    and an exact multiple of G (empty stream-K tail); bit-identical to the oracle."""
+    hybrid = 0
+    for (m, l, n) in [(2048, 256, 4096), (4500, 96, 5000), (9000, 40, 2000), (1200, 130, 16384)]:
+        A = oracle.random_dense(fname, m, l, m + 5)
+        B = oracle.random_dense(fname, l, n, n + 6)
+        want = expect(fname, A, B)
+        for rt, pipe in ((1, 0), (1, 1), (2, 0), (4, 2), (8, 2)):
+            m4rm_mod.set_plan_override(rt, -1, pipe, 256)
+            try:
+                p = m4rm_mod.plan(fname, m, l, n)
+            except RuntimeError as e:
+                assert "no compiled" in str(e)
+                continue
+            tiles = -(-m // p["rows_per_cta"]) * -(-n // 128)
+            hybrid += tiles >= p["ctas"]
+            C = gpu_multiply(fname, A, B)
+            assert np.array_equal(C.planes_numpy(), want), (fname, m, l, n, rt, pipe, tiles, p["ctas"])
+    # an exact multiple of the CTA count: every tile goes whole, the stream-K tail is empty
+    m4rm_mod.set_plan_override(1, -1, 0, 256)
+    G = m4rm_mod.plan(fname, 2048, 256, 4096)["ctas"]
+    m, l, n = 256 * 2, 72, 128 * G
+    A = oracle.random_dense(fname, m, l, 31)
+    B = oracle.random_dense(fname, l, n, 32)
+    p = m4rm_mod.plan(fname, m, l, n)
+    assert p["splits"] == -1 and 2 * (n // 128) == 2 * p["ctas"]
+    C = gpu_multiply(fname, A, B)
+    assert np.array_equal(C.planes_numpy(), expect(fname, A, B))
+    m4rm_mod.set_plan_override()
+    assert hybrid >= 4
+
+
 @pytest.mark.parametrize("fname", list(FIELDS))
 def test_general_k_pipelined_straddle(fname):
     """k = 5 (blocks straddle 32-bit words) through the pipelined schedule."""
