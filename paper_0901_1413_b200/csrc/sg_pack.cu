@@ -59,11 +59,37 @@ __device__ __forceinline__ void pack_word(const uint8_t* __restrict__ src, bool 
   constexpr int R = F == F2 ? 1 : (F == F5 || F == F7 || F == GF8 || F == Z8) ? 3 : 2;
   constexpr u32 order = F == F2 ? 2 : F == F3 ? 3 : F == F5 ? 5 : F == F7 ? 7 : (F == GF4 || F == Z4) ? 4 : 8;
   u32 x[8];
-  if (full && (reinterpret_cast<uintptr_t>(src) & 31) == 0) {
+  // a full word's 32 bytes by the widest accesses the row's alignment allows (rows of a ragged
+  // matrix start at any byte), a partial last word byte by byte
+  const uintptr_t al = reinterpret_cast<uintptr_t>(src);
+  if (full && (al & 31) == 0) {
     ldcs256(src, x);
-  } else if (full) {
+  } else if (full && (al & 15) == 0) {
     const uint4 a = __ldcs(reinterpret_cast<const uint4*>(src)), b = __ldcs(reinterpret_cast<const uint4*>(src) + 1);
     x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else if (full && (al & 7) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint2 a = __ldcs(reinterpret_cast<const uint2*>(src) + q);
+      x[2 * q] = a.x; x[2 * q + 1] = a.y;
+    }
+  } else if (full && (al & 3) == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = __ldcs(reinterpret_cast<const u32*>(src) + q);
+  } else if (full) {
+    // an odd row start: the seven aligned words inside the 32 bytes, the 4 - a head and a tail
+    // bytes one by one (nothing outside this thread's columns is read), funnel-shifted into place
+    const int a = (int)(al & 3);  // 1..3
+    const u32* base = reinterpret_cast<const u32*>(al - a);
+    u32 y[9];
+    y[0] = 0u;
+    for (int c = 0; c < 4 - a; ++c) y[0] |= (u32)src[c] << (8 * (a + c));
+#pragma unroll
+    for (int j = 1; j < 8; ++j) y[j] = __ldcs(base + j);
+    y[8] = 0u;
+    for (int c = 0; c < a; ++c) y[8] |= (u32)src[32 - a + c] << (8 * c);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = __funnelshift_r(y[q], y[q + 1], 8 * a);
   } else {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -76,15 +102,33 @@ __device__ __forceinline__ void pack_word(const uint8_t* __restrict__ src, bool 
       x[q] = v;
     }
   }
-  p[0] = p[1] = p[2] = 0u;
+  // Gather bit b of the 32 bytes into raw plane I[b]: (x & 0x01010101 << b) * 0x01020408 puts byte
+  // i's bit at 24 + b + i (the 16 partial products fall on distinct positions, the rest below
+  // 20 + b or past bit 31), one shift moves the nibble to 4q.  The range check and F3's value ->
+  // pattern map work on whole plane words afterwards (32 columns per instruction).
+  constexpr int NB = F == F2 ? 1 : (F == F3 || F == GF4 || F == Z4) ? 2 : 3;  // input bits per residue
+  u32 I[3] = {0u, 0u, 0u};
+  u32 any = 0u;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    u32 v = x[q];
-    bad |= __vcmpgeu4(v, 0x01010101u * order) != 0u;
-    if constexpr (F == F3) v = ((v | (v >> 1)) & 0x01010101u) | (v & 0x02020202u);  // 1->01, 2->11
-    p[0] |= gather_bit(v, 0) << (4 * q);
-    if constexpr (R > 1) p[1] |= gather_bit(v, 1) << (4 * q);
-    if constexpr (R > 2) p[2] |= gather_bit(v, 2) << (4 * q);
+    any |= x[q];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const u32 t = (x[q] & (0x01010101u << b)) * 0x01020408u;
+      const int sh = 24 + b - 4 * q;
+      I[b] |= (sh >= 0 ? t >> sh : t << -sh) & (0xFu << (4 * q));
+    }
+  }
+  bad |= (any & ~(((1u << NB) - 1u) * 0x01010101u)) != 0u;  // a byte >= 2^NB
+  if constexpr (F == F3) {
+    bad |= (I[0] & I[1]) != 0u;  // the residue 3
+    p[0] = I[0] | I[1];          // 1 -> 01, 2 -> 11 (fields.py:88-101)
+    p[1] = I[1];
+    p[2] = 0u;
+  } else {
+    if constexpr (order == 5) bad |= (I[2] & (I[1] | I[0])) != 0u;  // 5, 6, 7
+    if constexpr (order == 7) bad |= (I[0] & I[1] & I[2]) != 0u;    // 7
+    p[0] = I[0]; p[1] = I[1]; p[2] = I[2];
   }
 }
 
@@ -110,10 +154,10 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ d
     const int64_t row2 = row + step;
     const uint8_t* s1 = dense + row * ld + c0;
     const uint8_t* s2 = dense + row2 * ld + c0;
-    const bool al = c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(s1) & 15) == 0) && (ld & 15) == 0;
+    const bool full = c0 + 32 <= n;
     u32 p1[3], p2[3];
-    pack_word<F>(s1, al, c0, n, p1, bad);
-    if (row2 < m) pack_word<F>(s2, al, c0, n, p2, bad);
+    pack_word<F>(s1, full, c0, n, p1, bad);
+    if (row2 < m) pack_word<F>(s2, full, c0, n, p2, bad);
 #pragma unroll
     for (int d = 0; d < R; ++d) {
       __stcs(planes + ((int64_t)d * m + row) * wc32 + w, p1[d]);
@@ -124,22 +168,20 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ d
 }
 
 template <int F>
-__device__ __forceinline__ void unpack_word(const u32 (&p)[3], u32 (&x)[8], bool& bad) {
+__device__ __forceinline__ void unpack_word(const u32 (&pin)[3], u32 (&x)[8], bool& bad) {
+  // canonical patterns first, on whole plane words (32 columns per instruction): F5's 5, 6, 7 and
+  // F7's 7 are redundant encodings of 0, 1, 2 and 0 (_core_py.py:143-148, 171-175)
+  u32 p[3] = {pin[0], pin[1], pin[2]};
+  if constexpr (F == F5) f5_reduce(p[0], p[1], p[2]);
+  if constexpr (F == F7) f7_reduce(p[0], p[1], p[2]);
+  if constexpr (F == F3) bad |= (p[1] & ~p[0]) != 0u;  // sign without unit: illegal (fields.py:88-101)
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const u32 b0 = spread_nibble((p[0] >> (4 * q)) & 0xFu);
     const u32 b1 = spread_nibble((p[1] >> (4 * q)) & 0xFu);
     const u32 b2 = spread_nibble((p[2] >> (4 * q)) & 0xFu);
-    u32 v;
-    if constexpr (F == F3) {
-      bad |= (b1 & ~b0) != 0u;  // sign without unit: illegal (fields.py:88-101)
-      v = b0 + b1;
-    } else {
-      v = b0 | (b1 << 1) | (b2 << 2);
-      if constexpr (F == F5) v = __vsub4(v, __vcmpgeu4(v, 0x05050505u) & 0x05050505u);
-      if constexpr (F == F7) v = __vsub4(v, __vcmpeq4(v, 0x07070707u) & 0x07070707u);
-    }
-    x[q] = v;
+    if constexpr (F == F3) x[q] = b0 + b1;
+    else x[q] = b0 | (b1 << 1) | (b2 << 2);
   }
 }
 
@@ -171,6 +213,21 @@ __global__ void __launch_bounds__(256) unpack_kernel(const u32* __restrict__ pla
       } else if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
         __stcs(reinterpret_cast<uint4*>(dst), make_uint4(x[0], x[1], x[2], x[3]));
         __stcs(reinterpret_cast<uint4*>(dst) + 1, make_uint4(x[4], x[5], x[6], x[7]));
+      } else if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) __stcs(reinterpret_cast<uint2*>(dst) + q, make_uint2(x[2 * q], x[2 * q + 1]));
+      } else if (c0 + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) __stcs(reinterpret_cast<u32*>(dst) + q, x[q]);
+      } else if (c0 + 32 <= n) {
+        // an odd row start: a head bytes up to the next 4-byte boundary, seven aligned words
+        // assembled by funnel shifts, then the 4 - a tail bytes
+        const int a = (int)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);  // 1..3 here
+        for (int c = 0; c < a; ++c) dst[c] = (uint8_t)(x[0] >> (8 * c));
+#pragma unroll
+        for (int j = 0; j < 7; ++j)
+          __stcs(reinterpret_cast<u32*>(dst + a) + j, __funnelshift_r(x[j], x[j + 1], 8 * a));
+        for (int c = a + 28; c < 32; ++c) dst[c] = (uint8_t)(x[7] >> (8 * (c & 3)));
       } else {
         for (int c = 0; c < 32 && c0 + c < n; ++c) dst[c] = (uint8_t)(x[c >> 2] >> (8 * (c & 3)));
       }
