@@ -614,13 +614,23 @@ def test_no_writes_outside_c():
     from paper_0901_1413_b200 import _lib
     L = _lib.load()
     guard = 4096
-    for fname, (m, l, n) in (("f3", (77, 301, 130)), ("f7", (513, 257, 65)), ("gf4", (1, 9, 1)), ("f5", (300, 1000, 700))):
+    cases = [("f3", (77, 301, 130), None), ("f7", (513, 257, 65), None), ("gf4", (1, 9, 1), None),
+             ("f5", (300, 1000, 700), None)]
+    # the tensor-memory variants (row-slots per thread, both sets), split-K and stream-K, on rows
+    # that leave their 4096- / 8192- / 16384-row tiles mostly empty or ragged; and the stream-K
+    # hybrid (more tiles than CTAs: whole-tile waves plus a stream-K tail)
+    for fname, rt in (("f3", 32), ("gf4", 32), ("z4", 32), ("f2", 32), ("f2", 64), ("f5", 16), ("f7", 16), ("gf8", 16),
+                      ("z8", 16)):
+        cases += [(fname, (4099, 130, 200), ((rt, 6, 1), (rt, 6, 3), (rt, 6, -1))),
+                  (fname, (8200, 72, 129), ((rt, 6, -1),))]
+    cases += [("f3", (2300, 64, 4100), ((1, 0, -1), (2, 1, -1))), ("f5", (2300, 64, 4100), ((1, 0, -1), (4, 2, -1)))]
+    for fname, (m, l, n), plans in cases:
         f = FIELDS[fname]
         A = sg.BitslicedMatrix.from_dense(f, oracle.random_dense(fname, m, l, 1))
         B = sg.BitslicedMatrix.from_dense(f, oracle.random_dense(fname, l, n, 2))
         want = expect(fname, oracle.unpack(fname, A.planes_numpy(), l), oracle.unpack(fname, B.planes_numpy(), n))
         words = f.bits * m * ((n + 63) // 64)
-        for rt, sched, splits in ((1, 0, 1), (2, 1, 3), (4, 2, 2), (8, 2, 1)):
+        for rt, sched, splits in (plans or ((1, 0, 1), (2, 1, 3), (4, 2, 2), (8, 2, 1))):
             m4rm_mod.set_plan_override(rt, splits, sched, 256)
             buf = torch.full((words + 2 * guard,), 0x5A5A5A5A5A5A5A5A, dtype=torch.int64, device="cuda")
             try:
