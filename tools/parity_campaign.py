@@ -14,7 +14,9 @@ import torch  # noqa: E402
 import paper_0901_1413_b200 as sg  # noqa: E402
 from paper_0901_1413_b200 import m4rm as M  # noqa: E402
 
-FIELDS = {"f3": (sg.F3, 3), "f5": (sg.F5, 5), "f7": (sg.F7, 7), "gf4": (sg.GF4, None), "f2": (sg.F2, 2)}
+FIELDS = {"f3": (sg.F3, 3), "f5": (sg.F5, 5), "f7": (sg.F7, 7), "gf4": (sg.GF4, None), "f2": (sg.F2, 2),
+          "gf8": (sg.GF8, None), "z4": (sg.Z4, 4), "z8": (sg.Z8, 8)}
+TM_RT = {"f3": 32, "gf4": 32, "z4": 32, "f2": 32, "f5": 16, "f7": 16, "gf8": 16, "z8": 16}  # schedule-6 row-slots
 
 
 def exact(fname, A, B):
@@ -25,6 +27,18 @@ def exact(fname, A, B):
         c0 = torch.remainder(a0 @ b0 + p11, 2)
         c1 = torch.remainder(a0 @ b1 + a1 @ b0 + p11, 2)
         return (c0.to(torch.uint8) | (c1.to(torch.uint8) << 1))
+    if fname == "gf8":  # F2[x] / (x^3 + x + 1): x^3 = x + 1, x^4 = x^2 + x
+        a = [((A >> i) & 1).float() for i in range(3)]
+        b = [((B >> i) & 1).float() for i in range(3)]
+        d = [None] * 5
+        for i in range(3):
+            for j in range(3):
+                t = a[i] @ b[j]
+                d[i + j] = t if d[i + j] is None else d[i + j] + t
+        c0 = torch.remainder(d[0] + d[3], 2)
+        c1 = torch.remainder(d[1] + d[3] + d[4], 2)
+        c2 = torch.remainder(d[2] + d[4], 2)
+        return c0.to(torch.uint8) | (c1.to(torch.uint8) << 1) | (c2.to(torch.uint8) << 2)
     return torch.remainder(A.float() @ B.float(), FIELDS[fname][1]).to(torch.uint8)
 
 
@@ -43,10 +57,11 @@ def main():
             l = max(1, int(6e10 // (m * n)))
         k = int(rng.choice([8, 8, 8, 8, 5, 3]))
         plan = rng.choice(["auto", "auto", "tm", "ws5", "fused", "fusedp"])
-        ov = {"auto": (0, 0, -1, 0), "tm": (32 if fname in ("f3", "gf4") else 16, int(rng.choice([1, 2, -1])), 6, 256),
+        ov = {"auto": (0, 0, -1, 0),
+              "tm": (64 if fname == "f2" and rng.random() < 0.5 else TM_RT[fname], int(rng.choice([1, 2, -1])), 6, 256),
               "ws5": (16, -1, 5, 256), "fused": (int(rng.choice([1, 2, 4])), int(rng.choice([1, 4, 16])), 10, 256),
               "fusedp": (int(rng.choice([2, 4])), int(rng.choice([1, 4, 16])), 11, 256)}[plan]
-        order = 4 if fname == "gf4" else p
+        order = 4 if fname == "gf4" else 8 if fname == "gf8" else p
         A = torch.randint(0, order, (m, l), dtype=torch.uint8, device=dev)
         B = torch.randint(0, order, (l, n), dtype=torch.uint8, device=dev)
         M.set_plan_override(*ov)
