@@ -64,7 +64,9 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
             if a.is_pinned() and b.is_pinned():  # page-locked in, page-locked out: async copies
                 C = BitslicedMatrix.pinned_zero(field, m, n)
             else:
-                C = BitslicedMatrix.zero(field, m, n, device="cpu")
+                # every word of C (padding lanes included) comes down from the device: no need to
+                # zero 8 R m W bytes of fresh pageable memory first
+                C = BitslicedMatrix(field, m, n, torch.empty((field.bits, m, (n + 63) // 64), dtype=torch.int64))
         else:
             # sg_m4rm_host writes R*m*W words through this pointer: the same checks as on the
             # device, plus host residency (a device pointer is not a host buffer)
