@@ -153,9 +153,11 @@ def _same(A, B):
         raise ValueError("shape mismatch")
 
 
-def poly_reduce(spec: ExtFieldSpec, P):
+def poly_reduce(spec: ExtFieldSpec, P, inplace: bool = False):
     """P0 + x P1 + ... + x^(2n-2) P_(2n-2)  mod  spec.modulus, with add/sub/scalar_mul only
-    (SPEC.md:408-413): x^n = -(m_(n-1) x^(n-1) + ... + m_0), applied from the top down."""
+    (SPEC.md:408-413): x^n = -(m_(n-1) x^(n-1) + ... + m_0), applied from the top down.
+    inplace: the P_i are temporaries the caller owns (distinct device matrices) and may be
+    overwritten -- one launch per subtraction instead of a clone and a launch."""
     n = spec.degree
     P = list(P)
     for top in range(2 * n - 2, n - 1, -1):
@@ -163,25 +165,35 @@ def poly_reduce(spec: ExtFieldSpec, P):
         for j in range(n):
             c = spec.modulus[j]
             if c:
-                P[top - n + j] = P[top - n + j].sub(head.scalar_mul(c) if c != 1 else head)
+                t = head.scalar_mul(c) if c != 1 else head
+                P[top - n + j] = P[top - n + j]._isub(t) if inplace else P[top - n + j].sub(t)
     return P[:n]
+
+
+def _sum(x: BitslicedMatrix, y: BitslicedMatrix) -> BitslicedMatrix:
+    """x + y of two operand coefficient matrices (not owned: out of place).  Over F2 one XOR kernel."""
+    if x.field is F2 and x.device.type == "cuda" and y.device == x.device:
+        return BitslicedMatrix(F2, x.nrows, x.ncols, torch.bitwise_xor(x.planes, y.planes))
+    return x.add(y)
 
 
 def _karatsuba(A: ExtMatrix, B: ExtMatrix, params) -> ExtMatrix:
     global base_multiplies
     mul = lambda x, y: m4rm_multiply(x, y, params)  # noqa: E731
     a, b = A.coeffs, B.coeffs
+    # the products are fresh matrices owned here: the corrections run in place on them
     if A.spec.degree == 2:
         p0, p2 = mul(a[0], b[0]), mul(a[1], b[1])
-        p1 = mul(a[0].add(a[1]), b[0].add(b[1])).sub(p0).sub(p2)
+        p1 = mul(_sum(a[0], a[1]), _sum(b[0], b[1]))._isub(p0)._isub(p2)
         base_multiplies = 3
-        return ExtMatrix(A.spec, poly_reduce(A.spec, [p0, p1, p2]))
+        return ExtMatrix(A.spec, poly_reduce(A.spec, [p0, p1, p2], inplace=True))
     c0, c4, m1 = mul(a[0], b[0]), mul(a[2], b[2]), mul(a[1], b[1])
-    c1 = mul(a[0].add(a[1]), b[0].add(b[1])).sub(c0).sub(m1)
-    c3 = mul(a[2].add(a[1]), b[2].add(b[1])).sub(c4).sub(m1)
-    c2 = mul(a[0].add(a[2]), b[0].add(b[2])).sub(c0).sub(c4).add(m1)
+    c1 = mul(_sum(a[0], a[1]), _sum(b[0], b[1]))._isub(c0)._isub(m1)
+    c3 = mul(_sum(a[2], a[1]), _sum(b[2], b[1]))._isub(c4)._isub(m1)
+    c2 = mul(_sum(a[0], a[2]), _sum(b[0], b[2]))._isub(c0)._isub(c4)._iadd(m1)
     base_multiplies = 6
-    return ExtMatrix(A.spec, poly_reduce(A.spec, [c0, c1, c2, c3, c4]))
+    # (poly_reduce in place: m1 is not among its inputs, the five c_i are distinct)
+    return ExtMatrix(A.spec, poly_reduce(A.spec, [c0, c1, c2, c3, c4], inplace=True))
 
 
 def ext_multiply(A, B, params: M4rmParams = None, method: str = "karatsuba"):

@@ -271,6 +271,33 @@ class BitslicedMatrix:
                                                    tmask, scalar, _lib.current_stream_handle(dst.device)))
         return dst
 
+    def _iplane_op(self, op: str, src: "BitslicedMatrix" = None, scalar: int = 0) -> "BitslicedMatrix":
+        """`_plane_op` in place on a device matrix the caller owns (a temporary of a longer
+        computation: no clone, one launch); host matrices take the out-of-place route."""
+        if self.device.type != "cuda" or not self.planes.is_contiguous():
+            return self._plane_op(op, src, scalar)
+        R = self.field.bits
+        dptr, _k1 = _lib.ptr_array([self.planes[d].data_ptr() for d in range(R)])
+        sptr = None
+        if src is not None:
+            s = src.planes.to(self.device).contiguous()
+            sptr, _k2 = _lib.ptr_array([s[d].data_ptr() for d in range(R)])
+        rem = self.ncols % 64
+        tmask = ((1 << rem) - 1) if rem else (1 << 64) - 1
+        if self.nrows and self.words_per_row:
+            with torch.cuda.device(self.device):
+                _lib.check(_lib.load().sg_plane_op(_lib.OPS[op], dptr, sptr, self.nrows, self.words_per_row,
+                                                   tmask, scalar, _lib.current_stream_handle(self.device)))
+        return self
+
+    def _isub(self, other: "BitslicedMatrix") -> "BitslicedMatrix":
+        self._check_same(other)
+        return self._iplane_op(self._SUB[self.field.name], other)
+
+    def _iadd(self, other: "BitslicedMatrix") -> "BitslicedMatrix":
+        self._check_same(other)
+        return self._iplane_op(self._ADD[self.field.name], other)
+
     _ADD = {"f2": "f2_add", "f3": "f3_add", "f5": "f5_add", "f7": "f7_add", "gf4": "gf4_add", "gf8": "gf8_add",
             "z4": "z4_add", "z8": "z8_add"}
     _SUB = {"f2": "f2_add", "f3": "f3_sub", "f5": "f5_sub", "f7": "f7_sub", "gf4": "gf4_add", "gf8": "gf8_add",
