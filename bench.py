@@ -693,6 +693,10 @@ def main():
                                   "achieved_muladds_per_s": r["roofline"]["achieved_muladds_per_s"],
                                   "plan": r["plan"], "clocks": r["clocks"]}
     pack_unpack = run_pack_unpack(device) if not args.no_per_config else None
+    if pack_unpack is not None:  # a three-plane field beside it (its bit gather is heavier per byte)
+        p5 = run_pack_unpack(device, field="f5", m=16384, n=16384)
+        pack_unpack["f5_16384x16384"] = {k: p5[k] for k in ("pack_ms", "unpack_ms", "pack_gbps", "unpack_gbps",
+                                                             "pack_frac", "unpack_frac", "bytes_per_call")}
     next_rows = run_next_rows(args, device) if (world == 1 and not args.no_per_config) else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
