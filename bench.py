@@ -493,6 +493,23 @@ def run_e2e(f, A, B, m, l, n, args, world, device):
                              "step_ms_median": 1e3 * statistics.median(pts),
                              "operands_page_locked": bool(Ahm.planes.is_pinned() or Bhm.planes.is_pinned()),
                              "path": "m4rm_multiply(BitslicedMatrix over pageable numpy planes) -> sg_m4rm_host"}
+    if world == 1:
+        # the same product through the public Python call on the page-locked operands (C allocated
+        # page-locked by m4rm_multiply, returned as a BitslicedMatrix)
+        Apm, Bpm = sg.BitslicedMatrix(f, m, l, Ah), sg.BitslicedMatrix(f, l, n, Bh)
+        # (warm-up results kept alive together: the page-locked allocator then has the two blocks
+        # the timed loop alternates between; a fresh cudaHostAlloc costs tens of milliseconds)
+        keep = [sg.m4rm_multiply(Apm, Bpm, sg.M4rmParams(8)) for _ in range(3)]
+        del keep
+        qts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            Cp = sg.m4rm_multiply(Apm, Bpm, sg.M4rmParams(8))
+            qts.append(time.perf_counter() - t0)
+        extra["public_api_page_locked"] = {"ms_per_step": 1e3 * statistics.mean(qts), "step_ms_median": 1e3 * statistics.median(qts),
+                                           "step_ms_min": 1e3 * min(qts),
+                                           "verified_vs_device_path": bool(torch.equal(Cp.planes, Ch)),
+                                           "path": "m4rm_multiply(page-locked BitslicedMatrix operands) -> sg_m4rm_host"}
     extra["host_buffers"] = ("page-locked, allocated and written by one thread on one CPU "
                              "(BitslicedMatrix.pin_memory / pinned_zero)")
     return {"value": world * float(m) * l * n / per, "unit": UNIT, "ms_per_step": per * 1e3,

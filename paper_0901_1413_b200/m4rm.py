@@ -62,11 +62,12 @@ def m4rm_multiply(A: BitslicedMatrix, B: BitslicedMatrix, params: M4rmParams = N
         b = B.planes.contiguous()
         if out is None:
             if a.is_pinned() and b.is_pinned():  # page-locked in, page-locked out: async copies
-                C = BitslicedMatrix.pinned_zero(field, m, n)
+                C = BitslicedMatrix.pinned_empty(field, m, n) if m and n and l else BitslicedMatrix.pinned_zero(field, m, n)
             else:
                 # every word of C (padding lanes included) comes down from the device: no need to
                 # zero 8 R m W bytes of fresh pageable memory first
-                C = BitslicedMatrix(field, m, n, torch.empty((field.bits, m, (n + 63) // 64), dtype=torch.int64))
+                alloc = torch.empty if (m and n and l) else torch.zeros  # (an empty product writes nothing)
+                C = BitslicedMatrix(field, m, n, alloc((field.bits, m, (n + 63) // 64), dtype=torch.int64))
         else:
             # sg_m4rm_host writes R*m*W words through this pointer: the same checks as on the
             # device, plus host residency (a device pointer is not a host buffer)

@@ -197,6 +197,14 @@ class BitslicedMatrix:
             t = torch.zeros((field.bits, m, _words(n)), dtype=torch.int64, pin_memory=True)
         return cls(field, m, n, t)
 
+    @classmethod
+    def pinned_empty(cls, field, m: int, n: int) -> "BitslicedMatrix":
+        """An uninitialized page-locked host matrix: the result buffer of a host-buffer product,
+        every word of which (padding lanes included) is copied down from the device."""
+        if isinstance(field, str):
+            field = by_name(field)
+        return cls(field, m, n, torch.empty((field.bits, m, _words(n)), dtype=torch.int64, pin_memory=True))
+
     def planes_numpy(self) -> np.ndarray:
         """The reference-layout planes as a host uint64 array of shape (R, m, W)."""
         return self.planes.cpu().numpy().view(np.uint64)

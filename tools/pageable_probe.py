@@ -21,6 +21,8 @@ An = np.ascontiguousarray(A.planes.cpu().numpy().view(np.uint64))
 Bn = np.ascontiguousarray(B.planes.cpu().numpy().view(np.uint64))
 Ah = sg.BitslicedMatrix.from_planes(f, An, l, device="cpu")
 Bh = sg.BitslicedMatrix.from_planes(f, Bn, n, device="cpu")
+if os.environ.get("PINNED"):  # page-locked operands through the same public call
+    Ah, Bh = Ah.pin_memory(), Bh.pin_memory()
 want = sg.m4rm_multiply(A, B, sg.M4rmParams(8)).planes_numpy()
 for _ in range(3):
     C = sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8))
@@ -30,5 +32,5 @@ for _ in range(30):
     C = sg.m4rm_multiply(Ah, Bh, sg.M4rmParams(8)).planes_numpy()
     ts.append(1e3 * (time.perf_counter() - t0))
 ok = bool(np.array_equal(C, want))
-print(f"{name} STREAM={os.environ.get('SG_HOST_STREAM', '-')} CHUNKS={os.environ.get('SG_HOST_CHUNKS', '-')}: "
+print(f"{name} PINNED={os.environ.get('PINNED', '-')} STREAM={os.environ.get('SG_HOST_STREAM', '-')} CHUNKS={os.environ.get('SG_HOST_CHUNKS', '-')}: "
       f"mean {statistics.mean(ts):.3f} median {statistics.median(ts):.3f} min {min(ts):.3f} max {max(ts):.3f} ms ok={ok}")
