@@ -144,7 +144,10 @@ class BitslicedMatrix:
         target = _dev(device)
         gpu = target if target.type == "cuda" else _dev("cuda")
         _require_cuda(gpu)
-        out = cls.zero(field, m, n, device=gpu)
+        if m and n:  # the pack kernel writes every plane word (padding lanes as zeros): no zero fill first
+            out = cls(field, m, n, torch.empty((field.bits, m, _words(n)), dtype=torch.int64, device=gpu))
+        else:
+            out = cls.zero(field, m, n, device=gpu)
         if m and n:
             dd = dense.to(gpu, non_blocking=False).contiguous()
             with torch.cuda.device(gpu):
